@@ -1,0 +1,164 @@
+/*
+ * oracle.c -- plain CPU oracle for the HP-NFFT adjoint path (TEST INFRASTRUCTURE ONLY).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline, --impl reference)
+ * may load this library.  It shares no code, header, table or constant generator with
+ * the CUDA path (paper_2001_01583_b200/csrc/).
+ *
+ * O1  oracle_ndft    : direct NDFT, Eq. (5) of PAPER.md:37 (§1),
+ *                      fhat(k) = sum_{j<M} f_j exp(-2 pi i k.x_j), k in I_N,
+ *                      Kahan-compensated complex accumulation in float64, one output at a
+ *                      time (OpenMP over independent outputs only; every sum is serial).
+ * O2a oracle_spread  : the "Spreading" step of CUNFFT (§2 Fig. 1 and
+ *                      PAPER.md:162, §3): g(l) += f_j * prod_t Phi(u_t - l_t) over the
+ *                      truncated neighbourhood J(x_j), l taken modulo n (periodic grid).
+ *                      Plain serial loop over points, taps in natural order.
+ *
+ * Conventions (readings Q1-Q10):
+ *   u_t = n_t x_t (exact: n_t a power of two), c_t = floor(u_t), t_t = u_t - c_t (exact),
+ *   taps l_t = c_t - m + 1 + i, i = 0..2m-1, u_t - l_t = t_t + (m - 1 - i).
+ *   Strict truncation |u - l| < m: all taps are inside except i = 2m-1 when t_t == 0
+ *   (then u - l = -m exactly).  Kaiser-Bessel b = pi(2 - 1/sigma); Gaussian
+ *   b = 2 sigma/(2 sigma - 1) m / pi (see oracle/windows.py for the formulas).
+ */
+#define _GNU_SOURCE
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_KB 0
+#define ORACLE_GAUSS 1
+
+static const double PI = 3.14159265358979323846264338327950288;
+
+/* exp(-2 pi i k x) with the argument k*x reduced exactly: k*x = p + e (fma gives the
+ * exact product error e), r = (p - nearbyint(p)) + e, phase = exp(-2 pi i r). */
+static inline void phase(int64_t k, double x, double* re, double* im) {
+  double kd = (double)k;
+  double p = kd * x;
+  double e = fma(kd, x, -p);
+  double r = (p - nearbyint(p)) + e;
+  double s, c;
+  sincos(2.0 * PI * r, &s, &c);
+  *re = c;
+  *im = -s;
+}
+
+/* O1: direct NDFT.  x: [M][d], f: [M][2] (re,im), ks: [K][d] integer frequencies
+ * (or NULL: all of I_N in row-major order, last dimension fastest, index k_t + N_t/2).
+ * out: [K][2].  Returns 0 on success. */
+int oracle_ndft(int d, const int64_t* N, int64_t M, const double* x, const double* f,
+                int64_t K, const int64_t* ks, double* out, int nthreads) {
+  if (d < 1 || d > 3) return -1;
+  int64_t total = 1;
+  for (int t = 0; t < d; ++t) total *= N[t];
+  if (ks == NULL) K = total;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t q = 0; q < K; ++q) {
+    int64_t k[3] = {0, 0, 0};
+    if (ks) {
+      for (int t = 0; t < d; ++t) k[t] = ks[q * d + t];
+    } else {
+      int64_t r = q;
+      for (int t = d - 1; t >= 0; --t) {
+        k[t] = (r % N[t]) - N[t] / 2;
+        r /= N[t];
+      }
+    }
+    double sr = 0.0, si = 0.0, cr = 0.0, ci = 0.0; /* Kahan sums and compensations */
+    for (int64_t j = 0; j < M; ++j) {
+      double er = 1.0, ei = 0.0;
+      for (int t = 0; t < d; ++t) {
+        double pr, pi_;
+        phase(k[t], x[j * d + t], &pr, &pi_);
+        double nr = er * pr - ei * pi_;
+        double ni = er * pi_ + ei * pr;
+        er = nr;
+        ei = ni;
+      }
+      double fr = f[2 * j], fi = f[2 * j + 1];
+      double vr = fr * er - fi * ei;
+      double vi = fr * ei + fi * er;
+      double y, tt;
+      y = vr - cr; tt = sr + y; cr = (tt - sr) - y; sr = tt;
+      y = vi - ci; tt = si + y; ci = (tt - si) - y; si = tt;
+    }
+    out[2 * q] = sr;
+    out[2 * q + 1] = si;
+  }
+  return 0;
+}
+
+/* Window Phi(a) for a strictly inside the support (|a| < m). */
+static inline double window_value(double a, int m, double sigma, int window) {
+  if (window == ORACLE_KB) {
+    double b = PI * (2.0 - 1.0 / sigma);
+    double s = sqrt((double)m * (double)m - a * a);
+    return sinh(b * s) / (PI * s);
+  } else {
+    double b = 2.0 * sigma / (2.0 * sigma - 1.0) * (double)m / PI;
+    return exp(-a * a / b) / sqrt(PI * b);
+  }
+}
+
+/* O2a: spread.  n: grid sizes [3]; x: [M][3]; f: [M][2]; g: [n0][n1][n2][2], accumulated
+ * into (caller zeroes it).  Returns 0 on success. */
+int oracle_spread(const int64_t* n, int m, double sigma, int window, int64_t M,
+                  const double* x, const double* f, double* g) {
+  if (m < 1 || m > 16) return -1;
+  const int taps = 2 * m;
+  double w[3][32];
+  int64_t idx[3][32];
+  for (int64_t j = 0; j < M; ++j) {
+    for (int t = 0; t < 3; ++t) {
+      double u = (double)n[t] * x[j * 3 + t];
+      double c = floor(u);
+      double tt = u - c;
+      int64_t ci = (int64_t)c;
+      for (int i = 0; i < taps; ++i) {
+        int64_t l = ci - m + 1 + i;
+        /* |u - l| < m  <=>  not (i == 2m-1 and tt == 0) */
+        int inside = !(i == taps - 1 && tt == 0.0);
+        w[t][i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
+        int64_t lm = l % n[t];
+        if (lm < 0) lm += n[t];
+        idx[t][i] = lm;
+      }
+    }
+    const double fr = f[2 * j], fi = f[2 * j + 1];
+    for (int i0 = 0; i0 < taps; ++i0) {
+      for (int i1 = 0; i1 < taps; ++i1) {
+        for (int i2 = 0; i2 < taps; ++i2) {
+          double wt = w[0][i0] * w[1][i1] * w[2][i2];
+          int64_t off = ((idx[0][i0] * n[1] + idx[1][i1]) * n[2] + idx[2][i2]) * 2;
+          g[off] += fr * wt;
+          g[off + 1] += fi * wt;
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* 1-D weights of one coordinate (exposed for the window/tap pins in tests). */
+int oracle_taps(int64_t n, int m, double sigma, int window, double x, double* w, int64_t* idx) {
+  double u = (double)n * x;
+  double c = floor(u);
+  double tt = u - c;
+  int64_t ci = (int64_t)c;
+  for (int i = 0; i < 2 * m; ++i) {
+    int inside = !(i == 2 * m - 1 && tt == 0.0);
+    w[i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
+    int64_t lm = (ci - m + 1 + i) % n;
+    if (lm < 0) lm += n;
+    idx[i] = lm;
+  }
+  return 0;
+}
