@@ -1,0 +1,136 @@
+/*
+ * hpnfft.h -- C ABI of the B200-native adjoint NFFT (HP-NFFT hot path, arXiv 2001.01583).
+ *
+ * Operation (§1 Eq. 5):
+ *     fhat(k) = sum_{j=0}^{M-1} f_j * exp(-2 pi i k.x_j),   k in I_N,
+ *     I_N = { k in Z^3 : -N_t/2 <= k_t < N_t/2 }            (§1)
+ * computed by the CUNFFT gridding scheme (§2 Fig. 1; Alg. 2):
+ * bin-sort the points, spread each f_j with a Kaiser-Bessel (or Gaussian) window of 2m taps per
+ * dimension onto the sigma-oversampled grid I_n (n_t = sigma N_t), FFT that grid, divide by the
+ * window's Fourier weights c_k and crop to I_N ("Scaling", §3).
+ * The paper's "NDFT" direction (Eq. 5, minus sign) is called "adjoint" here.
+ *
+ * Conventions (readings Q1-Q10):
+ *   - points x_j in [-0.5, 0.5]^3 (Pi^3); x = 0.5 and x = -0.5 give the same result;
+ *   - u_t = n_t x_t, taps l_t = floor(u_t) - m + 1 .. floor(u_t) + m (strict |u - l| < m),
+ *     grid offset l_t mod n_t;
+ *   - Kaiser-Bessel: b = pi (2 - 1/sigma), Phi(u) = sinh(b sqrt(m^2-u^2)) / (pi sqrt(m^2-u^2)),
+ *     c_k = I0(m sqrt(b^2 - (2 pi k/n)^2)); Gaussian: b = 2 sigma/(2 sigma-1) m/pi,
+ *     Phi(u) = exp(-u^2/b)/sqrt(pi b), c_k = exp(-b pi^2 k^2/n^2);
+ *   - output fhat is row-major [N0][N1][N2] (last dimension fastest) at index k_t + N_t/2,
+ *     complex128 stored as interleaved (re, im) doubles; no normalisation.
+ *
+ * Memory and ownership: unless stated otherwise every data pointer is a CUDA DEVICE pointer
+ * (cudaMalloc / torch CUDA tensor memory) that the caller owns.  Calls are asynchronous on the
+ * plan's stream (stream order is the only synchronisation): a buffer passed to a call must stay
+ * valid until the stream has passed the call.  The plan owns its workspace (grid, FFT buffers,
+ * bins, permutation, tables), allocated by hpnfft_plan and released by hpnfft_destroy.
+ *
+ * Errors: every function returns HPNFFT_OK (0) or a negative status; hpnfft_last_error() gives
+ * a thread-local text for the last failure.  Argument validation is synchronous and happens
+ * before any launch; a failed hpnfft_plan leaves *out == NULL.  After HPNFFT_E_CUDA/E_NCCL the
+ * plan is sticky-failed: every later call except hpnfft_destroy returns HPNFFT_E_STATE.
+ * Threading: one host thread per plan at a time; distinct plans are independent.
+ */
+#ifndef HPNFFT_H_
+#define HPNFFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hpnfft_plan_s* hpnfft_plan_t;
+
+enum { HPNFFT_WINDOW_KAISER_BESSEL = 0, HPNFFT_WINDOW_GAUSSIAN = 1 };
+
+enum {
+  HPNFFT_OK = 0,
+  HPNFFT_E_INVALID = -1,            /* malformed argument (odd N_t, sigma <= 1, NULL, ...) */
+  HPNFFT_E_UNSUPPORTED = -2,        /* valid but not implemented (d != 3, n_t not 2^k, m range) */
+  HPNFFT_E_RANGE = -3,              /* a point coordinate outside [-0.5, 0.5] (or NaN) */
+  HPNFFT_E_NOMEM = -4,              /* device allocation failed */
+  HPNFFT_E_CUDA = -5,               /* CUDA runtime/launch error (plan becomes sticky-failed) */
+  HPNFFT_E_NCCL = -6,               /* reserved for the NCCL layer */
+  HPNFFT_E_STATE = -7,              /* call out of order (adjoint before set_points) or failed plan */
+  HPNFFT_E_DEGENERATE_WINDOW = -8   /* a Fourier weight c_k is not finite or below 1e-300 */
+};
+
+/* Spread kernel selection (for measurement; HPNFFT_SPREAD_AUTO is the product default). */
+enum { HPNFFT_SPREAD_AUTO = 0, HPNFFT_SPREAD_ATOMIC = 1, HPNFFT_SPREAD_SWEEP = 2 };
+
+/*
+ * Create a plan (A0 in SURVEY.md §8(a)): validates, allocates the workspace and builds the
+ * per-dimension deconvolution tables 1/c_k, the FFT twiddles and the window tap polynomials
+ * in device kernels.
+ *   out    : receives the plan handle (host pointer to a handle).
+ *   d      : dimension; only d = 3 is supported (else HPNFFT_E_UNSUPPORTED).
+ *   N      : HOST array of d bandwidths N_t, each even and >= 2, else E_INVALID.
+ *   M      : number of points this plan will be given (0 <= M < 2^31), else E_INVALID.
+ *   m      : cut-off, 2 <= m <= 8 (PAPER.md:266 uses 1..15; GPU kernels are instantiated for
+ *            2..8), else E_UNSUPPORTED.
+ *   sigma  : oversampling factor > 1; n_t = sigma N_t must be an integer power of two >= 2m
+ *            (PAPER.md:266 uses sigma = 2), else E_UNSUPPORTED (E_INVALID for sigma <= 1).
+ *   window : HPNFFT_WINDOW_KAISER_BESSEL or HPNFFT_WINDOW_GAUSSIAN.
+ *   stream : cudaStream_t (as void*) all work is enqueued on; NULL = legacy default stream.
+ */
+int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma,
+                int window, void* stream);
+
+/*
+ * Bin-sort the points (A1 keys + A2 counting sort).
+ *   x : DEVICE [M][3] float64 row-major, each coordinate in [-0.5, 0.5].  Read only; the plan
+ *       keeps its own sorted copy, so x may be released once the stream passes this call.
+ * Out-of-range or NaN coordinates return HPNFFT_E_RANGE; this is detected with a device flag
+ * that is read back once at the end of the call (the only host synchronisation of the path).
+ */
+int hpnfft_set_points(hpnfft_plan_t p, const double* x);
+
+/*
+ * Transform (A3 window, A4 spread, A5 FFT, A6 deconvolve + crop; Alg. 2).
+ *   f    : DEVICE [M][2] float64 (re, im) values in the ORIGINAL point order of set_points.
+ *   fhat : DEVICE [N0*N1*N2][2] float64 output, fully overwritten (no accumulation).
+ * Requires a prior successful hpnfft_set_points (else HPNFFT_E_STATE).  Asynchronous.
+ */
+int hpnfft_adjoint(hpnfft_plan_t p, const double* f, double* fhat);
+
+/* Release the plan and its workspace (synchronises the plan's stream).  NULL is a no-op. */
+int hpnfft_destroy(hpnfft_plan_t p);
+
+/* Thread-local text of the last failure (never NULL). */
+const char* hpnfft_last_error(void);
+
+/* Bytes of device workspace the plan owns (host query, no synchronisation). */
+size_t hpnfft_workspace_bytes(hpnfft_plan_t p);
+
+/* Change the stream later calls enqueue on (cudaStream_t as void*). */
+int hpnfft_set_stream(hpnfft_plan_t p, void* stream);
+
+/* Select the spread kernel (HPNFFT_SPREAD_*); AUTO picks the sweep kernel when the grid allows. */
+int hpnfft_set_spread_method(hpnfft_plan_t p, int method);
+
+/*
+ * Number of kernel launches the last hpnfft_set_points + hpnfft_adjoint enqueued (host counter;
+ * used by bench.py for "gpu_launches").
+ */
+int64_t hpnfft_launch_count(hpnfft_plan_t p);
+
+/*
+ * Per-stage device timing (CUDA events on the plan's stream) of the most recent calls, in ms:
+ * out[0] keys+histogram, out[1] scan, out[2] scatter, out[3] spread, out[4] FFT pass z,
+ * out[5] FFT pass y, out[6] FFT pass x + deconvolve.  Enabled by hpnfft_enable_timing(p, 1);
+ * reading synchronises the stream.  Returns the number of values written (<= n).
+ */
+int hpnfft_enable_timing(hpnfft_plan_t p, int on);
+int hpnfft_stage_times(hpnfft_plan_t p, float* out, int n);
+
+/* Library version string. */
+const char* hpnfft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPNFFT_H_ */

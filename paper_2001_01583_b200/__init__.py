@@ -1,0 +1,205 @@
+"""B200-native adjoint NFFT (the HP-NFFT hot path of arXiv 2001.01583).
+
+Thin Python binding over the C ABI in include/hpnfft.h (libhpnfft.so, sm_100a).  This module
+only marshals arguments: torch supplies device memory and the current CUDA stream; every step
+of the transform runs in the library's kernels.  There is no CPU fallback: if the library is
+missing or no GPU is present, the calls raise.
+
+    plan = Plan(N=(256, 256, 256), M=10**7, m=6, sigma=2.0, window="kb")
+    plan.set_points(x)          # x: cuda float64 [M, 3], coordinates in [-0.5, 0.5]
+    fhat = plan.adjoint(f)      # f: cuda complex128 [M]  ->  complex128 [N0, N1, N2]
+
+fhat[k0 + N0/2, k1 + N1/2, k2 + N2/2] = sum_j f_j exp(-2 pi i k.x_j)   (Eq. 5)
+up to the NFFT approximation error (E2 ~ 1e-11 at m = 6, sigma = 2, Kaiser-Bessel).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhpnfft.so")
+
+WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
+SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}
+STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv")
+
+HPNFFT_OK = 0
+_ERRORS = {
+    -1: ValueError,
+    -2: NotImplementedError,
+    -3: ValueError,
+    -4: MemoryError,
+    -5: RuntimeError,
+    -6: RuntimeError,
+    -7: RuntimeError,
+    -8: ValueError,
+}
+_ERROR_NAMES = {-1: "E_INVALID", -2: "E_UNSUPPORTED", -3: "E_RANGE", -4: "E_NOMEM", -5: "E_CUDA",
+                -6: "E_NCCL", -7: "E_STATE", -8: "E_DEGENERATE_WINDOW"}
+
+_lib = None
+
+
+class HpnfftError(RuntimeError):
+    pass
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libhpnfft.so and declare the C signatures (raises if the library is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    vp, i64, i64p, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p
+    lib.hpnfft_plan.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_int, vp]
+    lib.hpnfft_plan.restype = ctypes.c_int
+    lib.hpnfft_set_points.argtypes = [vp, dp]
+    lib.hpnfft_set_points.restype = ctypes.c_int
+    lib.hpnfft_adjoint.argtypes = [vp, dp, dp]
+    lib.hpnfft_adjoint.restype = ctypes.c_int
+    lib.hpnfft_destroy.argtypes = [vp]
+    lib.hpnfft_destroy.restype = ctypes.c_int
+    lib.hpnfft_last_error.argtypes = []
+    lib.hpnfft_last_error.restype = ctypes.c_char_p
+    lib.hpnfft_workspace_bytes.argtypes = [vp]
+    lib.hpnfft_workspace_bytes.restype = ctypes.c_size_t
+    lib.hpnfft_set_stream.argtypes = [vp, vp]
+    lib.hpnfft_set_stream.restype = ctypes.c_int
+    lib.hpnfft_set_spread_method.argtypes = [vp, ctypes.c_int]
+    lib.hpnfft_set_spread_method.restype = ctypes.c_int
+    lib.hpnfft_launch_count.argtypes = [vp]
+    lib.hpnfft_launch_count.restype = ctypes.c_int64
+    lib.hpnfft_enable_timing.argtypes = [vp, ctypes.c_int]
+    lib.hpnfft_enable_timing.restype = ctypes.c_int
+    lib.hpnfft_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    lib.hpnfft_stage_times.restype = ctypes.c_int
+    lib.hpnfft_version.argtypes = []
+    lib.hpnfft_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != HPNFFT_OK:
+        msg = load_library().hpnfft_last_error().decode()
+        exc = _ERRORS.get(rc, HpnfftError)
+        raise exc(f"hpnfft {_ERROR_NAMES.get(rc, rc)}: {msg}")
+
+
+def _stream_ptr(stream):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """One adjoint NFFT plan (hpnfft_plan): fixed N, M, m, sigma and window."""
+
+    def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None):
+        import torch
+
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("hpnfft needs a CUDA device (there is no CPU path)")
+        self.N = tuple(int(v) for v in N)
+        self.M = int(M)
+        self.m = int(m)
+        self.sigma = float(sigma)
+        self.window = WINDOWS[window] if isinstance(window, str) else int(window)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._stream = stream
+        arr = (ctypes.c_int64 * len(self.N))(*self.N)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib.hpnfft_plan(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window,
+                                   _stream_ptr(stream)))
+        self._h = h
+
+    # -- stream plumbing: every call runs on the caller's current torch stream (or the fixed one)
+    def _sync_stream(self):
+        _check(load_library().hpnfft_set_stream(self._h, _stream_ptr(self._stream)))
+
+    def set_points(self, x):
+        import torch
+
+        if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.shape[1] == 3):
+            raise TypeError("x must be a CUDA float64 tensor of shape [M, 3]")
+        if x.shape[0] != self.M:
+            raise ValueError(f"x has {x.shape[0]} points, the plan was built for M = {self.M}")
+        x = x.contiguous()
+        self._sync_stream()
+        _check(load_library().hpnfft_set_points(self._h, ctypes.c_void_p(x.data_ptr())))
+
+    def adjoint(self, f, out=None):
+        import torch
+
+        if not (f.is_cuda and f.dtype == torch.complex128 and f.numel() == self.M):
+            raise TypeError("f must be a CUDA complex128 tensor with M elements")
+        f = f.contiguous()
+        if out is None:
+            out = torch.empty(self.N, dtype=torch.complex128, device=f.device)
+        elif not (out.is_cuda and out.dtype == torch.complex128 and tuple(out.shape) == self.N and out.is_contiguous()):
+            raise TypeError("out must be a contiguous CUDA complex128 tensor of shape N")
+        self._sync_stream()
+        _check(load_library().hpnfft_adjoint(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def __call__(self, x, f):
+        self.set_points(x)
+        return self.adjoint(f)
+
+    def transform_host(self, x_host, f_host, out_host=None):
+        """End-to-end call with HOST inputs/outputs (pinned torch CPU tensors): H2D copy of x and
+        f, set_points + adjoint, D2H copy of fhat, all on the current stream."""
+        import torch
+
+        x = x_host.to(self.device, non_blocking=True)
+        f = f_host.to(self.device, non_blocking=True)
+        self.set_points(x)
+        fh = self.adjoint(f)
+        if out_host is None:
+            out_host = torch.empty(self.N, dtype=torch.complex128, pin_memory=True)
+        out_host.copy_(fh, non_blocking=True)
+        return out_host
+
+    def set_spread_method(self, method):
+        m = SPREAD_METHODS[method] if isinstance(method, str) else int(method)
+        _check(load_library().hpnfft_set_spread_method(self._h, m))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(load_library().hpnfft_workspace_bytes(self._h))
+
+    def launch_count(self) -> int:
+        return int(load_library().hpnfft_launch_count(self._h))
+
+    def enable_timing(self, on: bool = True):
+        _check(load_library().hpnfft_enable_timing(self._h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        buf = (ctypes.c_float * len(STAGES))()
+        w = load_library().hpnfft_stage_times(self._h, buf, len(STAGES))
+        if w < 0:
+            _check(w)
+        return {STAGES[i]: float(buf[i]) for i in range(w)}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().hpnfft_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def version() -> str:
+    return load_library().hpnfft_version().decode()

@@ -1,0 +1,351 @@
+// api.cu -- the C ABI of include/hpnfft.h: validation, workspace, orchestration.
+//
+// Per-call structure (Alg. 2 of the paper, without its per-call H2D/D2H and
+// allocation: data is device resident and the plan owns its workspace):
+//   hpnfft_set_points : keys + histogram -> exclusive scan -> scatter      (sort.cu)
+//   hpnfft_adjoint    : spread (spread_sweep.cu / spread_atomic.cu)
+//                       -> FFT pass z -> pass y -> pass x + deconvolve    (fft.cu)
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+namespace hpnfft {
+
+static thread_local std::string g_last_error = "no error";
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(Plan* p, int code, const std::string& msg) {
+  set_error(msg);
+  if (p && (code == HPNFFT_E_CUDA || code == HPNFFT_E_NCCL)) p->failed = true;
+  return code;
+}
+
+int check_launch(Plan* p, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(p, HPNFFT_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HPNFFT_OK;
+}
+
+void stage_begin(Plan* p, int slot) {
+  if (!p->timing) return;
+  if ((int)p->ev.size() < p->ev_used + 2) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    p->ev.push_back(a);
+    p->ev.push_back(b);
+  }
+  cudaEventRecord(p->ev[p->ev_used], p->stream);
+  (void)slot;
+}
+
+// each begin/end pair occupies two consecutive pool events; ev_slot[pair] is its stage id
+void stage_end(Plan* p, int slot) {
+  if (!p->timing) return;
+  cudaEventRecord(p->ev[p->ev_used + 1], p->stream);
+  p->ev_used += 2;
+  p->ev_slot.push_back(slot);
+}
+
+int64_t scan_workspace_elems(int64_t nbins);
+
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static void free_plan(Plan* p) {
+  if (!p) return;
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  else cudaDeviceSynchronize();
+  cudaFree(p->grid);
+  cudaFree(p->bufA);
+  for (int t = 0; t < 3; ++t) {
+    cudaFree(p->inv_c[t]);
+    cudaFree(p->twiddle[t]);
+  }
+  cudaFree(p->poly);
+  cudaFree(p->bin_count);
+  cudaFree(p->key);
+  cudaFree(p->rank);
+  cudaFree(p->perm);
+  cudaFree(p->xs);
+  cudaFree(p->scan_tmp);
+  cudaFree(p->err_flag);
+  if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
+  for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+  delete p;
+}
+
+template <typename T>
+static int alloc(Plan* p, T** ptr, size_t count) {
+  size_t bytes = sizeof(T) * (count ? count : 1);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("device allocation of ") + std::to_string(bytes) + " bytes failed: " +
+              cudaGetErrorString(e));
+    return HPNFFT_E_NOMEM;
+  }
+  p->ws_bytes += bytes;
+  return HPNFFT_OK;
+}
+
+}  // namespace hpnfft
+
+using namespace hpnfft;
+
+extern "C" {
+
+const char* hpnfft_version(void) { return "hpnfft-b200 0.1 (sm_100a)"; }
+
+const char* hpnfft_last_error(void) { return g_last_error.c_str(); }
+
+int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
+                void* stream) {
+  if (!out) {
+    set_error("hpnfft_plan: out is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  *out = nullptr;
+  if (!N) {
+    set_error("hpnfft_plan: N is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  if (d < 1) {
+    set_error("hpnfft_plan: d must be >= 1");
+    return HPNFFT_E_INVALID;
+  }
+  for (int t = 0; t < d; ++t) {
+    if (N[t] < 2 || (N[t] & 1)) {
+      set_error("invalid bandwidth: every N_t must be even and >= 2 (PAPER.md:27)");
+      return HPNFFT_E_INVALID;
+    }
+  }
+  if (d != 3) {
+    set_error("only d = 3 is implemented on the GPU");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  if (M < 0 || M >= (int64_t(1) << 31)) {
+    set_error("M must satisfy 0 <= M < 2^31");
+    return HPNFFT_E_INVALID;
+  }
+  if (!(sigma > 1.0)) {
+    set_error("sigma must be > 1");
+    return HPNFFT_E_INVALID;
+  }
+  if (window != HPNFFT_WINDOW_KAISER_BESSEL && window != HPNFFT_WINDOW_GAUSSIAN) {
+    set_error("unknown window");
+    return HPNFFT_E_INVALID;
+  }
+  if (m < kMinM || m > kMaxM) {
+    set_error("m must be in [2, 8] for the GPU kernels");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  int64_t n[3];
+  for (int t = 0; t < 3; ++t) {
+    double nt = sigma * (double)N[t];
+    int64_t ni = (int64_t)(nt + 0.5);
+    if (fabs(nt - (double)ni) > 1e-9 || !is_pow2(ni)) {
+      set_error("n_t = sigma * N_t must be an integer power of two");
+      return HPNFFT_E_UNSUPPORTED;
+    }
+    if (ni < 4 || ni > 1024) {
+      set_error("n_t must be in [4, 1024] for the FFT kernels");
+      return HPNFFT_E_UNSUPPORTED;
+    }
+    n[t] = ni;
+  }
+  int64_t cells = n[0] * n[1] * n[2];
+  Plan* p = new (std::nothrow) Plan();
+  if (!p) {
+    set_error("host allocation failed");
+    return HPNFFT_E_NOMEM;
+  }
+  p->d = 3;
+  for (int t = 0; t < 3; ++t) {
+    p->N[t] = N[t];
+    p->n[t] = n[t];
+    int l = 0;
+    while ((int64_t(1) << l) < n[t]) ++l;
+    p->logn[t] = l;
+  }
+  p->M = M;
+  p->m = m;
+  p->sigma = sigma;
+  p->window = window;
+  p->stream = reinterpret_cast<cudaStream_t>(stream);
+  int s2 = 0;
+  while ((1 << (s2 + 1)) <= 8 && (int64_t(1) << (s2 + 1)) <= n[2]) ++s2;
+  p->nbins = n[1] * (n[2] >> s2) * n[0];
+  int rc = HPNFFT_OK;
+  rc = rc ? rc : alloc(p, &p->grid, 2 * (size_t)cells);
+  rc = rc ? rc : alloc(p, &p->bufA, 2 * (size_t)(n[0] * n[1] * N[2]));
+  for (int t = 0; t < 3 && !rc; ++t) {
+    rc = alloc(p, &p->inv_c[t], (size_t)N[t]);
+    rc = rc ? rc : alloc(p, &p->twiddle[t], 2 * (size_t)n[t]);
+  }
+  rc = rc ? rc : alloc(p, &p->poly, (size_t)(2 * kMaxM * (kPolyDeg + 1)));
+  rc = rc ? rc : alloc(p, &p->bin_count, (size_t)(p->nbins + 1));
+  rc = rc ? rc : alloc(p, &p->key, (size_t)M);
+  rc = rc ? rc : alloc(p, &p->rank, (size_t)M);
+  rc = rc ? rc : alloc(p, &p->perm, (size_t)M);
+  rc = rc ? rc : alloc(p, &p->xs, 3 * (size_t)M);
+  p->scan_tmp_elems = scan_workspace_elems(p->nbins);
+  rc = rc ? rc : alloc(p, reinterpret_cast<uint32_t**>(&p->scan_tmp), (size_t)p->scan_tmp_elems);
+  rc = rc ? rc : alloc(p, &p->err_flag, 1);
+  if (!rc) {
+    cudaError_t e = cudaMallocHost(&p->err_flag_host, sizeof(int));
+    if (e != cudaSuccess) {
+      set_error("pinned allocation failed");
+      rc = HPNFFT_E_NOMEM;
+    }
+  }
+  p->bufB = p->grid;   // pass y output reuses the grid (dead after pass z)
+  if (!rc) rc = build_tables(p);
+  if (rc) {
+    free_plan(p);
+    return rc;
+  }
+  *out = reinterpret_cast<hpnfft_plan_t>(p);
+  return HPNFFT_OK;
+}
+
+int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (p->failed) {
+    set_error("plan is in a failed state (an earlier CUDA error)");
+    return HPNFFT_E_STATE;
+  }
+  if (!x && p->M > 0) {
+    set_error("x is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  p->points_set = false;
+  p->launches = 0;
+  int rc = sort_points(p, x);
+  if (rc) return rc;
+  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream),
+                  "flag d2h");
+  HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
+  if (*p->err_flag_host) {
+    set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
+    return HPNFFT_E_RANGE;
+  }
+  p->points_set = true;
+  return HPNFFT_OK;
+}
+
+int hpnfft_adjoint(hpnfft_plan_t h, const double* f, double* fhat) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (p->failed) {
+    set_error("plan is in a failed state (an earlier CUDA error)");
+    return HPNFFT_E_STATE;
+  }
+  if (!p->points_set) {
+    set_error("hpnfft_adjoint called before a successful hpnfft_set_points");
+    return HPNFFT_E_STATE;
+  }
+  if (!fhat || (!f && p->M > 0)) {
+    set_error("f or fhat is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  int rc;
+  stage_begin(p, 3);
+  bool sweep = (p->spread_method == HPNFFT_SPREAD_SWEEP) ||
+               (p->spread_method == HPNFFT_SPREAD_AUTO && sweep_supported(p));
+  if (p->spread_method == HPNFFT_SPREAD_SWEEP && !sweep_supported(p)) {
+    set_error("sweep spread kernel not supported for this grid");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  rc = sweep ? spread_sweep(p, f) : spread_atomic(p, f);
+  stage_end(p, 3);
+  if (rc) return rc;
+  return fft_and_deconvolve(p, fhat);
+}
+
+int hpnfft_destroy(hpnfft_plan_t h) {
+  free_plan(reinterpret_cast<Plan*>(h));
+  return HPNFFT_OK;
+}
+
+size_t hpnfft_workspace_bytes(hpnfft_plan_t h) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  return p ? p->ws_bytes : 0;
+}
+
+int hpnfft_set_stream(hpnfft_plan_t h, void* stream) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  p->stream = reinterpret_cast<cudaStream_t>(stream);
+  return HPNFFT_OK;
+}
+
+int hpnfft_set_spread_method(hpnfft_plan_t h, int method) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (method < HPNFFT_SPREAD_AUTO || method > HPNFFT_SPREAD_SWEEP) {
+    set_error("unknown spread method");
+    return HPNFFT_E_INVALID;
+  }
+  p->spread_method = method;
+  return HPNFFT_OK;
+}
+
+int64_t hpnfft_launch_count(hpnfft_plan_t h) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  return p ? p->launches : -1;
+}
+
+int hpnfft_enable_timing(hpnfft_plan_t h, int on) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  p->timing = on != 0;
+  return HPNFFT_OK;
+}
+
+int hpnfft_stage_times(hpnfft_plan_t h, float* out, int nout) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p || !out) {
+    set_error("NULL argument");
+    return HPNFFT_E_INVALID;
+  }
+  HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "timing sync");
+  double acc[kNumStages] = {0};
+  int cnt[kNumStages] = {0};
+  for (size_t pair = 0; pair < p->ev_slot.size(); ++pair) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p->ev[2 * pair], p->ev[2 * pair + 1]);
+    int sl = p->ev_slot[pair];
+    if (sl >= 0 && sl < kNumStages) {
+      acc[sl] += ms;
+      cnt[sl] += 1;
+    }
+  }
+  p->ev_slot.clear();
+  p->ev_used = 0;
+  int w = 0;
+  for (int s = 0; s < kNumStages && w < nout; ++s, ++w) out[w] = cnt[s] ? (float)(acc[s] / cnt[s]) : 0.0f;
+  return w;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// common.cuh -- plan object, error plumbing and small device helpers of libhpnfft.
+// Product code (the CUDA path).  Shares nothing with oracle/ (see DESIGN.md "Boundary").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hpnfft.h"
+
+namespace hpnfft {
+
+constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
+constexpr int kMinM = 2;
+constexpr int kPolyDeg = 14;      // window tap polynomial degree
+constexpr int kNumStages = 7;     // timing slots, see hpnfft_stage_times
+
+struct Dims3 {
+  int64_t v[3];
+};
+
+// Plan: everything one adjoint transform needs, owned by the library.
+struct Plan {
+  int d = 3;
+  int64_t N[3] = {0, 0, 0};   // bandwidths N_t
+  int64_t n[3] = {0, 0, 0};   // oversampled grid n_t = sigma N_t (powers of two)
+  int logn[3] = {0, 0, 0};
+  int64_t M = 0;
+  int m = 6;
+  double sigma = 2.0;
+  int window = HPNFFT_WINDOW_KAISER_BESSEL;
+  cudaStream_t stream = nullptr;
+  int spread_method = HPNFFT_SPREAD_AUTO;
+  bool failed = false;
+  bool points_set = false;
+
+  // ---- device workspace (plan-owned) ----
+  double* grid = nullptr;       // [n0][n1][n2] complex (2 doubles)
+  double* bufA = nullptr;       // [n0][n1][N2] complex (FFT pass z output)
+  double* bufB = nullptr;       // [n0][N1][N2] complex (aliases grid)
+  double* inv_c[3] = {nullptr, nullptr, nullptr};   // 1/c_k per dim, index k + N/2
+  double* twiddle[3] = {nullptr, nullptr, nullptr}; // exp(-2 pi i t/n_t), t < n_t (complex)
+  double* poly = nullptr;       // window tap polynomials [2m][kPolyDeg+1]
+  // bin sort
+  int64_t nbins = 0;            // n1 * (n2/8) * n0 bins, key = (c1 * nb2 + c2/8) * n0 + c0
+  uint32_t* bin_count = nullptr;  // [nbins + 1], becomes exclusive prefix (bin_start)
+  uint32_t* key = nullptr;        // [M]
+  uint32_t* rank = nullptr;       // [M] arrival rank inside the bin
+  uint32_t* perm = nullptr;       // [M] sorted position -> original index
+  double* xs = nullptr;           // [M][3] sorted coordinates
+  void* scan_tmp = nullptr;       // block sums for the scan
+  int64_t scan_tmp_elems = 0;
+  int* err_flag = nullptr;        // device range-error flag
+  int* err_flag_host = nullptr;   // pinned mirror
+  size_t ws_bytes = 0;
+
+  int64_t launches = 0;         // kernel launches since the last set_points
+
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pool, kNumStages+1 events per call
+  int ev_used = 0;
+  std::vector<int> ev_slot;     // stage id of each recorded begin/end pair
+  double stage_ms_acc[kNumStages] = {0};
+  int stage_calls[kNumStages] = {0};
+};
+
+void set_error(const std::string& msg);
+int fail(Plan* p, int code, const std::string& msg);
+
+// Launch-error check helper: returns HPNFFT_OK or records the CUDA error on the plan.
+int check_launch(Plan* p, const char* what);
+
+// timing helpers (no-ops unless p->timing)
+void stage_begin(Plan* p, int slot);
+void stage_end(Plan* p, int slot);
+
+// kernels' host launchers (each returns HPNFFT_OK or an error code)
+int build_tables(Plan* p);
+int sort_points(Plan* p, const double* x);
+int spread_atomic(Plan* p, const double* f);
+int spread_sweep(Plan* p, const double* f);
+bool sweep_supported(const Plan* p);
+int fft_and_deconvolve(Plan* p, double* fhat);
+
+}  // namespace hpnfft
+
+#define HPNFFT_CUDA_TRY(p, expr, what)                                       \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      return ::hpnfft::fail((p), HPNFFT_E_CUDA,                              \
+                            std::string(what) + ": " + cudaGetErrorString(e_)); \
+    }                                                                        \
+  } while (0)

@@ -1,0 +1,170 @@
+// sort.cu -- A1 (keys) + A2 (bin sort) of SURVEY.md §8(a): `hpnfft_set_points`.
+//
+// Not in the paper (its CUNFFT spreads points in input order, one thread per point,
+// PAPER.md:162-164); the B200 design sorts the points once so the spread kernel can sweep
+// the grid with register-resident windows.
+//   u_t = n_t x_t (exact for power-of-two n_t), c_t = floor(u_t) mod n_t  (integer cell)
+//   bin  = (c1 * nb2 + (c2 >> s2)) * n0 + c0       nb2 = n2 >> s2, s2 = log2(min(8, n2))
+// i.e. "pencils" of (one c1 row, 8 consecutive c2) with the c0 index fastest, so the points a
+// sweep CTA needs for its current c0 plane are contiguous per pencil.
+// Counting sort: histogram with arrival ranks (atomicAdd) -> exclusive scan -> scatter.
+// The order inside a bin is the atomic arrival order (not deterministic; Q21).
+#include "common.cuh"
+
+namespace hpnfft {
+
+__global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2,
+                       uint32_t* __restrict__ count, uint32_t* __restrict__ key, uint32_t* __restrict__ rank,
+                       int* __restrict__ err) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
+  if (!(fabs(x0) <= 0.5 && fabs(x1) <= 0.5 && fabs(x2) <= 0.5)) {
+    *err = 1;   // benign race: any writer sets 1
+    x0 = x1 = x2 = 0.0;
+  }
+  int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x0)) & (n0 - 1);
+  int64_t c1 = (int64_t)floor(__dmul_rn((double)n1, x1)) & (n1 - 1);
+  int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
+  int64_t nb2 = n2 >> s2;
+  uint32_t k = (uint32_t)((c1 * nb2 + (c2 >> s2)) * n0 + c0);
+  key[j] = k;
+  rank[j] = atomicAdd(&count[k], 1u);
+}
+
+// ---- device-wide exclusive scan of uint32 (three-phase, recursive over block sums) ----
+constexpr int kScanThreads = 1024;
+constexpr int kScanPerThread = 8;
+constexpr int kScanTile = kScanThreads * kScanPerThread;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t warp_sums[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = (lane < (int)(blockDim.x >> 5)) ? warp_sums[lane] : 0u;
+    uint32_t si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) si += t;
+    }
+    warp_sums[lane] = si - s;   // exclusive warp offsets
+    if (lane == 31) *total = si;
+  }
+  __syncthreads();
+  uint32_t r = warp_sums[wid] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// scans each tile of kScanTile elements in place (exclusive), writes tile totals to sums
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(uint32_t* __restrict__ a, int64_t n,
+                                                             uint32_t* __restrict__ sums) {
+  __shared__ uint32_t total;
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPerThread;
+  uint32_t v[kScanPerThread];
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) {
+    v[q] = (base + q < n) ? a[base + q] : 0u;
+    s += v[q];
+  }
+  uint32_t off = block_exclusive_scan(s, &total);
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) {
+    if (base + q < n) a[base + q] = off;
+    off += v[q];
+  }
+  if (threadIdx.x == 0 && sums) sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_add(uint32_t* __restrict__ a, int64_t n, const uint32_t* __restrict__ sums) {
+  int64_t i = (int64_t)blockIdx.x * kScanTile + threadIdx.x;
+  uint32_t add = sums[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) {
+    int64_t e = i + (int64_t)q * kScanThreads;
+    if (e < n) a[e] += add;
+  }
+}
+
+static int64_t scan_tmp_need(int64_t n) {
+  int64_t need = 0;
+  while (n > kScanTile) {
+    int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    need += tiles;
+    n = tiles;
+  }
+  return need + 1;
+}
+
+static int scan_exclusive(Plan* p, uint32_t* a, int64_t n, uint32_t* tmp) {
+  int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles <= 1) {
+    k_scan_tiles<<<1, kScanThreads, 0, p->stream>>>(a, n, nullptr);
+    p->launches++;
+    return check_launch(p, "scan");
+  }
+  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, p->stream>>>(a, n, tmp);
+  p->launches++;
+  int rc = scan_exclusive(p, tmp, tiles, tmp + tiles);
+  if (rc) return rc;
+  k_scan_add<<<(unsigned)tiles, kScanThreads, 0, p->stream>>>(a, n, tmp);
+  p->launches++;
+  return check_launch(p, "scan add");
+}
+
+__global__ void k_scatter(const double* __restrict__ x, int64_t M, const uint32_t* __restrict__ key,
+                          const uint32_t* __restrict__ rank, const uint32_t* __restrict__ start,
+                          uint32_t* __restrict__ perm, double* __restrict__ xs) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  uint32_t pos = start[key[j]] + rank[j];
+  perm[pos] = (uint32_t)j;
+  xs[3 * (int64_t)pos] = x[3 * j];
+  xs[3 * (int64_t)pos + 1] = x[3 * j + 1];
+  xs[3 * (int64_t)pos + 2] = x[3 * j + 2];
+}
+
+int64_t scan_workspace_elems(int64_t nbins) { return scan_tmp_need(nbins + 1); }
+
+int sort_points(Plan* p, const double* x) {
+  const int64_t M = p->M;
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count, 0, sizeof(uint32_t) * (p->nbins + 1), p->stream), "memset bins");
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag, 0, sizeof(int), p->stream), "memset flag");
+  int s2 = 0;
+  while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
+  stage_begin(p, 0);
+  if (M > 0) {
+    k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->n[0], p->n[1], p->n[2], s2, p->bin_count,
+                                                               p->key, p->rank, p->err_flag);
+    p->launches++;
+    int rc = check_launch(p, "keys");
+    if (rc) return rc;
+  }
+  stage_end(p, 0);
+  stage_begin(p, 1);
+  int rc = scan_exclusive(p, p->bin_count, p->nbins + 1, reinterpret_cast<uint32_t*>(p->scan_tmp));
+  if (rc) return rc;
+  stage_end(p, 1);
+  stage_begin(p, 2);
+  if (M > 0) {
+    k_scatter<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->key, p->rank, p->bin_count, p->perm,
+                                                                  p->xs);
+    p->launches++;
+    rc = check_launch(p, "scatter");
+    if (rc) return rc;
+  }
+  stage_end(p, 2);
+  return HPNFFT_OK;
+}
+
+}  // namespace hpnfft

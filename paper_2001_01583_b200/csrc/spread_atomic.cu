@@ -1,0 +1,77 @@
+// spread_atomic.cu -- generic spreading kernel (A4 of SURVEY.md §8(a)), the paper's scheme:
+// "each thread is responsible for one point ... AtomicAdd()" (§3), refined to one
+// thread per (point, tap i0) so a point's (2m)^3 stencil is split over 2m threads.
+//   g(l) += f_j * w0[i0] * w1[i1] * w2[i2]   over the 2m x 2m taps (i1, i2) of this thread,
+// with native FP64 global atomics (RED.E.ADD.F64) into the zeroed grid.  Points are visited
+// in sorted (bin) order for L2 locality.  Works for every supported grid (n_t >= 2m); it is
+// the correctness baseline that the sweep kernel (spread_sweep.cu) is measured against.
+#include "spread_common.cuh"
+
+namespace hpnfft {
+
+template <int M_>
+__global__ void k_spread_atomic(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
+                                const double* __restrict__ f, int64_t M, int64_t n0, int64_t n1, int64_t n2,
+                                const double* __restrict__ poly_g, double* __restrict__ grid) {
+  constexpr int W = 2 * M_;
+  __shared__ double poly[W * (kPolyDeg + 1)];
+  for (int e = threadIdx.x; e < W * (kPolyDeg + 1); e += blockDim.x) poly[e] = poly_g[e];
+  __syncthreads();
+  int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= M * W) return;
+  int64_t j = gid / W;
+  int i0 = (int)(gid % W);
+  CellT a0 = cell_of(xs[3 * j], n0), a1 = cell_of(xs[3 * j + 1], n1), a2 = cell_of(xs[3 * j + 2], n2);
+  uint32_t src = perm[j];
+  double fr = f[2 * (int64_t)src], fi = f[2 * (int64_t)src + 1];
+  double w0 = tap_weight(poly, i0, a0.t, M_);
+  double w1[W], w2[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    w1[i] = tap_weight(poly, i, a1.t, M_);
+    w2[i] = tap_weight(poly, i, a2.t, M_);
+  }
+  int64_t l0 = (a0.c - M_ + 1 + i0) & (n0 - 1);
+  double gr = fr * w0, gi = fi * w0;
+#pragma unroll 1
+  for (int i1 = 0; i1 < W; ++i1) {
+    int64_t l1 = (a1.c - M_ + 1 + i1) & (n1 - 1);
+    double hr = gr * w1[i1], hi = gi * w1[i1];
+    double* row = grid + 2 * ((l0 * n1 + l1) * n2);
+#pragma unroll
+    for (int i2 = 0; i2 < W; ++i2) {
+      int64_t l2 = (a2.c - M_ + 1 + i2) & (n2 - 1);
+      atomicAdd(row + 2 * l2, hr * w2[i2]);
+      atomicAdd(row + 2 * l2 + 1, hi * w2[i2]);
+    }
+  }
+}
+
+template <int M_>
+static int launch_atomic(Plan* p, const double* f) {
+  int64_t total = p->M * 2 * M_;
+  if (total == 0) return HPNFFT_OK;
+  k_spread_atomic<M_><<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
+      p->xs, p->perm, f, p->M, p->n[0], p->n[1], p->n[2], p->poly, p->grid);
+  p->launches++;
+  return check_launch(p, "spread_atomic");
+}
+
+int spread_atomic(Plan* p, const double* f) {
+  size_t bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->grid, 0, bytes, p->stream), "zero grid");
+  switch (p->m) {
+    case 2: return launch_atomic<2>(p, f);
+    case 3: return launch_atomic<3>(p, f);
+    case 4: return launch_atomic<4>(p, f);
+    case 5: return launch_atomic<5>(p, f);
+    case 6: return launch_atomic<6>(p, f);
+    case 7: return launch_atomic<7>(p, f);
+    case 8: return launch_atomic<8>(p, f);
+    default:
+      set_error("m not supported by the spread kernels");
+      return HPNFFT_E_UNSUPPORTED;
+  }
+}
+
+}  // namespace hpnfft

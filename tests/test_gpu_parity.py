@@ -1,0 +1,212 @@
+"""GPU parity tests: the CUDA path (through the C ABI via the thin binding) against the CPU oracle.
+
+Bars (BASELINE.json north_star): E2 <= 1e-12 against the CPU NFFT oracle (O2, same conventions)
+and E2 <= 1e-9 against the direct NDFT (O1).  Inputs are the seeded generators of inputs/.
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _hp():
+    import paper_2001_01583_b200 as hp
+
+    hp.load_library()
+    return hp
+
+
+def gpu_adjoint(x, f, N, m=6, sigma=2.0, window="kb", method="auto"):
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, x.shape[0], m=m, sigma=sigma, window=window, device=dev)
+    plan.set_spread_method(method)
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(x)).to(dev))
+    out = plan.adjoint(torch.from_numpy(np.ascontiguousarray(f)).to(dev)).cpu().numpy()
+    plan.close()
+    return out
+
+
+METHODS = ["atomic", "auto"]
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_config1_uniform(method):
+    """BASELINE config 1: N = 16^3, M = 1000 uniform, KB m = 6, sigma = 2."""
+    N, M = (16, 16, 16), 1000
+    x, f = inputs.uniform_points(M), inputs.uniform_values(M)
+    g = gpu_adjoint(x, f, N, method=method)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    assert oracle.rel_l2_error(g, oracle.ndft_direct(x, f, N)) <= 1e-9
+
+
+@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("N", [(32, 16, 64), (64, 64, 32), (8, 128, 16)])
+def test_ragged_noncubic(method, N):
+    """Several tiles per dimension and ragged tails: non-cubic N, M not a multiple of anything."""
+    M = 4099
+    x, f = inputs.uniform_points(M, seed=77), inputs.uniform_values(M, seed=77)
+    g = gpu_adjoint(x, f, N, method=method)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
+def test_all_cutoffs_match_cpu_nfft(m):
+    N, M = (32, 32, 32), 2000
+    x, f = inputs.uniform_points(M, seed=m), inputs.uniform_values(M, seed=m)
+    g = gpu_adjoint(x, f, N, m=m)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m)) <= 1e-12
+
+
+def test_gaussian_window():
+    N, M = (16, 32, 16), 1500
+    x, f = inputs.uniform_points(M, seed=3), inputs.uniform_values(M, seed=3)
+    g = gpu_adjoint(x, f, N, window="gaussian")
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, window=oracle.GAUSSIAN)) <= 1e-12
+
+
+def test_on_node_and_boundary_points():
+    """Equispaced on-node points (t = 0: strict truncation drops the last tap) plus x = +-0.5."""
+    N = (16, 16, 16)
+    x = inputs.equispaced_points(N)
+    x[:16, 0] = 0.5
+    x[16:32, 1] = -0.5
+    f = inputs.uniform_values(x.shape[0], seed=5)
+    g = gpu_adjoint(x, f, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    assert oracle.rel_l2_error(g, oracle.ndft_direct(x, f, N)) <= 1e-9
+
+
+def test_single_point_and_empty():
+    N = (16, 16, 16)
+    g = gpu_adjoint(np.zeros((1, 3)), np.array([1.0 + 0j]), N)
+    assert np.max(np.abs(g - 1.0)) < 1e-9
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(np.zeros((1, 3)), np.array([1.0 + 0j]), N)) <= 1e-12
+    e = gpu_adjoint(np.zeros((0, 3)), np.zeros(0, dtype=complex), N)
+    assert np.all(e == 0)
+
+
+def test_tiny_grid_wraps():
+    """n = 4 < 2m: a point's taps wrap onto the same nodes several times."""
+    N = (2, 4, 8)
+    x, f = inputs.uniform_points(50, seed=9), inputs.uniform_values(50, seed=9)
+    g = gpu_adjoint(x, f, N, m=3)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=3)) <= 1e-12
+
+
+@pytest.mark.parametrize("s", [0.05, 0.01])
+def test_clustered(s):
+    N, M = (64, 64, 64), 200000
+    x = inputs.clustered_points(M, s=s)
+    f = inputs.uniform_values(M)
+    g = gpu_adjoint(x, f, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+def test_config2_madelung_caf2():
+    """BASELINE config 2: fluorite 8^3 cells, N = 64^3, S(n) from the GPU -> Madelung 2.5194."""
+    import json
+    import os
+
+    from oracle import ewald
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "madelung.json")))["caf2"]
+    N = (64, 64, 64)
+    x, f, L = inputs.crystal_nfft_inputs("caf2", 8)
+    g = gpu_adjoint(x, f, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    v = ewald.madelung("caf2", 8, N, 0.85, fhat_fn=lambda *a: g)
+    assert abs(v - gold["value"]) < gold["tolerance"]
+    v_o2 = ewald.madelung("caf2", 8, N, 0.85, fhat_fn=lambda xx, ff, NN: oracle.nfft_adjoint(xx, ff, NN))
+    assert abs(v - v_o2) < 1e-10
+
+
+def test_config3_full_vs_cpu_nfft():
+    """BASELINE config 3: N = 128^3, M = 10^6 uniform: full fhat vs O2, sampled k vs O1."""
+    N, M = (128, 128, 128), 10 ** 6
+    x, f = inputs.uniform_points(M), inputs.uniform_values(M)
+    g = gpu_adjoint(x, f, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    rng = np.random.default_rng(3)
+    ks = np.concatenate([rng.integers(-64, 64, size=(48, 3)), [[0, 0, 0], [-64, -64, -64], [63, 0, -64]]])
+    ref = oracle.ndft_direct(x, f, N, ks=ks)
+    got = np.array([g[tuple(k + 64)] for k in ks])
+    assert oracle.rel_l2_error(got, ref) <= 1e-9
+
+
+def test_config4_bench_size_sampled_ndft():
+    """BASELINE config 4 (the bench workload): N = 256^3, M = 10^7 uniform, in the bench's
+    launch configuration; sampled frequencies against the direct NDFT."""
+    import inputs.device as idev
+
+    hp = _hp()
+    N, M = (256, 256, 256), 10 ** 7
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, M, m=6, sigma=2.0, device=dev)
+    xd = idev.uniform_points(M, device=dev)
+    fd = idev.uniform_values(M, device=dev)
+    x = inputs.uniform_points(M)
+    assert np.array_equal(xd.cpu().numpy(), x)          # device generator is bit-identical
+    f = inputs.uniform_values(M)
+    plan.set_points(xd)
+    g = plan.adjoint(fd).cpu().numpy()
+    rng = np.random.default_rng(4)
+    ks = np.concatenate([rng.integers(-128, 128, size=(16, 3)), [[0, 0, 0], [-128, 127, 5]]])
+    ref = oracle.ndft_direct(x, f, N, ks=ks)
+    got = np.array([g[tuple(k + 128)] for k in ks])
+    assert oracle.rel_l2_error(got, ref) <= 1e-9
+    # f_hat(0) = sum f is fixed independently of any oracle sum order
+    assert abs(g[128, 128, 128] - np.sum(f)) / abs(np.sum(f)) < 1e-9
+
+
+def test_partition_invariance_on_gpu():
+    """Eq. 8 on the device: two plans over an x-slab split sum to the single-plan result."""
+    N, M = (32, 32, 32), 20000
+    x, f = inputs.uniform_points(M, seed=8), inputs.uniform_values(M, seed=8)
+    whole = gpu_adjoint(x, f, N)
+    lo = x[:, 0] < 0
+    parts = gpu_adjoint(x[lo], f[lo], N) + gpu_adjoint(x[~lo], f[~lo], N)
+    assert oracle.rel_l2_error(parts, whole) <= 1e-13
+
+
+def test_errors_range_and_state():
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan((16, 16, 16), 4, device=dev)
+    with pytest.raises(RuntimeError):
+        plan.adjoint(torch.zeros(4, dtype=torch.complex128, device=dev))     # E_STATE
+    bad = torch.zeros((4, 3), dtype=torch.float64, device=dev)
+    bad[2, 1] = 0.6
+    with pytest.raises(ValueError):
+        plan.set_points(bad)                                               # E_RANGE
+    bad[2, 1] = float("nan")
+    with pytest.raises(ValueError):
+        plan.set_points(bad)
+    good = torch.zeros((4, 3), dtype=torch.float64, device=dev)
+    plan.set_points(good)
+    out = plan.adjoint(torch.ones(4, dtype=torch.complex128, device=dev))
+    assert torch.allclose(out, torch.full_like(out, 4.0), atol=1e-9)
+    plan.close()
+
+
+def test_plan_reuse_and_methods_agree():
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (32, 64, 32), 5000
+    plan = hp.Plan(N, M, device=dev)
+    outs = []
+    for seed in (1, 2):
+        x, f = inputs.uniform_points(M, seed=seed), inputs.uniform_values(M, seed=seed)
+        plan.set_points(torch.from_numpy(x).to(dev))
+        g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+        assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+        outs.append(g)
+    plan.set_spread_method("atomic")
+    g2 = plan.adjoint(torch.from_numpy(inputs.uniform_values(M, seed=2)).to(dev)).cpu().numpy()
+    assert oracle.rel_l2_error(g2, outs[1]) <= 1e-13
+    plan.close()
