@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 adjoint NFFT hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--dist uniform|clustered] [--config 4|3|5] [--method auto|atomic|sweep]
+
+Workload (BASELINE.json configs[3], the metric's config): d = 3, N = 256^3, M = 10^7 points,
+float64, Kaiser-Bessel m = 6, sigma = 2 (grid 512^3).  One step = one pass of the whole hot
+path: set_points (keys, bin sort) + adjoint (spread, 3 FFT passes with the
+fused deconvolve/crop); for N > 1 GPUs every rank owns the points of one equal-size x-slab
+("subcells with same size") and the partial fhat are summed with an NCCL
+all-reduce (Eq. 8 / Alg. 3).  Total work is fixed as N grows
+(strong scaling).  Inputs are resident in HBM before the timed region and are larger than
+L2 (x 240 MB, f 160 MB, grid 2.1 GB), so no explicit L2 flush is needed.
+
+--impl reference times the CPU oracle (oracle/, the independent CPU NFFT) on the host cores
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "3": {"N": (128, 128, 128), "M": 10 ** 6},
+    "4": {"N": (256, 256, 256), "M": 10 ** 7},
+    "5": {"N": (512, 512, 512), "M": 10 ** 9},
+}
+METRIC = "adjoint NFFT nonuniform points/s at N=256³ float64, 1/2/4/8 B200; E2 error"
+M_WINDOW, SIGMA = 6, 2.0
+# FP64 peak derived from unit counts and clocks: 148 SMs x 64 FP64
+# FMA/clk/SM x 2 flop x 1.965 GHz max SM clock.  The FMA-chain microbenchmark measured
+# 34.2 TFLOP/s (tools/ubench_fp64.cu, profiles/ubench_fp64.txt).
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def spread_flops_per_point(m: int) -> float:
+    """Algorithmic FP64 work of the spread per point: 2(2m)^3 FMAs for the
+    complex-times-real tap updates + 2(2m)^2 for the per-(i1,i2) coefficient, 2 flop each."""
+    w = 2 * m
+    return 2.0 * (2 * w ** 3 + 2 * w ** 2)
+
+
+def fft_bytes(N, sigma=2.0):
+    """Algorithmic HBM bytes of the three pruned FFT passes."""
+    n = [int(sigma * v) for v in N]
+    c = 16
+    z = c * (n[0] * n[1] * n[2] + n[0] * n[1] * N[2])
+    y = c * (n[0] * n[1] * N[2] + n[0] * N[1] * N[2])
+    x = c * (n[0] * N[1] * N[2] + N[0] * N[1] * N[2])
+    return {"fft_z": z, "fft_y": y, "fft_x_deconv": x}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(cfg, dist_kind, device):
+    import inputs.device as idev
+
+    M = cfg["M"]
+    if dist_kind == "clustered":
+        x = idev.clustered_points(M, s=0.05, device=device)
+    else:
+        x = idev.uniform_points(M, device=device)
+    f = idev.uniform_values(M, device=device)
+    return x, f
+
+
+def slab_select(x, f, rank, ws):
+    """Equal-size x-slab subcell of this rank: x0 in [-1/2 + r/P, -1/2 + (r+1)/P)."""
+    if ws == 1:
+        return x, f
+    lo = -0.5 + rank / ws
+    hi = -0.5 + (rank + 1) / ws
+    x0 = x[:, 0]
+    mask = (x0 >= lo) & (x0 < hi)
+    if rank == ws - 1:
+        mask |= x0 >= 0.5
+    return x[mask].contiguous(), f[mask].contiguous()
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2001_01583_b200 as hp
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS[args.config]
+    N = cfg["N"]
+    M_total = cfg["M"]
+    x_all, f_all = make_inputs(cfg, args.dist, dev)
+    x, f = slab_select(x_all, f_all, rank, ws)
+    del x_all, f_all
+    M_local = x.shape[0]
+    torch.cuda.synchronize()
+
+    plan = hp.Plan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", device=dev)
+    plan.set_spread_method(args.method)
+    out = torch.empty(N, dtype=torch.complex128, device=dev)
+
+    def step():
+        plan.set_points(x)
+        plan.adjoint(f, out=out)
+        if ws > 1:
+            tdist.all_reduce(out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = plan.launch_count()
+
+    # ---- timed region: K steps, CUDA events on the plan's (current) stream ----
+    plan.enable_timing(True)
+    plan.stage_times()   # reset
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    clocks = sampler.stop()
+    ms_local = e0.elapsed_time(e1)
+    stages = plan.stage_times()
+    plan.enable_timing(False)
+    ms = ms_local
+    if ws > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = M_total / (ms_per_step * 1e-3)
+
+    # ---- e2e: the public API with HOST buffers (pinned), H2D + transform + D2H each step ----
+    xh = x.cpu().pin_memory()
+    fh = f.cpu().pin_memory()
+    oh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+
+    def e2e_step():
+        res = plan.transform_host(xh, fh, oh)
+        if ws > 1:
+            d = res.to(dev, non_blocking=True)
+            tdist.all_reduce(d)
+            res.copy_(d, non_blocking=True)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        e2e_step()
+    torch.cuda.synchronize()
+    k_e2e = max(1, min(args.steps, 5))
+    if ws > 1:
+        tdist.barrier()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(k_e2e):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = a0.elapsed_time(a1) / k_e2e
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = int(xh.numel() * 8 + fh.numel() * 16)
+    d2h = int(oh.numel() * 16)
+
+    # ---- roofline of the dominant kernel (largest stage) ----
+    kern = {k: v for k, v in stages.items() if k in ("spread", "fft_z", "fft_y", "fft_x_deconv")}
+    dom = max(kern, key=kern.get) if kern else "spread"
+    peaks = measured_peaks()
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get(f"config{args.config}_{args.dist}_{dom}_P{ws}")
+    except Exception:
+        pass
+    if dom == "spread":
+        fl = M_local * spread_flops_per_point(M_WINDOW)
+        achieved = fl / (stages["spread"] * 1e-3) / 1e12
+        roof = {"kernel": "spread", "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured FMA chain: 34.2)",
+                "algorithmic": f"{spread_flops_per_point(M_WINDOW):.0f} flop/point x {M_local} points"}
+    else:
+        byts = fft_bytes(N)[dom]
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        achieved = byts / (stages[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+    fft_ms = sum(stages.get(k, 0.0) for k in ("fft_z", "fft_y", "fft_x_deconv"))
+    fbytes = sum(fft_bytes(N).values())
+    extra = {
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "fft_hbm": {"achieved_gbs": fbytes / (fft_ms * 1e-3) / 1e9 if fft_ms else None,
+                    "frac": (fbytes / (fft_ms * 1e-3) / 1e9) / peaks.get("hbm_gbs", 6650.0) if fft_ms else None},
+        "M_local": M_local,
+    }
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.dist)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "points/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": f"synthetic seeded {args.dist} points (inputs/), counter-based generator",
+            "config": {"workload": f"BASELINE config {args.config}: d=3, N={N[0]}^3, M={M_total}, "
+                                   f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}",
+                       "N": list(N), "M": M_total, "m": M_WINDOW, "sigma": SIGMA, "window": "kaiser_bessel",
+                       "points": args.dist, "partition": f"equal-size x-slabs x{ws}",
+                       "exchange": "ncclAllReduce(fhat)" if ws > 1 else "none",
+                       "spread_method": args.method,
+                       "l2": "inputs larger than L2 (x 240 MB, f 160 MB, grid 2.1 GB); no flush"},
+            "e2e": {"value": M_total / (e2e_ms * 1e-3), "unit": "points/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "detail": extra,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- CPU oracle --
+def _oracle_timing(cfg, dist_kind, sample_points, fft_once=True):
+    """Time the CPU oracle (oracle.nfft_adjoint's steps, unmodified) on a bounded sample:
+    the serial C spread on `sample_points` of the M points and the FFT + deconvolve of the
+    full oversampled grid.  Returns (t_spread_per_point, t_fft)."""
+    import numpy as np
+
+    import inputs
+    import oracle
+
+    N = cfg["N"]
+    n = oracle.grid_size(N, SIGMA)
+    if dist_kind == "clustered":
+        x = inputs.clustered_points(sample_points, s=0.05)
+    else:
+        x = inputs.uniform_points(sample_points)
+    f = inputs.uniform_values(sample_points)
+    t0 = time.perf_counter()
+    g = oracle.spread(x, f, n, M_WINDOW, SIGMA)
+    t1 = time.perf_counter()
+    tf = None
+    if fft_once:
+        t2 = time.perf_counter()
+        oracle.deconvolve_crop(oracle.fft_grid(g), N, M_WINDOW, SIGMA)
+        tf = time.perf_counter() - t2
+    return (t1 - t0) / sample_points, tf
+
+
+def cpu_baseline(cfg, dist_kind):
+    sample = 100000
+    t_pp, t_fft = _oracle_timing(cfg, dist_kind, sample)
+    t_est = t_pp * cfg["M"] + t_fft
+    return {"value": cfg["M"] / t_est, "unit": "points/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle/ CPU NFFT: serial C spread timed on {sample} of the {cfg['M']} points "
+                      f"({t_pp * 1e6:.2f} us/point, scaled to M) + numpy FFT/deconvolve of the full "
+                      f"grid timed once ({t_fft:.2f} s)",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    sample = 20000
+    # the FFT + deconvolve of the full grid is timed once (warm-up); each step spreads a sample
+    _, t_fft = _oracle_timing(cfg, args.dist, 2000, fft_once=True)
+    for _ in range(args.warmup):
+        _oracle_timing(cfg, args.dist, sample, fft_once=False)
+    per = []
+    for _ in range(args.steps):
+        t_pp, _ = _oracle_timing(cfg, args.dist, sample, fft_once=False)
+        per.append(t_pp)
+    t_pp = statistics.median(per)
+    t_est = t_pp * cfg["M"] + t_fft
+    value = cfg["M"] / t_est
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "points/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_est * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": f"synthetic seeded {args.dist} points (inputs/)",
+        "config": {"workload": f"BASELINE config {args.config}: d=3, N={cfg['N'][0]}^3, M={cfg['M']}, "
+                               f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "kind": "oracle", "cores": 1,
+                         "sample": f"each step: serial C spread of {sample} points (median us/point scaled to "
+                                   f"M={cfg['M']}); FFT+deconvolve of the full grid timed once ({t_fft:.2f} s)"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dist", default="uniform", choices=["uniform", "clustered"])
+    ap.add_argument("--config", default="4", choices=sorted(CONFIGS))
+    ap.add_argument("--method", default="auto", choices=["auto", "atomic", "sweep"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -210,3 +210,23 @@ def test_plan_reuse_and_methods_agree():
     g2 = plan.adjoint(torch.from_numpy(inputs.uniform_values(M, seed=2)).to(dev)).cpu().numpy()
     assert oracle.rel_l2_error(g2, outs[1]) <= 1e-13
     plan.close()
+
+
+@pytest.mark.parametrize("N", [(32, 16, 64), (64, 64, 32), (32, 32, 32), (64, 32, 128)])
+@pytest.mark.parametrize("dist", ["uniform", "clustered"])
+def test_sweep_kernel_explicit(N, dist):
+    """The sweep spread kernel (the bench's kernel) forced on, several CTA patches and segments."""
+    M = 30011
+    x = inputs.uniform_points(M, seed=12) if dist == "uniform" else inputs.clustered_points(M, s=0.02, seed=12)
+    f = inputs.uniform_values(M, seed=12)
+    g = gpu_adjoint(x, f, N, method="sweep")
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+def test_sweep_dense_batches_overflow():
+    """Very dense clusters: one plane holds more candidates than a shared-memory batch."""
+    N, M = (32, 32, 64), 300000
+    x = inputs.clustered_points(M, K=2, s=0.004, seed=13)
+    f = inputs.uniform_values(M, seed=13)
+    g = gpu_adjoint(x, f, N, method="sweep")
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12

@@ -1,0 +1,31 @@
+"""One warm-up + one profiled pass of the hot path at a BASELINE config (for ncu captures)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import inputs.device as idev  # noqa: E402
+import paper_2001_01583_b200 as hp  # noqa: E402
+
+CONFIGS = {"3": ((128,) * 3, 10 ** 6), "4": ((256,) * 3, 10 ** 7), "5": ((512,) * 3, 10 ** 8)}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="4")
+ap.add_argument("--dist", default="uniform")
+ap.add_argument("--method", default="auto")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+N, M = CONFIGS[a.config]
+dev = torch.device("cuda", 0)
+x = idev.uniform_points(M, device=dev) if a.dist == "uniform" else idev.clustered_points(M, device=dev)
+f = idev.uniform_values(M, device=dev)
+plan = hp.Plan(N, M, device=dev)
+plan.set_spread_method(a.method)
+for _ in range(a.reps):
+    plan.set_points(x)
+    out = plan.adjoint(f)
+torch.cuda.synchronize()
+print("ok", float(out.abs().sum()))
