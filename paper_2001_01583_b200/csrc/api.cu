@@ -6,6 +6,7 @@
 //   hpnfft_adjoint    : spread (spread_sweep.cu / spread_atomic.cu)
 //                       -> FFT pass z -> pass y -> pass x + deconvolve    (fft.cu)
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -73,6 +74,8 @@ static void free_plan(Plan* p) {
   cudaFree(p->perm);
   cudaFree(p->xs);
   cudaFree(p->scan_tmp);
+  cudaFree(p->rec);
+  cudaFree(p->group_rows);
   cudaFree(p->err_flag);
   if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
@@ -204,6 +207,34 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     }
   }
   p->bufB = p->grid;   // pass y output reuses the grid (dead after pass z)
+  // records for the sweep spread: all M points if they fit in half of the free memory,
+  // otherwise groups of points processed one after another
+  if (!rc) {
+    rc = alloc(p, &p->group_rows, 2);
+    p->rec_group = 1;   // provisional so that sweep_supported() only checks the grid shape
+    p->rec = reinterpret_cast<double*>(1);
+    bool grid_ok = sweep_supported(p);
+    p->rec = nullptr;
+    p->rec_group = 0;
+    if (!rc && grid_ok) {
+      size_t rb = record_bytes(m);
+      size_t freeb = 0, totalb = 0;
+      cudaMemGetInfo(&freeb, &totalb);
+      int64_t fit = (int64_t)((freeb / 2) / rb);
+      int64_t want = M > 0 ? M : 1;
+      int64_t g = want < fit ? want : fit;
+      const char* env = getenv("HPNFFT_REC_GROUP");
+      if (env && atoll(env) > 0 && atoll(env) < g) g = atoll(env);
+      if (g >= 1024 || g == want) {
+        if (alloc(p, &p->rec, (size_t)g * (rb / sizeof(double))) == HPNFFT_OK) {
+          p->rec_group = g;
+        } else {
+          p->rec = nullptr;   // the atomic spread is used instead
+          set_error("no error");
+        }
+      }
+    }
+  }
   if (!rc) rc = build_tables(p);
   if (rc) {
     free_plan(p);

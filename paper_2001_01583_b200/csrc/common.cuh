@@ -52,6 +52,9 @@ struct Plan {
   double* xs = nullptr;           // [M][3] sorted coordinates
   void* scan_tmp = nullptr;       // block sums for the scan
   int64_t scan_tmp_elems = 0;
+  double* rec = nullptr;          // point records for the sweep spread [rec_group][6 + 6m]
+  int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
+  int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep
   int* err_flag = nullptr;        // device range-error flag
   int* err_flag_host = nullptr;   // pinned mirror
   size_t ws_bytes = 0;
@@ -83,6 +86,7 @@ int sort_points(Plan* p, const double* x);
 int spread_atomic(Plan* p, const double* f);
 int spread_sweep(Plan* p, const double* f);
 bool sweep_supported(const Plan* p);
+size_t record_bytes(int m);
 int fft_and_deconvolve(Plan* p, double* fhat);
 
 }  // namespace hpnfft

@@ -1,22 +1,31 @@
-// spread_sweep.cu -- the B200 spreading kernel (A3 + A4 of SURVEY.md §8(a)).
+// spread_sweep.cu -- the B200 spreading path (A3 + A4 of SURVEY.md §8(a)).
 //
 // Computes the "Spreading" step of CUNFFT (Fig. 1; §3)
 //     g(l) = sum_j f_j * prod_t Phi(n_t x_jt - l_t),   l in I_n (periodic),
-// without atomics and without a zero fill: every grid node is written exactly once.
+// without atomics and (for a single point group) without a zero fill: every grid node is
+// written exactly once.
 //
-// Design: a CTA owns a P1 x P2 patch of grid columns (l1, l2) and a segment
-// of S planes along l0.  Each lane owns ONE column and keeps a sliding window of the 2m nodes
-// l0 = cur-m+1 .. cur+m of that column in registers.  The CTA sweeps cur over the planes; all
-// points whose cell c0 equals cur contribute to exactly the 2m window registers (static register
-// indices, no dynamic addressing), so the 2(2m)^3 FMAs of a point become 2m FMA pairs per active
-// lane.  After the points of plane cur are applied, node cur-m+1 is final and is stored once
-// (coalesced: a warp covers 4 rows x 8 consecutive l2), then the window shifts by one plane.
-// The points of plane cur are found through the bin table of sort.cu: bins are (c1 row, 8
-// consecutive c2, c0 plane) with c0 fastest, so for each (row, c2-bin) "pencil" around the patch
-// the points of plane cur are one contiguous range.  Per batch of planes the CTA stages the
-// candidate points in shared memory: cell, t, f and the 3 x 2m tap weights (computed once per
-// CTA from the window polynomials), and each warp compacts the records whose 2m x 2m footprint
-// touches its 4 x 8 sub-patch into its own ordered list.
+// Two kernels:
+//  k_point_records  one thread per sorted point: cell (c1, c2), f_j, and the 3 x 2m tap weights
+//                   from the window polynomials -> a 16-byte aligned record in HBM (A3).
+//  k_spread_sweep   a CTA owns a P1 x P2 patch of grid columns (l1, l2) and a segment of S planes
+//                   along l0.  Each lane owns ONE column and keeps a sliding window of the 2m nodes
+//                   l0 = cur-m+1 .. cur+m of that column in registers.  The CTA sweeps cur over the
+//                   planes; every point whose cell c0 equals cur adds f w1[i1] w2[i2] w0[i] to the
+//                   2m window registers (static register indices), i.e. the 2(2m)^3 FMAs of a
+//                   point become 2m FMA pairs on each lane of its footprint.  After plane cur, node
+//                   cur-m+1 is final and stored once (a warp covers 4 rows x 8 consecutive l2:
+//                   coalesced 128-byte rows), then the window shifts by one plane.
+// The points of plane cur come from the bin table of sort.cu: bins are (c1 row, 8 consecutive
+// c2, c0 plane) with c0 fastest, so for each (row, c2-bin) pencil around the patch the points of
+// plane cur are one contiguous range of sorted records.  Per batch of planes the CTA copies those
+// records to shared memory; each warp compacts the records whose 2m x 2m footprint touches its
+// 4 x 8 sub-patch into its own plane-ordered list and applies them.
+// When the records of all M points do not fit in the workspace, the sorted points are processed
+// in groups ("the mass data have to be divided into several groups"): the grid is
+// zeroed once and every group's sweep accumulates (CTAs whose rows miss the group exit early).
+#include <stdlib.h>
+
 #include "spread_common.cuh"
 
 namespace hpnfft {
@@ -27,6 +36,17 @@ constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 8 cols (l2) = 3
 constexpr int kWC = 8;
 constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 constexpr int kChunk = 8;       // planes whose pencil ranges are looked up together
+
+// record layout in doubles: [0] c1|c2 (int2)  [1] pad  [2..3] f  [4..4+W) w0
+//                           [4+W .. 5+2W) w1 (+ zero pad)  [5+2W .. 6+3W) w2 (+ zero pad)
+template <int W>
+struct Rec {
+  static constexpr int kW0 = 4;
+  static constexpr int kW1 = 4 + W;
+  static constexpr int kW2 = 5 + 2 * W;
+  static constexpr int kDoubles = 6 + 3 * W;      // even -> 16-byte multiple
+  static constexpr int kChunks16 = kDoubles / 2;
+};
 
 template <int P1, int P2, int M_>
 struct SweepCfg {
@@ -49,12 +69,12 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 }
 
 struct SweepParams {
-  const double* xs;        // sorted coordinates [M][3]
-  const uint32_t* perm;    // sorted -> original
-  const double* f;         // values, original order [M][2]
+  const double* rec;       // point records of the group (record r = sorted point g0 + r)
   const uint32_t* start;   // bin_start [nbins + 1]
-  const double* poly;      // [2m][kPolyDeg+1]
   double* grid;            // [n0][n1][n2] complex
+  const int* rows;         // [2] c1 rows spanned by the group (multi-group pass only)
+  uint32_t g0, g1;         // sorted point range of this group
+  int accumulate;          // 1: grid += window (multi-group), 0: grid = window
   int n0, n1, n2;
   int nb2;                 // n2 / 8
   int seg;                 // S: planes per segment
@@ -64,52 +84,124 @@ struct SweepParams {
 
 }  // namespace
 
+// ------------------------------------------------------------------------------------------
+// A3: point records.  Thread (k, i) evaluates tap i of sorted point g0 + k in the three dimensions
+// (coefficients of tap i in registers, 3 independent Horner chains); tap 0 also writes the cell,
+// f_j and the zero pads.
+template <int M_>
+__global__ void __launch_bounds__(256) k_point_records(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
+                                                        const double* __restrict__ f, const double* __restrict__ poly_g,
+                                                        double* __restrict__ rec, uint32_t g0, uint32_t count,
+                                                        int64_t n0, int64_t n1, int64_t n2) {
+  constexpr int W = 2 * M_;
+  constexpr int PD = kPolyDeg + 1;
+  using R = Rec<W>;
+  __shared__ double poly[W * PD];
+  for (int e = threadIdx.x; e < W * PD; e += blockDim.x) poly[e] = poly_g[e];
+  __syncthreads();
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)count * W) return;
+  const uint32_t k = (uint32_t)(gid / W);
+  const int i = (int)(gid - (uint64_t)k * W);
+  const size_t src = (size_t)g0 + k;
+  double* out = rec + (size_t)k * R::kDoubles;
+  const CellT a0 = cell_of(__ldg(xs + 3 * src), n0);
+  const CellT a1 = cell_of(__ldg(xs + 3 * src + 1), n1);
+  const CellT a2 = cell_of(__ldg(xs + 3 * src + 2), n2);
+  double cf[PD];
+#pragma unroll
+  for (int j = 0; j < PD; ++j) cf[j] = poly[i * PD + j];
+  const double s0 = fma(2.0, a0.t, -1.0), s1 = fma(2.0, a1.t, -1.0), s2 = fma(2.0, a2.t, -1.0);
+  double v0 = cf[PD - 1], v1 = cf[PD - 1], v2 = cf[PD - 1];
+#pragma unroll
+  for (int j = PD - 2; j >= 0; --j) {
+    v0 = fma(v0, s0, cf[j]);
+    v1 = fma(v1, s1, cf[j]);
+    v2 = fma(v2, s2, cf[j]);
+  }
+  if (i == W - 1) {   // strict truncation |u - l| < m (Q4)
+    if (a0.t == 0.0) v0 = 0.0;
+    if (a1.t == 0.0) v1 = 0.0;
+    if (a2.t == 0.0) v2 = 0.0;
+  }
+  out[R::kW0 + i] = v0;
+  out[R::kW1 + i] = v1;
+  out[R::kW2 + i] = v2;
+  if (i == 0) {
+    const uint32_t j = __ldg(perm + src);
+    reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, 0, 0);
+    reinterpret_cast<double2*>(out)[1] = __ldg(reinterpret_cast<const double2*>(f) + j);
+    out[R::kW1 + W] = 0.0;
+    out[R::kW2 + W] = 0.0;
+  }
+}
+
+// c1 rows spanned by sorted points [g0, g1): binary search of the bin table (multi-group only).
+__global__ void k_group_rows(const uint32_t* __restrict__ start, int64_t nbins, uint32_t g0, uint32_t g1,
+                             int64_t bins_per_row, int* rows) {
+  const int which = threadIdx.x;   // 0: first point, 1: last point
+  if (which > 1) return;
+  const uint32_t target = which == 0 ? g0 : g1 - 1;
+  int64_t lo = 0, hi = nbins - 1;   // largest bin with start[bin] <= target
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) / 2;
+    if (start[mid] <= target) lo = mid;
+    else hi = mid - 1;
+  }
+  rows[which] = (int)(lo / bins_per_row);
+}
+
+// ------------------------------------------------------------------------------------------
 template <int P1, int P2, int M_>
-__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sweep(SweepParams prm) {
+__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, (SweepCfg<P1, P2, M_>::kThreads <= 256 ? 2 : 1))
+k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
+  using R = Rec<2 * M_>;
   constexpr int W = C::W;
   constexpr int NT = C::kThreads;
-  constexpr int NP = C::kPencils;
   constexpr int NE = C::kEntries;
   constexpr int NW = C::kWarps;
-  constexpr int PD = kPolyDeg + 1;
+  constexpr int RD = R::kDoubles;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // ---- shared-memory carve-up ----
-  double* s_poly = reinterpret_cast<double*>(smem_raw);                 // [W][PD]
-  double* s_w = s_poly + W * PD;                                        // [cap][3][W] weights
-  double2* s_f = reinterpret_cast<double2*>(s_w + (size_t)prm.cap * 3 * W);   // [cap]
-  double* s_t = reinterpret_cast<double*>(s_f + prm.cap);               // [cap][3]
-  int* s_c = reinterpret_cast<int*>(s_t + (size_t)prm.cap * 3);         // [cap][2] (c1, c2)
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_c + (size_t)prm.cap * 2);   // [cap] sorted point index
-  uint16_t* s_step = reinterpret_cast<uint16_t*>(s_idx + prm.cap);      // [cap] plane (relative)
-  uint16_t* s_list = s_step + prm.cap;                                  // [NW][cap] per-warp lists
-  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_list + (size_t)NW * prm.cap + ((NW * prm.cap) & 1));
-  uint32_t* s_off = s_beg + NE;                                         // exclusive offsets
-  uint32_t* s_misc = s_off + NE;                                        // [32] scan scratch + totals
+  double* s_rec = reinterpret_cast<double*>(smem_raw);                          // [cap][RD]
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_rec + (size_t)prm.cap * RD);  // [cap] record index
+  uint16_t* s_step = reinterpret_cast<uint16_t*>(s_idx + prm.cap);              // [cap] plane
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(s_step + prm.cap);             // [NW][cap]
+  uint32_t* s_beg = s_list + (size_t)NW * prm.cap;                              // [NE]
+  uint32_t* s_off = s_beg + NE;                                                 // [NE]
+  uint32_t* s_misc = s_off + NE;                                                // [40]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
 
   // CTA -> (patch row block, patch col block, segment)
   const int npc = n2 / P2;
-  const int npr = n1 / P1;
   int b = blockIdx.x;
   const int segi = b % prm.nseg;
   b /= prm.nseg;
   const int pc = b % npc;
   const int pr = b / npc;
-  (void)npr;
   const int R0 = pr * P1, C0 = pc * P2;
   const int L0 = segi * prm.seg;
   const int nsteps = prm.seg + W - 1;            // planes cur = L0 - m .. L0 + S + m - 2
   const int first = L0 - M_;
+
+  // multi-group pass: skip CTAs whose candidate rows [R0 - m, R0 + P1 + m - 2] miss the group
+  if (prm.accumulate) {
+    const int row_lo = prm.rows[0], row_hi = prm.rows[1];
+    const int lo = R0 - M_, hi = R0 + P1 + M_ - 2;
+    bool hit = false;
+    for (int sft = -n1; sft <= n1; sft += n1) hit |= !(hi + sft < row_lo || lo + sft > row_hi);
+    if (!hit) return;
+  }
 
   // this lane's column
   const int wr0 = R0 + (warp / (P2 / kWC)) * kWR;
   const int wc0 = C0 + (warp % (P2 / kWC)) * kWC;
   const int l1 = wr0 + lane / kWC;
   const int l2 = wc0 + lane % kWC;
+  const int lo1 = l1 + M_ - 1, lo2 = l2 + M_ - 1;   // tap index = (l - c + m - 1) mod n
 
   // candidate pencils: rows c1 = R0 - m + r (r < kRows), bins b2 = b2lo + q (q < nq)
   const int b2lo = (C0 - M_ >= 0) ? (C0 - M_) / kBinW : -((M_ - C0 + kBinW - 1) / kBinW);
@@ -117,19 +209,27 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
   const int nq = b2hi - b2lo + 1;
   const int np_used = C::kRows * nq;
 
-  for (int e = tid; e < W * PD; e += NT) s_poly[e] = prm.poly[e];
-
   double2 acc[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
   int cur = 0;   // relative plane of the window (warp-uniform)
+  double2* gcol = reinterpret_cast<double2*>(prm.grid) + (size_t)l1 * n2 + l2;
+  const size_t plane = (size_t)n1 * n2;
 
   // flush node of plane `cur` (relative) and shift the window by one plane
   auto advance = [&](int upto) {
     while (cur < upto) {
       if (cur >= W - 1) {
-        int l0 = (first + cur - M_ + 1) & (n0 - 1);
-        reinterpret_cast<double2*>(prm.grid)[((size_t)l0 * n1 + l1) * n2 + l2] = acc[0];
+        const int l0 = (first + cur - M_ + 1) & (n0 - 1);
+        double2* dst = gcol + (size_t)l0 * plane;
+        if (prm.accumulate) {
+          double2 o = *dst;
+          o.x += acc[0].x;
+          o.y += acc[0].y;
+          *dst = o;
+        } else {
+          *dst = acc[0];
+        }
       }
 #pragma unroll
       for (int i = 0; i < W - 1; ++i) acc[i] = acc[i + 1];
@@ -140,49 +240,52 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
 
   for (int ch0 = 0; ch0 < nsteps; ch0 += kChunk) {
     const int nch = min(kChunk, nsteps - ch0);
-    // ---- A: (plane, pencil) ranges of this chunk ----
+    // ---- A: (plane, pencil) ranges of this chunk, clipped to the group ----
     __syncthreads();
     for (int e = tid; e < kChunk * np_used; e += NT) {
-      int s = e / np_used, p = e % np_used;
+      const int s = e / np_used, p = e % np_used;
       uint32_t beg = 0, cnt = 0;
       if (s < nch) {
-        int r = p / nq, q = p % nq;
-        int c1 = (R0 - M_ + r) & (n1 - 1);
+        const int r = p / nq, q = p % nq;
+        const int c1 = (R0 - M_ + r) & (n1 - 1);
         int b2 = (b2lo + q) % prm.nb2;
         if (b2 < 0) b2 += prm.nb2;
-        int c0 = (first + ch0 + s) & (n0 - 1);
-        size_t bin = ((size_t)c1 * prm.nb2 + b2) * n0 + c0;
-        beg = __ldg(prm.start + bin);
-        cnt = __ldg(prm.start + bin + 1) - beg;
+        const int c0 = (first + ch0 + s) & (n0 - 1);
+        const size_t bin = ((size_t)c1 * prm.nb2 + b2) * n0 + c0;
+        uint32_t lo = __ldg(prm.start + bin), hi = __ldg(prm.start + bin + 1);
+        lo = max(lo, prm.g0);
+        hi = min(hi, prm.g1);
+        beg = lo - prm.g0;
+        cnt = hi > lo ? hi - lo : 0u;
       }
       s_beg[e] = beg;
       s_off[e] = cnt;
     }
     __syncthreads();
     // exclusive scan of the counts in (plane-major, pencil-minor) order
+    const int ne = kChunk * np_used;
+    const int per = (ne + NT - 1) / NT;
     {
-      const int ne = kChunk * np_used;
-      const int per = (ne + NT - 1) / NT;
       uint32_t local = 0;
       for (int k = 0; k < per; ++k) {
-        int e = tid * per + k;
+        const int e = tid * per + k;
         if (e < ne) local += s_off[e];
       }
-      uint32_t incl = warp_incl_scan(local, lane);
+      const uint32_t incl = warp_incl_scan(local, lane);
       if (lane == 31) s_misc[warp] = incl;
       __syncthreads();
       if (warp == 0) {
-        uint32_t v = (lane < NW) ? s_misc[lane] : 0u;
-        uint32_t vi = warp_incl_scan(v, lane);
+        const uint32_t v = (lane < NW) ? s_misc[lane] : 0u;
+        const uint32_t vi = warp_incl_scan(v, lane);
         if (lane < NW) s_misc[lane] = vi - v;
         if (lane == 31) s_misc[32] = vi;
       }
       __syncthreads();
       uint32_t run = s_misc[warp] + incl - local;
       for (int k = 0; k < per; ++k) {
-        int e = tid * per + k;
+        const int e = tid * per + k;
         if (e < ne) {
-          uint32_t c = s_off[e];
+          const uint32_t c = s_off[e];
           s_off[e] = run;
           run += c;
         }
@@ -194,91 +297,98 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
     for (uint32_t b0 = 0; b0 < total; b0 += prm.cap) {
       const uint32_t b1 = min(total, b0 + (uint32_t)prm.cap);
       const int B = (int)(b1 - b0);
-      // ---- B: record -> sorted point index and plane ----
+      // ---- B: batch slot -> record index and plane ----
+      for (int k = 0; k < per; ++k) {
+        const int e = tid * per + k;
+        if (e >= ne) break;
+        const uint32_t off = s_off[e];
+        const uint32_t cnt = (e + 1 < ne ? s_off[e + 1] : total) - off;
+        if (cnt == 0 || off >= b1 || off + cnt <= b0) continue;
+        const uint32_t beg = s_beg[e];
+        const uint32_t k0 = off < b0 ? b0 - off : 0u;
+        const uint32_t k1 = min(cnt, b1 - off);
+        const uint16_t step = (uint16_t)(ch0 + e / np_used);
+        for (uint32_t kk = k0; kk < k1; ++kk) {
+          s_idx[off + kk - b0] = beg + kk;
+          s_step[off + kk - b0] = step;
+        }
+      }
+      __syncthreads();
+      // ---- C: copy the batch's records to shared memory (16-byte chunks, coalesced per record) ----
       {
-        const int ne = kChunk * np_used;
-        const int per = (ne + NT - 1) / NT;
-        for (int k = 0; k < per; ++k) {
-          int e = tid * per + k;
-          if (e >= ne) break;
-          uint32_t off = s_off[e];
-          uint32_t cnt = (e + 1 < ne ? s_off[e + 1] : total) - off;
-          if (cnt == 0 || off >= b1 || off + cnt <= b0) continue;
-          uint32_t beg = s_beg[e];
-          uint32_t k0 = off < b0 ? b0 - off : 0u;
-          uint32_t k1 = min(cnt, b1 - off);
-          uint16_t step = (uint16_t)(ch0 + e / np_used);
-          for (uint32_t kk = k0; kk < k1; ++kk) {
-            s_idx[off + kk - b0] = beg + kk;
-            s_step[off + kk - b0] = step;
-          }
+        const int nchunk = B * R::kChunks16;
+        const double2* gsrc = reinterpret_cast<const double2*>(prm.rec);
+        double2* sdst = reinterpret_cast<double2*>(s_rec);
+        for (int c = tid; c < nchunk; c += NT) {
+          const int e = c / R::kChunks16, part = c - e * R::kChunks16;
+          sdst[c] = __ldg(gsrc + (size_t)s_idx[e] * R::kChunks16 + part);
         }
       }
       __syncthreads();
-      // ---- C: per record cell, t, f ----
-      for (int e = tid; e < B; e += NT) {
-        uint32_t k = s_idx[e];
-        CellT a0 = cell_of(__ldg(prm.xs + 3 * (size_t)k), n0);
-        CellT a1 = cell_of(__ldg(prm.xs + 3 * (size_t)k + 1), n1);
-        CellT a2 = cell_of(__ldg(prm.xs + 3 * (size_t)k + 2), n2);
-        (void)a0.c;
-        s_t[3 * e] = a0.t;
-        s_t[3 * e + 1] = a1.t;
-        s_t[3 * e + 2] = a2.t;
-        s_c[2 * e] = a1.c;
-        s_c[2 * e + 1] = a2.c;
-        uint32_t src = __ldg(prm.perm + k);
-        s_f[e] = __ldg(reinterpret_cast<const double2*>(prm.f) + src);
-      }
-      __syncthreads();
-      // ---- D: tap weights (w0 all taps; w1/w2 only taps landing inside the patch) ----
-      for (int e = tid; e < B * 3 * W; e += NT) {
-        int rec = e / (3 * W), r = e % (3 * W), d = r / W, i = r % W;
-        bool need = true;
-        if (d == 1) {
-          int l = (s_c[2 * rec] - M_ + 1 + i - R0) & (n1 - 1);
-          need = l < P1;
-        } else if (d == 2) {
-          int l = (s_c[2 * rec + 1] - M_ + 1 + i - C0) & (n2 - 1);
-          need = l < P2;
-        }
-        if (need) s_w[(size_t)rec * 3 * W + d * W + i] = tap_weight(s_poly, i, s_t[3 * rec + d], M_);
-      }
-      __syncthreads();
-      // ---- E: this warp's ordered list of records touching its 4 x 8 sub-patch ----
+      // ---- E: this warp's plane-ordered list of records touching its 4 x 8 sub-patch ----
       int nlist = 0;
-      uint16_t* my = s_list + (size_t)warp * prm.cap;
+      uint32_t* my = s_list + (size_t)warp * prm.cap;
       for (int base = 0; base < B; base += 32) {
-        int e = base + lane;
+        const int e = base + lane;
         bool rel = false;
         if (e < B) {
-          int c1 = s_c[2 * e], c2 = s_c[2 * e + 1];
-          int d1 = (wr0 - (c1 - M_ + 1) + (kWR - 1)) & (n1 - 1);
-          int d2 = (wc0 - (c2 - M_ + 1) + (kWC - 1)) & (n2 - 1);
+          const int2 cc = *reinterpret_cast<const int2*>(s_rec + (size_t)e * RD);
+          const int d1 = (wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1);
+          const int d2 = (wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1);
           rel = (d1 < W + kWR - 1) && (d2 < W + kWC - 1);
         }
-        unsigned bal = __ballot_sync(0xffffffffu, rel);
-        if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint16_t)e;
+        const unsigned bal = __ballot_sync(0xffffffffu, rel);
+        if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint32_t)e | ((uint32_t)s_step[e] << 16);
         nlist += __popc(bal);
       }
       __syncwarp();
-      // ---- F: apply the records to the register windows ----
-      for (int k = 0; k < nlist; ++k) {
-        int e = my[k];
-        advance((int)s_step[e]);
-        int c1 = s_c[2 * e], c2 = s_c[2 * e + 1];
-        unsigned i1 = (unsigned)((l1 - c1 + M_ - 1) & (n1 - 1));
-        unsigned i2 = (unsigned)((l2 - c2 + M_ - 1) & (n2 - 1));
-        if (i1 < (unsigned)W && i2 < (unsigned)W) {
-          const double* w = s_w + (size_t)e * 3 * W;
-          double2 fv = s_f[e];
-          double w12 = w[W + i1] * w[2 * W + i2];
-          double cr = fv.x * w12, ci = fv.y * w12;
+      // ---- F: apply the records plane by plane; the window shifts only between planes.
+      //      Records of one plane are taken two at a time so their shared-memory loads overlap. ----
+      if (nlist > 0) {
+        auto coef = [&](int e, double& cr, double& ci) {
+          const double* r = s_rec + (size_t)e * RD;
+          const int2 cc = *reinterpret_cast<const int2*>(r);
+          const unsigned i1 = min((unsigned)((lo1 - cc.x) & (n1 - 1)), (unsigned)W);
+          const unsigned i2 = min((unsigned)((lo2 - cc.y) & (n2 - 1)), (unsigned)W);
+          const double2 fv = *reinterpret_cast<const double2*>(r + 2);
+          const double w12 = r[R::kW1 + i1] * r[R::kW2 + i2];
+          cr = fv.x * w12;
+          ci = fv.y * w12;
+        };
+        int k = 0;
+        uint32_t ent = my[0];
+        while (k < nlist) {
+          const int st = (int)(ent >> 16);
+          advance(st);
+          for (;;) {
+            const int ea = (int)(ent & 0xffffu);
+            ++k;
+            ent = (k < nlist) ? my[k] : 0xffffffffu;
+            const bool pair = (int)(ent >> 16) == st && k < nlist;
+            const int eb = pair ? (int)(ent & 0xffffu) : ea;
+            if (pair) {
+              ++k;
+              ent = (k < nlist) ? my[k] : 0xffffffffu;
+            }
+            double ar, ai, br, bi;
+            coef(ea, ar, ai);
+            coef(eb, br, bi);
+            if (!pair) {
+              br = 0.0;
+              bi = 0.0;
+            }
+            const double* wa = s_rec + (size_t)ea * RD + R::kW0;
+            const double* wb = s_rec + (size_t)eb * RD + R::kW0;
 #pragma unroll
-          for (int i = 0; i < W; ++i) {
-            double w0 = w[i];
-            acc[i].x = fma(cr, w0, acc[i].x);
-            acc[i].y = fma(ci, w0, acc[i].y);
+            for (int i = 0; i < W; i += 2) {
+              const double2 xa = *reinterpret_cast<const double2*>(wa + i);
+              const double2 xb = *reinterpret_cast<const double2*>(wb + i);
+              acc[i].x = fma(br, xb.x, fma(ar, xa.x, acc[i].x));
+              acc[i].y = fma(bi, xb.x, fma(ai, xa.x, acc[i].y));
+              acc[i + 1].x = fma(br, xb.y, fma(ar, xa.y, acc[i + 1].x));
+              acc[i + 1].y = fma(bi, xb.y, fma(ai, xa.y, acc[i + 1].y));
+            }
+            if (!((int)(ent >> 16) == st && k < nlist)) break;
           }
         }
       }
@@ -294,33 +404,39 @@ template <int P1, int P2, int M_>
 size_t sweep_smem_bytes(int cap) {
   using C = SweepCfg<P1, P2, M_>;
   size_t b = 0;
-  b += sizeof(double) * C::W * (kPolyDeg + 1);
-  b += sizeof(double) * (size_t)cap * 3 * C::W;
-  b += sizeof(double2) * cap;
-  b += sizeof(double) * (size_t)cap * 3;
-  b += sizeof(int) * (size_t)cap * 2;
+  b += sizeof(double) * (size_t)cap * Rec<2 * M_>::kDoubles;
   b += sizeof(uint32_t) * cap;
   b += sizeof(uint16_t) * cap;
-  b += sizeof(uint16_t) * ((size_t)C::kWarps * cap + 1);
+  b += sizeof(uint32_t) * ((size_t)C::kWarps * cap);
   b += sizeof(uint32_t) * (2 * C::kEntries + 40);
   return b + 64;
 }
 
+// CTA patch variant: 0 = 16 x 32 (512 threads, 1 CTA/SM), 1 = 16 x 16 (256 threads, 2 CTAs/SM).
+int sweep_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HPNFFT_SWEEP_PATCH");
+    v = (e && e[0] == '1' && e[1] == '6' && e[2] == 'x' && e[3] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 template <int P1, int P2, int M_>
-int launch_sweep(Plan* p, const double* f) {
+int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool accumulate) {
   using C = SweepCfg<P1, P2, M_>;
-  const size_t smem_max = 227 * 1024;
-  // largest record capacity that fits the shared memory
+  const size_t smem_max = C::kThreads <= 256 ? (size_t)(113 * 1024) : (size_t)(227 * 1024);
   int cap = 64;
   while (sweep_smem_bytes<P1, P2, M_>(cap + 64) <= smem_max) cap += 64;
-  size_t smem = sweep_smem_bytes<P1, P2, M_>(cap);
+  const size_t smem = sweep_smem_bytes<P1, P2, M_>(cap);
   SweepParams prm;
-  prm.xs = p->xs;
-  prm.perm = p->perm;
-  prm.f = f;
+  prm.rec = p->rec;
   prm.start = p->bin_count;
-  prm.poly = p->poly;
   prm.grid = p->grid;
+  prm.rows = rows;
+  prm.g0 = g0;
+  prm.g1 = g1;
+  prm.accumulate = accumulate ? 1 : 0;
   prm.n0 = (int)p->n[0];
   prm.n1 = (int)p->n[1];
   prm.n2 = (int)p->n[2];
@@ -331,36 +447,72 @@ int launch_sweep(Plan* p, const double* f) {
   auto kern = k_spread_sweep<P1, P2, M_>;
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                   "sweep smem attr");
-  int64_t blocks = (p->n[1] / P1) * (p->n[2] / P2) * prm.nseg;
+  const int64_t blocks = (p->n[1] / P1) * (p->n[2] / P2) * prm.nseg;
   kern<<<(unsigned)blocks, C::kThreads, smem, p->stream>>>(prm);
   p->launches++;
   return check_launch(p, "spread_sweep");
 }
 
-constexpr int kP1 = 16, kP2 = 32;
+template <int M_>
+int run_sweep(Plan* p, const double* f) {
+  const uint32_t M = (uint32_t)p->M;
+  const uint32_t G = (uint32_t)p->rec_group;
+  const bool multi = M > G;
+  if (multi) {
+    const size_t bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
+    HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->grid, 0, bytes, p->stream), "zero grid");
+  }
+  uint32_t g0 = 0;
+  do {
+    const uint32_t g1 = (M - g0) < G ? M : g0 + G;
+    const uint32_t cnt = g1 - g0;
+    if (cnt > 0) {
+      const uint64_t threads = (uint64_t)cnt * (2 * M_);
+      k_point_records<M_><<<(unsigned)((threads + 255) / 256), 256, 0, p->stream>>>(
+          p->xs, p->perm, f, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
+      p->launches++;
+      int rc = check_launch(p, "point records");
+      if (rc) return rc;
+    }
+    if (multi) {
+      k_group_rows<<<1, 32, 0, p->stream>>>(p->bin_count, p->nbins, g0, g1, (p->n[2] / kBinW) * p->n[0],
+                                            p->group_rows);
+      p->launches++;
+    }
+    int rc = sweep_variant() == 1 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
+                                  : launch_sweep_group<16, 32, M_>(p, g0, g1, p->group_rows, multi);
+    if (rc) return rc;
+    g0 = g1;
+  } while (g0 < M);
+  return HPNFFT_OK;
+}
 
 }  // namespace
 
+size_t record_bytes(int m) { return sizeof(double) * (6 + 3 * 2 * m); }
+
 bool sweep_supported(const Plan* p) {
   const int W = 2 * p->m;
-  if (p->n[2] < kP2 || p->n[1] < kP1) return false;
-  if (p->n[1] < kP1 + W - 1) return false;                    // candidate rows must be distinct
-  int b2lo_span = (kP2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
-  if (p->n[2] / kBinW < b2lo_span) return false;
+  const int P1 = 16, P2 = 32;   // largest patch of any variant
+  if (p->n[2] < P2 || p->n[1] < P1) return false;
+  if (p->n[1] < P1 + W - 1) return false;                     // candidate rows must be distinct
+  const int bins = (P2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
+  if (p->n[2] / kBinW < bins) return false;
   if (p->n[0] < W) return false;
-  if (p->n[0] > 65535) return false;
+  if (p->n[0] + W > 65535) return false;
+  if (p->rec == nullptr || p->rec_group == 0) return false;
   return true;
 }
 
 int spread_sweep(Plan* p, const double* f) {
   switch (p->m) {
-    case 2: return launch_sweep<kP1, kP2, 2>(p, f);
-    case 3: return launch_sweep<kP1, kP2, 3>(p, f);
-    case 4: return launch_sweep<kP1, kP2, 4>(p, f);
-    case 5: return launch_sweep<kP1, kP2, 5>(p, f);
-    case 6: return launch_sweep<kP1, kP2, 6>(p, f);
-    case 7: return launch_sweep<kP1, kP2, 7>(p, f);
-    case 8: return launch_sweep<kP1, kP2, 8>(p, f);
+    case 2: return run_sweep<2>(p, f);
+    case 3: return run_sweep<3>(p, f);
+    case 4: return run_sweep<4>(p, f);
+    case 5: return run_sweep<5>(p, f);
+    case 6: return run_sweep<6>(p, f);
+    case 7: return run_sweep<7>(p, f);
+    case 8: return run_sweep<8>(p, f);
     default:
       set_error("m not supported by the sweep kernel");
       return HPNFFT_E_UNSUPPORTED;

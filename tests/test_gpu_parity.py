@@ -230,3 +230,15 @@ def test_sweep_dense_batches_overflow():
     f = inputs.uniform_values(M, seed=13)
     g = gpu_adjoint(x, f, N, method="sweep")
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("dist", ["uniform", "clustered"])
+def test_sweep_multi_group_accumulate(dist, monkeypatch):
+    """Points processed in several record groups (PAPER.md:49 'divided into several groups'):
+    the grid is zeroed once and each group's sweep accumulates."""
+    monkeypatch.setenv("HPNFFT_REC_GROUP", "4096")
+    N, M = (32, 32, 64), 30011
+    x = inputs.uniform_points(M, seed=14) if dist == "uniform" else inputs.clustered_points(M, s=0.02, seed=14)
+    f = inputs.uniform_values(M, seed=14)
+    g = gpu_adjoint(x, f, N, method="sweep")
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12

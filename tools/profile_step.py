@@ -17,6 +17,7 @@ ap.add_argument("--config", default="4")
 ap.add_argument("--dist", default="uniform")
 ap.add_argument("--method", default="auto")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--timing", action="store_true")
 a = ap.parse_args()
 N, M = CONFIGS[a.config]
 dev = torch.device("cuda", 0)
@@ -24,8 +25,14 @@ x = idev.uniform_points(M, device=dev) if a.dist == "uniform" else idev.clustere
 f = idev.uniform_values(M, device=dev)
 plan = hp.Plan(N, M, device=dev)
 plan.set_spread_method(a.method)
-for _ in range(a.reps):
+ap2 = None
+for r in range(a.reps):
+    if r == a.reps - 1 and a.timing:
+        plan.enable_timing(True)
     plan.set_points(x)
     out = plan.adjoint(f)
 torch.cuda.synchronize()
-print("ok", float(out.abs().sum()))
+msg = {"config": a.config, "dist": a.dist, "patch": os.environ.get("HPNFFT_SWEEP_PATCH", "default")}
+if a.timing:
+    msg.update(plan.stage_times())
+print("ok", float(out.abs().sum()), msg)
