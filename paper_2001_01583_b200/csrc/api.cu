@@ -76,6 +76,7 @@ static void free_plan(Plan* p) {
   cudaFree(p->scan_tmp);
   cudaFree(p->rec);
   cudaFree(p->group_rows);
+  cudaFree(p->tile_counter);
   cudaFree(p->err_flag);
   if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
@@ -211,6 +212,7 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   // otherwise groups of points processed one after another
   if (!rc) {
     rc = alloc(p, &p->group_rows, 2);
+    rc = rc ? rc : alloc(p, &p->tile_counter, 1);
     p->rec_group = 1;   // provisional so that sweep_supported() only checks the grid shape
     p->rec = reinterpret_cast<double*>(1);
     bool grid_ok = sweep_supported(p);

@@ -55,6 +55,7 @@ struct Plan {
   double* rec = nullptr;          // point records for the sweep spread [rec_group][6 + 6m]
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
   int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep
+  int* tile_counter = nullptr;    // sweep tile scheduler counter
   int* err_flag = nullptr;        // device range-error flag
   int* err_flag_host = nullptr;   // pinned mirror
   size_t ws_bytes = 0;

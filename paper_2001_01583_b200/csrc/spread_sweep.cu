@@ -79,7 +79,8 @@ struct SweepParams {
   int nb2;                 // n2 / 8
   int seg;                 // S: planes per segment
   int nseg;                // n0 / S
-  int cap;                 // record capacity of the shared-memory batch
+  int cap;                 // record capacity of one shared-memory batch buffer
+  int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
 };
 
 }  // namespace
@@ -152,74 +153,245 @@ __global__ void k_group_rows(const uint32_t* __restrict__ start, int64_t nbins, 
 }
 
 // ------------------------------------------------------------------------------------------
+// Warp-specialised persistent sweep.  NW consumer warps own the 4 x 8 sub-patches of the CTA's
+// P1 x P2 patch; NP producer warps fetch tiles (patch x segment) from a global counter, look up
+// the (plane, pencil) ranges and stage batches of records into an NS-stage shared-memory ring with
+// cp.async.  Stages are handed over with mbarriers (full: producer threads arrive; empty: one
+// arrival per consumer warp), so consumer warps never wait for each other or for global memory.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void producer_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
+
+struct BatchHdr {
+  int B;      // records in the batch; -1 terminates
+  int tile;   // tile id
+  int end;    // 1: last batch of the tile (flush), 2: tile skipped in this group pass
+  int pad;
+};
+
 template <int P1, int P2, int M_>
-__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, (SweepCfg<P1, P2, M_>::kThreads <= 256 ? 2 : 1))
-k_spread_sweep(SweepParams prm) {
+struct SweepLayout {
+  static constexpr int NW = (P1 / kWR) * (P2 / kWC);   // consumer warps
+  static constexpr int NP = 4;                          // producer warps
+  static constexpr int NS = 3;                          // ring stages
+  static constexpr int kThreads = (NW + NP) * 32;
+};
+
+template <int P1, int P2, int M_>
+__global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
+  using L = SweepLayout<P1, P2, M_>;
   using R = Rec<2 * M_>;
   constexpr int W = C::W;
-  constexpr int NT = C::kThreads;
+  constexpr int NW = L::NW, NS = L::NS;
+  constexpr int NPT = L::NP * 32;        // producer threads
   constexpr int NE = C::kEntries;
-  constexpr int NW = C::kWarps;
   constexpr int RD = R::kDoubles;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s_rec = reinterpret_cast<double*>(smem_raw);                          // [cap][RD]
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_rec + (size_t)prm.cap * RD);  // [cap] record index
-  uint16_t* s_step = reinterpret_cast<uint16_t*>(s_idx + prm.cap);              // [cap] plane
-  uint32_t* s_list = reinterpret_cast<uint32_t*>(s_step + prm.cap);             // [NW][cap]
-  uint32_t* s_beg = s_list + (size_t)NW * prm.cap;                              // [NE]
-  uint32_t* s_off = s_beg + NE;                                                 // [NE]
-  uint32_t* s_misc = s_off + NE;                                                // [40]
+  const int cap = prm.cap;
+  double* s_rec = reinterpret_cast<double*>(smem_raw);                            // [NS][cap][RD]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_rec + (size_t)NS * cap * RD);  // [NS]
+  uint64_t* s_empty = s_full + NS;                                                // [NS]
+  BatchHdr* s_hdr = reinterpret_cast<BatchHdr*>(s_empty + NS);                    // [NS]
+  uint16_t* s_step = reinterpret_cast<uint16_t*>(s_hdr + NS);                     // [NS][cap]
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(s_step + NS * cap + (NS * cap & 1));   // [NW][cap]
+  uint32_t* s_idx = s_list + (size_t)NW * cap;                                    // [cap]  producer
+  uint32_t* s_beg = s_idx + cap;                                                  // [NE]   producer
+  uint32_t* s_off = s_beg + NE;                                                   // [NE]   producer
+  uint32_t* s_misc = s_off + NE;                                                  // [16]   producer
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
+  const int npc = n2 / P2, npr = (n1 + P1 - 1) / P1;
+  const int ntiles = npc * npr * prm.nseg;
+  const int nsteps = prm.seg + W - 1;   // planes cur = L0 - m .. L0 + S + m - 2 of a tile
 
-  // CTA -> (patch row block, patch col block, segment)
-  const int npc = n2 / P2;
-  int b = blockIdx.x;
-  const int segi = b % prm.nseg;
-  b /= prm.nseg;
-  const int pc = b % npc;
-  const int pr = b / npc;
-  const int R0 = pr * P1, C0 = pc * P2;
-  const int L0 = segi * prm.seg;
-  const int nsteps = prm.seg + W - 1;            // planes cur = L0 - m .. L0 + S + m - 2
-  const int first = L0 - M_;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&s_full[i], NPT);
+      mbar_init(&s_empty[i], NW);
+    }
+  }
+  __syncthreads();
 
-  // multi-group pass: skip CTAs whose candidate rows [R0 - m, R0 + P1 + m - 2] miss the group
-  if (prm.accumulate) {
+  auto tile_geom = [&](int t, int& R0, int& C0, int& L0) {
+    const int pc = t % npc;
+    const int rest = t / npc;
+    const int pr = rest % npr;
+    const int segi = rest / npr;
+    R0 = pr * P1;
+    C0 = pc * P2;
+    L0 = segi * prm.seg;
+  };
+  auto tile_skip = [&](int R0) -> bool {   // multi-group pass: rows of the tile miss the group
+    if (!prm.accumulate) return false;
     const int row_lo = prm.rows[0], row_hi = prm.rows[1];
     const int lo = R0 - M_, hi = R0 + P1 + M_ - 2;
     bool hit = false;
     for (int sft = -n1; sft <= n1; sft += n1) hit |= !(hi + sft < row_lo || lo + sft > row_hi);
-    if (!hit) return;
+    return !hit;
+  };
+
+  if (warp >= NW) {
+    // =============================== producer warps ===============================
+    const int pt = tid - NW * 32;   // 0 .. NPT-1
+    const int pw = pt >> 5;
+    int stage = 0;
+    uint32_t phase = 0;
+    auto next_stage = [&]() {
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    };
+    for (;;) {
+      if (pt == 0) s_misc[8] = (uint32_t)atomicAdd(prm.tile_counter, 1);
+      producer_bar(NPT);
+      const int t = (int)s_misc[8];
+      producer_bar(NPT);
+      if (t >= ntiles) break;
+      int R0, C0, L0;
+      tile_geom(t, R0, C0, L0);
+      const int first = L0 - M_;
+      const bool skip = tile_skip(R0);
+      if (!skip) {
+        const int b2lo = (C0 - M_ >= 0) ? (C0 - M_) / kBinW : -((M_ - C0 + kBinW - 1) / kBinW);
+        const int b2hi = (C0 + P2 + M_ - 2) / kBinW;
+        const int nq = b2hi - b2lo + 1;
+        const int np_used = C::kRows * nq;
+        for (int ch0 = 0; ch0 < nsteps; ch0 += kChunk) {
+          const int nch = min(kChunk, nsteps - ch0);
+          const int ne = nch * np_used;
+          const int per = (ne + NPT - 1) / NPT;
+          // (plane, pencil) ranges clipped to the group; thread owns entries [pt*per, pt*per+per)
+          uint32_t local = 0;
+          for (int k = 0; k < per; ++k) {
+            const int e = pt * per + k;
+            if (e >= ne) break;
+            const int sidx = e / np_used, pidx = e - sidx * np_used;
+            const int r = pidx / nq, q = pidx - r * nq;
+            const int c1 = (R0 - M_ + r) & (n1 - 1);
+            int b2 = (b2lo + q) % prm.nb2;
+            if (b2 < 0) b2 += prm.nb2;
+            const int c0 = (first + ch0 + sidx) & (n0 - 1);
+            const size_t bin = ((size_t)c1 * prm.nb2 + b2) * n0 + c0;
+            uint32_t lo = __ldg(prm.start + bin), hi = __ldg(prm.start + bin + 1);
+            lo = max(lo, prm.g0);
+            hi = min(hi, prm.g1);
+            const uint32_t cnt = hi > lo ? hi - lo : 0u;
+            s_beg[e] = lo - prm.g0;
+            s_off[e] = cnt;
+            local += cnt;
+          }
+          // exclusive scan over the producer threads
+          const uint32_t incl = warp_incl_scan(local, lane);
+          if (lane == 31) s_misc[pw] = incl;
+          producer_bar(NPT);
+          uint32_t wbase = 0, total = 0;
+#pragma unroll
+          for (int w = 0; w < L::NP; ++w) {
+            const uint32_t v = s_misc[w];
+            wbase += (w < pw) ? v : 0u;
+            total += v;
+          }
+          uint32_t run = wbase + incl - local;
+          for (int k = 0; k < per; ++k) {
+            const int e = pt * per + k;
+            if (e >= ne) break;
+            const uint32_t c = s_off[e];
+            s_off[e] = run;
+            run += c;
+          }
+          producer_bar(NPT);
+          for (uint32_t b0 = 0; b0 < total; b0 += (uint32_t)cap) {
+            const uint32_t b1 = min(total, b0 + (uint32_t)cap);
+            const int B = (int)(b1 - b0);
+            mbar_wait(&s_empty[stage], phase ^ 1u);
+            uint16_t* stp = s_step + stage * cap;
+            for (int k = 0; k < per; ++k) {
+              const int e = pt * per + k;
+              if (e >= ne) break;
+              const uint32_t off = s_off[e];
+              const uint32_t cnt = (e + 1 < ne ? s_off[e + 1] : total) - off;
+              if (cnt == 0 || off >= b1 || off + cnt <= b0) continue;
+              const uint32_t beg = s_beg[e];
+              const uint32_t k0 = off < b0 ? b0 - off : 0u;
+              const uint32_t k1 = min(cnt, b1 - off);
+              const uint16_t step = (uint16_t)(ch0 + e / np_used);
+              for (uint32_t kk = k0; kk < k1; ++kk) {
+                s_idx[off + kk - b0] = beg + kk;
+                stp[off + kk - b0] = step;
+              }
+            }
+            producer_bar(NPT);
+            double* dst = s_rec + (size_t)stage * cap * RD;
+            const int nchunk = B * R::kChunks16;
+            for (int c = pt; c < nchunk; c += NPT) {
+              const int e = c / R::kChunks16, part = c - e * R::kChunks16;
+              cp_async16(dst + 2 * (size_t)c, prm.rec + (size_t)s_idx[e] * RD + 2 * part);
+            }
+            cp_async_wait_all();
+            if (pt == 0) s_hdr[stage] = BatchHdr{B, t, 0, 0};
+            mbar_arrive(&s_full[stage]);
+            next_stage();
+            producer_bar(NPT);   // s_idx is rewritten by the next batch
+          }
+        }
+      }
+      // end-of-tile marker (consumers flush every node of the tile unless it is skipped)
+      mbar_wait(&s_empty[stage], phase ^ 1u);
+      if (pt == 0) s_hdr[stage] = BatchHdr{0, t, skip ? 2 : 1, 0};
+      mbar_arrive(&s_full[stage]);
+      next_stage();
+    }
+    mbar_wait(&s_empty[stage], phase ^ 1u);
+    if (pt == 0) s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
+    mbar_arrive(&s_full[stage]);
+    return;
   }
 
-  // this lane's column
-  const int wr0 = R0 + (warp / (P2 / kWC)) * kWR;
-  const int wc0 = C0 + (warp % (P2 / kWC)) * kWC;
-  const int l1 = wr0 + lane / kWC;
-  const int l2 = wc0 + lane % kWC;
-  const int lo1 = l1 + M_ - 1, lo2 = l2 + M_ - 1;   // tap index = (l - c + m - 1) mod n
-
-  // candidate pencils: rows c1 = R0 - m + r (r < kRows), bins b2 = b2lo + q (q < nq)
-  const int b2lo = (C0 - M_ >= 0) ? (C0 - M_) / kBinW : -((M_ - C0 + kBinW - 1) / kBinW);
-  const int b2hi = (C0 + P2 + M_ - 2) / kBinW;
-  const int nq = b2hi - b2lo + 1;
-  const int np_used = C::kRows * nq;
-
+  // =============================== consumer warps ===============================
+  const int wr_off = (warp / (P2 / kWC)) * kWR;
+  const int wc_off = (warp % (P2 / kWC)) * kWC;
+  int cur_tile = -1;
+  int first = 0, wr0 = 0, wc0 = 0, lo1 = 0, lo2 = 0;
+  bool valid = true;
+  double2* gcol = nullptr;
+  const size_t plane = (size_t)n1 * n2;
   double2 acc[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
-  int cur = 0;   // relative plane of the window (warp-uniform)
-  double2* gcol = reinterpret_cast<double2*>(prm.grid) + (size_t)l1 * n2 + l2;
-  const size_t plane = (size_t)n1 * n2;
+  int cur = 0;
 
-  // flush node of plane `cur` (relative) and shift the window by one plane
   auto advance = [&](int upto) {
     while (cur < upto) {
-      if (cur >= W - 1) {
+      if (cur >= W - 1 && valid) {
         const int l0 = (first + cur - M_ + 1) & (n0 - 1);
         double2* dst = gcol + (size_t)l0 * plane;
         if (prm.accumulate) {
@@ -238,164 +410,107 @@ k_spread_sweep(SweepParams prm) {
     }
   };
 
-  for (int ch0 = 0; ch0 < nsteps; ch0 += kChunk) {
-    const int nch = min(kChunk, nsteps - ch0);
-    // ---- A: (plane, pencil) ranges of this chunk, clipped to the group ----
-    __syncthreads();
-    for (int e = tid; e < kChunk * np_used; e += NT) {
-      const int s = e / np_used, p = e % np_used;
-      uint32_t beg = 0, cnt = 0;
-      if (s < nch) {
-        const int r = p / nq, q = p % nq;
-        const int c1 = (R0 - M_ + r) & (n1 - 1);
-        int b2 = (b2lo + q) % prm.nb2;
-        if (b2 < 0) b2 += prm.nb2;
-        const int c0 = (first + ch0 + s) & (n0 - 1);
-        const size_t bin = ((size_t)c1 * prm.nb2 + b2) * n0 + c0;
-        uint32_t lo = __ldg(prm.start + bin), hi = __ldg(prm.start + bin + 1);
-        lo = max(lo, prm.g0);
-        hi = min(hi, prm.g1);
-        beg = lo - prm.g0;
-        cnt = hi > lo ? hi - lo : 0u;
-      }
-      s_beg[e] = beg;
-      s_off[e] = cnt;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&s_full[stage], phase);
+    const BatchHdr hdr = s_hdr[stage];
+    if (hdr.B < 0) break;
+    if (hdr.tile != cur_tile) {
+      cur_tile = hdr.tile;
+      int R0, C0, L0;
+      tile_geom(cur_tile, R0, C0, L0);
+      first = L0 - M_;
+      wr0 = R0 + wr_off;
+      wc0 = C0 + wc_off;
+      const int l1 = wr0 + lane / kWC;
+      const int l2 = wc0 + lane % kWC;
+      valid = l1 < n1;   // ghost rows of the last row tile when P1 does not divide n1
+      lo1 = l1 + M_ - 1;
+      lo2 = l2 + M_ - 1;
+      gcol = reinterpret_cast<double2*>(prm.grid) + (size_t)(l1 & (n1 - 1)) * n2 + l2;
+      cur = 0;
+#pragma unroll
+      for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
     }
-    __syncthreads();
-    // exclusive scan of the counts in (plane-major, pencil-minor) order
-    const int ne = kChunk * np_used;
-    const int per = (ne + NT - 1) / NT;
-    {
-      uint32_t local = 0;
-      for (int k = 0; k < per; ++k) {
-        const int e = tid * per + k;
-        if (e < ne) local += s_off[e];
+    const int B = hdr.B;
+    const double* recs = s_rec + (size_t)stage * cap * RD;
+    const uint16_t* stp = s_step + stage * cap;
+    // ---- this warp's plane-ordered list of records touching its 4 x 8 sub-patch ----
+    int nlist = 0;
+    uint32_t* my = s_list + (size_t)warp * cap;
+    for (int base = 0; base < B; base += 32) {
+      const int e = base + lane;
+      bool rel = false;
+      if (e < B) {
+        const int2 cc = *reinterpret_cast<const int2*>(recs + (size_t)e * RD);
+        const int d1 = (wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1);
+        const int d2 = (wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1);
+        rel = (d1 < W + kWR - 1) && (d2 < W + kWC - 1);
       }
-      const uint32_t incl = warp_incl_scan(local, lane);
-      if (lane == 31) s_misc[warp] = incl;
-      __syncthreads();
-      if (warp == 0) {
-        const uint32_t v = (lane < NW) ? s_misc[lane] : 0u;
-        const uint32_t vi = warp_incl_scan(v, lane);
-        if (lane < NW) s_misc[lane] = vi - v;
-        if (lane == 31) s_misc[32] = vi;
-      }
-      __syncthreads();
-      uint32_t run = s_misc[warp] + incl - local;
-      for (int k = 0; k < per; ++k) {
-        const int e = tid * per + k;
-        if (e < ne) {
-          const uint32_t c = s_off[e];
-          s_off[e] = run;
-          run += c;
-        }
-      }
+      const unsigned bal = __ballot_sync(0xffffffffu, rel);
+      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint32_t)e | ((uint32_t)stp[e] << 16);
+      nlist += __popc(bal);
     }
-    __syncthreads();
-    const uint32_t total = s_misc[32];
-
-    for (uint32_t b0 = 0; b0 < total; b0 += prm.cap) {
-      const uint32_t b1 = min(total, b0 + (uint32_t)prm.cap);
-      const int B = (int)(b1 - b0);
-      // ---- B: batch slot -> record index and plane ----
-      for (int k = 0; k < per; ++k) {
-        const int e = tid * per + k;
-        if (e >= ne) break;
-        const uint32_t off = s_off[e];
-        const uint32_t cnt = (e + 1 < ne ? s_off[e + 1] : total) - off;
-        if (cnt == 0 || off >= b1 || off + cnt <= b0) continue;
-        const uint32_t beg = s_beg[e];
-        const uint32_t k0 = off < b0 ? b0 - off : 0u;
-        const uint32_t k1 = min(cnt, b1 - off);
-        const uint16_t step = (uint16_t)(ch0 + e / np_used);
-        for (uint32_t kk = k0; kk < k1; ++kk) {
-          s_idx[off + kk - b0] = beg + kk;
-          s_step[off + kk - b0] = step;
-        }
-      }
-      __syncthreads();
-      // ---- C: copy the batch's records to shared memory (16-byte chunks, coalesced per record) ----
-      {
-        const int nchunk = B * R::kChunks16;
-        const double2* gsrc = reinterpret_cast<const double2*>(prm.rec);
-        double2* sdst = reinterpret_cast<double2*>(s_rec);
-        for (int c = tid; c < nchunk; c += NT) {
-          const int e = c / R::kChunks16, part = c - e * R::kChunks16;
-          sdst[c] = __ldg(gsrc + (size_t)s_idx[e] * R::kChunks16 + part);
-        }
-      }
-      __syncthreads();
-      // ---- E: this warp's plane-ordered list of records touching its 4 x 8 sub-patch ----
-      int nlist = 0;
-      uint32_t* my = s_list + (size_t)warp * prm.cap;
-      for (int base = 0; base < B; base += 32) {
-        const int e = base + lane;
-        bool rel = false;
-        if (e < B) {
-          const int2 cc = *reinterpret_cast<const int2*>(s_rec + (size_t)e * RD);
-          const int d1 = (wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1);
-          const int d2 = (wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1);
-          rel = (d1 < W + kWR - 1) && (d2 < W + kWC - 1);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, rel);
-        if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint32_t)e | ((uint32_t)s_step[e] << 16);
-        nlist += __popc(bal);
-      }
-      __syncwarp();
-      // ---- F: apply the records plane by plane; the window shifts only between planes.
-      //      Records of one plane are taken two at a time so their shared-memory loads overlap. ----
-      if (nlist > 0) {
-        auto coef = [&](int e, double& cr, double& ci) {
-          const double* r = s_rec + (size_t)e * RD;
-          const int2 cc = *reinterpret_cast<const int2*>(r);
-          const unsigned i1 = min((unsigned)((lo1 - cc.x) & (n1 - 1)), (unsigned)W);
-          const unsigned i2 = min((unsigned)((lo2 - cc.y) & (n2 - 1)), (unsigned)W);
-          const double2 fv = *reinterpret_cast<const double2*>(r + 2);
-          const double w12 = r[R::kW1 + i1] * r[R::kW2 + i2];
-          cr = fv.x * w12;
-          ci = fv.y * w12;
-        };
-        int k = 0;
-        uint32_t ent = my[0];
-        while (k < nlist) {
-          const int st = (int)(ent >> 16);
-          advance(st);
-          for (;;) {
-            const int ea = (int)(ent & 0xffffu);
+    __syncwarp();
+    // ---- apply the records plane by plane (pairs of records share one pass over w0) ----
+    if (nlist > 0) {
+      auto coef = [&](int e, double& cr, double& ci) {
+        const double* r = recs + (size_t)e * RD;
+        const int2 cc = *reinterpret_cast<const int2*>(r);
+        const unsigned i1 = min((unsigned)((lo1 - cc.x) & (n1 - 1)), (unsigned)W);
+        const unsigned i2 = min((unsigned)((lo2 - cc.y) & (n2 - 1)), (unsigned)W);
+        const double2 fv = *reinterpret_cast<const double2*>(r + 2);
+        const double w12 = r[R::kW1 + i1] * r[R::kW2 + i2];
+        cr = fv.x * w12;
+        ci = fv.y * w12;
+      };
+      int k = 0;
+      uint32_t ent = my[0];
+      while (k < nlist) {
+        const int st = (int)(ent >> 16);
+        advance(st);
+        for (;;) {
+          const int ea = (int)(ent & 0xffffu);
+          ++k;
+          ent = (k < nlist) ? my[k] : 0xffffffffu;
+          const bool pair = (int)(ent >> 16) == st && k < nlist;
+          const int eb = pair ? (int)(ent & 0xffffu) : ea;
+          if (pair) {
             ++k;
             ent = (k < nlist) ? my[k] : 0xffffffffu;
-            const bool pair = (int)(ent >> 16) == st && k < nlist;
-            const int eb = pair ? (int)(ent & 0xffffu) : ea;
-            if (pair) {
-              ++k;
-              ent = (k < nlist) ? my[k] : 0xffffffffu;
-            }
-            double ar, ai, br, bi;
-            coef(ea, ar, ai);
-            coef(eb, br, bi);
-            if (!pair) {
-              br = 0.0;
-              bi = 0.0;
-            }
-            const double* wa = s_rec + (size_t)ea * RD + R::kW0;
-            const double* wb = s_rec + (size_t)eb * RD + R::kW0;
-#pragma unroll
-            for (int i = 0; i < W; i += 2) {
-              const double2 xa = *reinterpret_cast<const double2*>(wa + i);
-              const double2 xb = *reinterpret_cast<const double2*>(wb + i);
-              acc[i].x = fma(br, xb.x, fma(ar, xa.x, acc[i].x));
-              acc[i].y = fma(bi, xb.x, fma(ai, xa.x, acc[i].y));
-              acc[i + 1].x = fma(br, xb.y, fma(ar, xa.y, acc[i + 1].x));
-              acc[i + 1].y = fma(bi, xb.y, fma(ai, xa.y, acc[i + 1].y));
-            }
-            if (!((int)(ent >> 16) == st && k < nlist)) break;
           }
+          double ar, ai, br, bi;
+          coef(ea, ar, ai);
+          coef(eb, br, bi);
+          if (!pair) {
+            br = 0.0;
+            bi = 0.0;
+          }
+          const double* wa = recs + (size_t)ea * RD + R::kW0;
+          const double* wb = recs + (size_t)eb * RD + R::kW0;
+#pragma unroll
+          for (int i = 0; i < W; i += 2) {
+            const double2 xa = *reinterpret_cast<const double2*>(wa + i);
+            const double2 xb = *reinterpret_cast<const double2*>(wb + i);
+            acc[i].x = fma(br, xb.x, fma(ar, xa.x, acc[i].x));
+            acc[i].y = fma(bi, xb.x, fma(ai, xa.x, acc[i].y));
+            acc[i + 1].x = fma(br, xb.y, fma(ar, xa.y, acc[i + 1].x));
+            acc[i + 1].y = fma(bi, xb.y, fma(ai, xa.y, acc[i + 1].y));
+          }
+          if (!((int)(ent >> 16) == st && k < nlist)) break;
         }
       }
-      __syncthreads();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[stage]);
+    if (hdr.end == 1) advance(nsteps);   // tile finished: flush the remaining nodes
+    if (hdr.end == 2) cur = nsteps;      // tile skipped in a multi-group pass: nothing to write
+    if (++stage == NS) {
+      stage = 0;
+      phase ^= 1u;
     }
   }
-  advance(nsteps);
 }
 
 namespace {
@@ -403,29 +518,31 @@ namespace {
 template <int P1, int P2, int M_>
 size_t sweep_smem_bytes(int cap) {
   using C = SweepCfg<P1, P2, M_>;
+  using L = SweepLayout<P1, P2, M_>;
   size_t b = 0;
-  b += sizeof(double) * (size_t)cap * Rec<2 * M_>::kDoubles;
+  b += sizeof(double) * (size_t)L::NS * cap * Rec<2 * M_>::kDoubles;
+  b += (sizeof(uint64_t) * 2 + sizeof(BatchHdr)) * L::NS;
+  b += sizeof(uint16_t) * (L::NS * cap + 1);
+  b += sizeof(uint32_t) * ((size_t)L::NW * cap);
   b += sizeof(uint32_t) * cap;
-  b += sizeof(uint16_t) * cap;
-  b += sizeof(uint32_t) * ((size_t)C::kWarps * cap);
-  b += sizeof(uint32_t) * (2 * C::kEntries + 40);
+  b += sizeof(uint32_t) * (2 * C::kEntries + 16);
   return b + 64;
 }
 
-// CTA patch variant: 0 = 16 x 32 (512 threads, 1 CTA/SM), 1 = 16 x 16 (256 threads, 2 CTAs/SM).
+// CTA patch variant: 0 = 12 x 32 (12 consumer + 4 producer warps), 1 = 8 x 32 (8 + 4 warps).
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    v = (e && e[0] == '1' && e[1] == '6' && e[2] == 'x' && e[3] == '1') ? 1 : 0;
+    v = (e && e[0] == '8') ? 1 : 0;
   }
   return v;
 }
 
 template <int P1, int P2, int M_>
 int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool accumulate) {
-  using C = SweepCfg<P1, P2, M_>;
-  const size_t smem_max = C::kThreads <= 256 ? (size_t)(113 * 1024) : (size_t)(227 * 1024);
+  using L = SweepLayout<P1, P2, M_>;
+  const size_t smem_max = (size_t)(226 * 1024);
   int cap = 64;
   while (sweep_smem_bytes<P1, P2, M_>(cap + 64) <= smem_max) cap += 64;
   const size_t smem = sweep_smem_bytes<P1, P2, M_>(cap);
@@ -444,11 +561,16 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   prm.seg = (int)(p->n[0] < 256 ? p->n[0] : 256);
   prm.nseg = (int)(p->n[0] / prm.seg);
   prm.cap = cap;
+  prm.tile_counter = p->tile_counter;
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
   auto kern = k_spread_sweep<P1, P2, M_>;
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                   "sweep smem attr");
-  const int64_t blocks = (p->n[1] / P1) * (p->n[2] / P2) * prm.nseg;
-  kern<<<(unsigned)blocks, C::kThreads, smem, p->stream>>>(prm);
+  const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t blocks = tiles < (int64_t)sms ? tiles : (int64_t)sms;
+  kern<<<(unsigned)blocks, L::kThreads, smem, p->stream>>>(prm);
   p->launches++;
   return check_launch(p, "spread_sweep");
 }
@@ -479,8 +601,8 @@ int run_sweep(Plan* p, const double* f) {
                                             p->group_rows);
       p->launches++;
     }
-    int rc = sweep_variant() == 1 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                                  : launch_sweep_group<16, 32, M_>(p, g0, g1, p->group_rows, multi);
+    int rc = sweep_variant() == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+                                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
@@ -493,7 +615,7 @@ size_t record_bytes(int m) { return sizeof(double) * (6 + 3 * 2 * m); }
 
 bool sweep_supported(const Plan* p) {
   const int W = 2 * p->m;
-  const int P1 = 16, P2 = 32;   // largest patch of any variant
+  const int P1 = 12, P2 = 32;   // largest patch of any variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;
   if (p->n[1] < P1 + W - 1) return false;                     // candidate rows must be distinct
   const int bins = (P2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
