@@ -122,16 +122,26 @@ static int scan_exclusive(Plan* p, uint32_t* a, int64_t n, uint32_t* tmp) {
   return check_launch(p, "scan add");
 }
 
-__global__ void k_scatter(const double* __restrict__ x, int64_t M, const uint32_t* __restrict__ key,
-                          const uint32_t* __restrict__ rank, const uint32_t* __restrict__ start,
-                          uint32_t* __restrict__ perm, double* __restrict__ xs) {
+// scatter only the 4-byte permutation (random writes), then gather the coordinates in sorted
+// order (random 24-byte reads, coalesced writes): scattered partial-sector writes of the
+// coordinates would cost a DRAM read-modify-write each.
+__global__ void k_scatter(int64_t M, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rank,
+                          const uint32_t* __restrict__ start, uint32_t* __restrict__ perm) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= M) return;
   uint32_t pos = start[key[j]] + rank[j];
   perm[pos] = (uint32_t)j;
-  xs[3 * (int64_t)pos] = x[3 * j];
-  xs[3 * (int64_t)pos + 1] = x[3 * j + 1];
-  xs[3 * (int64_t)pos + 2] = x[3 * j + 2];
+}
+
+__global__ void k_gather_x(const double* __restrict__ x, int64_t M, const uint32_t* __restrict__ perm,
+                           double* __restrict__ xs) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  const int64_t j = perm[k];
+  const double a = __ldg(x + 3 * j), b = __ldg(x + 3 * j + 1), c = __ldg(x + 3 * j + 2);
+  xs[3 * k] = a;
+  xs[3 * k + 1] = b;
+  xs[3 * k + 2] = c;
 }
 
 int64_t scan_workspace_elems(int64_t nbins) { return scan_tmp_need(nbins + 1); }
@@ -157,9 +167,9 @@ int sort_points(Plan* p, const double* x) {
   stage_end(p, 1);
   stage_begin(p, 2);
   if (M > 0) {
-    k_scatter<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->key, p->rank, p->bin_count, p->perm,
-                                                                  p->xs);
-    p->launches++;
+    k_scatter<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(M, p->key, p->rank, p->bin_count, p->perm);
+    k_gather_x<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->perm, p->xs);
+    p->launches += 2;
     rc = check_launch(p, "scatter");
     if (rc) return rc;
   }

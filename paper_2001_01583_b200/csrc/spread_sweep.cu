@@ -86,9 +86,10 @@ struct SweepParams {
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
-// A3: point records.  Thread (k, i) evaluates tap i of sorted point g0 + k in the three dimensions
-// (coefficients of tap i in registers, 3 independent Horner chains); tap 0 also writes the cell,
-// f_j and the zero pads.
+// A3: point records.  A CTA of 256 threads handles PB = 256 / 2m consecutive sorted points:
+// thread (k, i) evaluates tap i of point k in the three dimensions (coefficients of tap i in
+// registers, 3 independent Horner chains) into a shared-memory staging copy of the records, which
+// is then written to HBM with coalesced 16-byte stores (the records of a CTA are contiguous).
 template <int M_>
 __global__ void __launch_bounds__(256) k_point_records(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
                                                         const double* __restrict__ f, const double* __restrict__ poly_g,
@@ -96,45 +97,54 @@ __global__ void __launch_bounds__(256) k_point_records(const double* __restrict_
                                                         int64_t n0, int64_t n1, int64_t n2) {
   constexpr int W = 2 * M_;
   constexpr int PD = kPolyDeg + 1;
+  constexpr int PB = 256 / W;
   using R = Rec<W>;
   __shared__ double poly[W * PD];
+  __shared__ __align__(16) double stage[PB * R::kDoubles];
   for (int e = threadIdx.x; e < W * PD; e += blockDim.x) poly[e] = poly_g[e];
   __syncthreads();
-  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (uint64_t)count * W) return;
-  const uint32_t k = (uint32_t)(gid / W);
-  const int i = (int)(gid - (uint64_t)k * W);
-  const size_t src = (size_t)g0 + k;
-  double* out = rec + (size_t)k * R::kDoubles;
-  const CellT a0 = cell_of(__ldg(xs + 3 * src), n0);
-  const CellT a1 = cell_of(__ldg(xs + 3 * src + 1), n1);
-  const CellT a2 = cell_of(__ldg(xs + 3 * src + 2), n2);
-  double cf[PD];
+  const uint32_t kb = blockIdx.x * PB;                 // first point of this CTA (group-relative)
+  const int kl = threadIdx.x / W, i = threadIdx.x - kl * W;
+  const uint32_t k = kb + kl;
+  if (kl < PB && k < count) {
+    const size_t src = (size_t)g0 + k;
+    double* out = stage + kl * R::kDoubles;
+    const CellT a0 = cell_of(__ldg(xs + 3 * src), n0);
+    const CellT a1 = cell_of(__ldg(xs + 3 * src + 1), n1);
+    const CellT a2 = cell_of(__ldg(xs + 3 * src + 2), n2);
+    double cf[PD];
 #pragma unroll
-  for (int j = 0; j < PD; ++j) cf[j] = poly[i * PD + j];
-  const double s0 = fma(2.0, a0.t, -1.0), s1 = fma(2.0, a1.t, -1.0), s2 = fma(2.0, a2.t, -1.0);
-  double v0 = cf[PD - 1], v1 = cf[PD - 1], v2 = cf[PD - 1];
+    for (int j = 0; j < PD; ++j) cf[j] = poly[i * PD + j];
+    const double s0 = fma(2.0, a0.t, -1.0), s1 = fma(2.0, a1.t, -1.0), s2 = fma(2.0, a2.t, -1.0);
+    double v0 = cf[PD - 1], v1 = cf[PD - 1], v2 = cf[PD - 1];
 #pragma unroll
-  for (int j = PD - 2; j >= 0; --j) {
-    v0 = fma(v0, s0, cf[j]);
-    v1 = fma(v1, s1, cf[j]);
-    v2 = fma(v2, s2, cf[j]);
+    for (int j = PD - 2; j >= 0; --j) {
+      v0 = fma(v0, s0, cf[j]);
+      v1 = fma(v1, s1, cf[j]);
+      v2 = fma(v2, s2, cf[j]);
+    }
+    if (i == W - 1) {   // strict truncation |u - l| < m (Q4)
+      if (a0.t == 0.0) v0 = 0.0;
+      if (a1.t == 0.0) v1 = 0.0;
+      if (a2.t == 0.0) v2 = 0.0;
+    }
+    out[R::kW0 + i] = v0;
+    out[R::kW1 + i] = v1;
+    out[R::kW2 + i] = v2;
+    if (i == 0) {
+      const uint32_t j = __ldg(perm + src);
+      reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, 0, 0);
+      reinterpret_cast<double2*>(out)[1] = __ldg(reinterpret_cast<const double2*>(f) + j);
+      out[R::kW1 + W] = 0.0;
+      out[R::kW2 + W] = 0.0;
+    }
   }
-  if (i == W - 1) {   // strict truncation |u - l| < m (Q4)
-    if (a0.t == 0.0) v0 = 0.0;
-    if (a1.t == 0.0) v1 = 0.0;
-    if (a2.t == 0.0) v2 = 0.0;
-  }
-  out[R::kW0 + i] = v0;
-  out[R::kW1 + i] = v1;
-  out[R::kW2 + i] = v2;
-  if (i == 0) {
-    const uint32_t j = __ldg(perm + src);
-    reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, 0, 0);
-    reinterpret_cast<double2*>(out)[1] = __ldg(reinterpret_cast<const double2*>(f) + j);
-    out[R::kW1 + W] = 0.0;
-    out[R::kW2 + W] = 0.0;
-  }
+  __syncthreads();
+  const uint32_t npts = min((uint32_t)PB, count - kb);
+  const int nchunk = (int)npts * R::kChunks16;
+  const double2* sp = reinterpret_cast<const double2*>(stage);
+  double2* gp = reinterpret_cast<double2*>(rec + (size_t)kb * R::kDoubles);
+  for (int c = threadIdx.x; c < nchunk; c += blockDim.x) gp[c] = sp[c];
 }
 
 // c1 rows spanned by sorted points [g0, g1): binary search of the bin table (multi-group only).
@@ -589,8 +599,8 @@ int run_sweep(Plan* p, const double* f) {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
     if (cnt > 0) {
-      const uint64_t threads = (uint64_t)cnt * (2 * M_);
-      k_point_records<M_><<<(unsigned)((threads + 255) / 256), 256, 0, p->stream>>>(
+      constexpr int PB = 256 / (2 * M_);
+      k_point_records<M_><<<(unsigned)((cnt + PB - 1) / PB), 256, 0, p->stream>>>(
           p->xs, p->perm, f, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
       p->launches++;
       int rc = check_launch(p, "point records");
