@@ -143,16 +143,14 @@ def make_inputs(cfg, dist_kind, device):
     return x, f
 
 
-def slab_select(x, f, rank, ws):
-    """Equal-size x-slab subcell of this rank: x0 in [-1/2 + r/P, -1/2 + (r+1)/P)."""
+def slab_select(x, f, rank, ws, partition="equal_size"):
+    """This rank's x-slab subcell: equal-size slabs, or equal-count slabs."""
+    from paper_2001_01583_b200.dist import equal_count_edges, slab_mask
+
     if ws == 1:
         return x, f
-    lo = -0.5 + rank / ws
-    hi = -0.5 + (rank + 1) / ws
-    x0 = x[:, 0]
-    mask = (x0 >= lo) & (x0 < hi)
-    if rank == ws - 1:
-        mask |= x0 >= 0.5
+    edges = equal_count_edges(x, ws) if partition == "equal_count" else None
+    mask = slab_mask(x, rank, ws, edges)
     return x[mask].contiguous(), f[mask].contiguous()
 
 
@@ -172,7 +170,7 @@ def run_ours(args):
     N = cfg["N"]
     M_total = cfg["M"]
     x_all, f_all = make_inputs(cfg, args.dist, dev)
-    x, f = slab_select(x_all, f_all, rank, ws)
+    x, f = slab_select(x_all, f_all, rank, ws, args.partition)
     del x_all, f_all
     M_local = x.shape[0]
     torch.cuda.synchronize()
@@ -309,7 +307,7 @@ def run_ours(args):
             "config": {"workload": f"BASELINE config {args.config}: d=3, N={N[0]}^3, M={M_total}, "
                                    f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}",
                        "N": list(N), "M": M_total, "m": M_WINDOW, "sigma": SIGMA, "window": "kaiser_bessel",
-                       "points": args.dist, "partition": f"equal-size x-slabs x{ws}",
+                       "points": args.dist, "partition": f"{args.partition} x-slabs x{ws}",
                        "exchange": "ncclAllReduce(fhat)" if ws > 1 else "none",
                        "spread_method": args.method,
                        "l2": "inputs larger than L2 (x 240 MB, f 160 MB, grid 2.1 GB); no flush"},
@@ -418,6 +416,7 @@ def main():
     ap.add_argument("--config", default="4", choices=sorted(CONFIGS))
     ap.add_argument("--method", default="auto", choices=["auto", "atomic", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="equal_size", choices=["equal_size", "equal_count"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(256) k_point_records(const double* __restrict_
   if (kl < PB && k < count) {
     const size_t src = (size_t)g0 + k;
     double* out = stage + kl * R::kDoubles;
+    // issue the dependent gather f[perm[src]] first so its latency overlaps the Horner chains
+    double2 fv = make_double2(0.0, 0.0);
+    if (i == 0) fv = __ldg(reinterpret_cast<const double2*>(f) + __ldg(perm + src));
     const CellT a0 = cell_of(__ldg(xs + 3 * src), n0);
     const CellT a1 = cell_of(__ldg(xs + 3 * src + 1), n1);
     const CellT a2 = cell_of(__ldg(xs + 3 * src + 2), n2);
@@ -132,9 +135,8 @@ __global__ void __launch_bounds__(256) k_point_records(const double* __restrict_
     out[R::kW1 + i] = v1;
     out[R::kW2 + i] = v2;
     if (i == 0) {
-      const uint32_t j = __ldg(perm + src);
       reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, 0, 0);
-      reinterpret_cast<double2*>(out)[1] = __ldg(reinterpret_cast<const double2*>(f) + j);
+      reinterpret_cast<double2*>(out)[1] = fv;
       out[R::kW1 + W] = 0.0;
       out[R::kW2 + W] = 0.0;
     }

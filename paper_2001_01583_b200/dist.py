@@ -1,0 +1,139 @@
+"""Multi-GPU layer: the paper's accumulative decomposition on one process per GPU.
+
+HP-NFFT (§3, Eqs. 7-8) splits the points into equal-size spatial subcells,
+computes a partial NFFT per node and sums the partial results ("Accumulate", Alg. 3,
+PAPER.md:174-200, a binomial tree of MPI Send/Recv).  Here every rank is one GPU of one node:
+
+* the subcells are x-slabs (dimension 0): equal-size as the paper states (PAPER.md:93,
+  "subcells with same size") or equal-count (quantiles, for clustered inputs);
+* each rank runs the single-GPU path (``Plan``) on its slab;
+* the partial fhat are summed with one collective over torch.distributed (NCCL over
+  NVLink/NVSwitch on GPUs): ``allreduce`` (every rank gets fhat), ``reduce`` (rank 0 gets
+  fhat, Alg. 3's semantics) or ``reduce_scatter`` (fhat left distributed over k0 slabs).
+
+The collective and the partition are host logic that is exercised on CPU with the gloo
+backend in tests/test_dist_gloo.py; the local transform is injectable for those tests.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+MODES = ("allreduce", "reduce", "reduce_scatter")
+
+
+def slab_bounds(rank: int, world: int):
+    """Equal-size x-slab [lo, hi) of `rank` among `world`."""
+    lo = -0.5 + rank / world
+    hi = -0.5 + (rank + 1) / world
+    return lo, hi
+
+
+def slab_mask(x, rank: int, world: int, edges=None):
+    """Boolean mask of the points (tensor [M, 3]) whose x0 lies in this rank's slab.
+
+    Coordinates equal to +0.5 belong to the last slab (x = 0.5 is x = -0.5 by periodicity, but
+    the partition only has to be a partition).  `edges` (world + 1 increasing values) selects
+    an equal-count partition instead of equal size.
+    """
+    if world == 1:
+        import torch
+
+        return torch.ones(x.shape[0], dtype=torch.bool, device=x.device)
+    x0 = x[:, 0]
+    if edges is None:
+        lo, hi = slab_bounds(rank, world)
+    else:
+        lo, hi = float(edges[rank]), float(edges[rank + 1])
+    m = (x0 >= lo) & (x0 < hi)
+    if rank == world - 1:
+        m |= x0 >= hi
+    if rank == 0:
+        m |= x0 < lo
+    return m
+
+
+def equal_count_edges(x, world: int):
+    """Slab edges at the x0 quantiles so every rank owns ~M/world points (load balance)."""
+    import torch
+
+    x0 = torch.sort(x[:, 0]).values
+    M = x0.shape[0]
+    edges = [-0.5]
+    for r in range(1, world):
+        edges.append(float(x0[min(M - 1, (r * M) // world)]))
+    edges.append(0.5)
+    return edges
+
+
+class DistPlan:
+    """Distributed adjoint NFFT: local Plan on this rank's points + one collective on fhat.
+
+    group   : torch.distributed process group (None = WORLD)
+    mode    : "allreduce" | "reduce" | "reduce_scatter"
+    local_fn: optional callable (x_local, f_local) -> partial fhat tensor; defaults to the GPU
+              Plan (the only product path).  Tests inject the CPU oracle here to check the
+              partition/collective logic with the gloo backend.
+    """
+
+    def __init__(self, N, M_local: int, m: int = 6, sigma: float = 2.0, window="kb", group=None,
+                 mode: str = "allreduce", device=None, local_fn: Optional[Callable] = None):
+        import torch.distributed as dist
+
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        self.N = tuple(int(v) for v in N)
+        self.mode = mode
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.local_fn = local_fn
+        self.plan = None
+        if local_fn is None:
+            from . import Plan
+
+            self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device)
+        if mode == "reduce_scatter" and self.N[0] % self.world:
+            raise ValueError("reduce_scatter needs N0 divisible by the world size")
+
+    def set_points(self, x):
+        self._x = x
+        if self.plan is not None:
+            self.plan.set_points(x)
+
+    def partial(self, f):
+        """This rank's partial fhat_rank(k) (Eq. 8 term), before the collective."""
+        if self.plan is not None:
+            return self.plan.adjoint(f)
+        return self.local_fn(self._x, f)
+
+    def adjoint(self, f):
+        """fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate of Alg. 3)."""
+        import torch
+        import torch.distributed as dist
+
+        fh = self.partial(f)
+        if self.world == 1:
+            return fh
+        if self.mode == "allreduce":
+            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
+            return fh
+        if self.mode == "reduce":
+            dist.reduce(fh, dst=0, op=dist.ReduceOp.SUM, group=self.group)
+            return fh if self.rank == 0 else None
+        # reduce_scatter: rank r receives fhat[k0 slab r] (N0 / world planes)
+        rows = self.N[0] // self.world
+        if dist.get_backend(self.group) == "gloo":   # gloo has no reduce_scatter: reduce + slice
+            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
+            return fh[self.rank * rows:(self.rank + 1) * rows].clone()
+        out = torch.empty((rows,) + self.N[1:], dtype=fh.dtype, device=fh.device)
+        if fh.is_complex():
+            dist.reduce_scatter_tensor(torch.view_as_real(out), torch.view_as_real(fh.contiguous()),
+                                       op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            dist.reduce_scatter_tensor(out, fh.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
+        return out
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None
