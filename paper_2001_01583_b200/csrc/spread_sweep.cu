@@ -32,8 +32,8 @@ namespace hpnfft {
 
 namespace {
 
-constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 8 cols (l2) = 32 lanes
-constexpr int kWC = 8;
+constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 4 cols (l2) = 16 columns,
+constexpr int kWC = 4;          // two lanes per column (real part, imaginary part)
 constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 constexpr int kChunk = 8;       // planes whose pencil ranges are looked up together
 
@@ -389,35 +389,33 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
   }
 
   // =============================== consumer warps ===============================
+  // lane = 2 * (4 * r + c) + part: column (wr0 + r, wc0 + c) of the 4 x 4 sub-patch, part 0 keeps
+  // the real and part 1 the imaginary component of the 2m-node window (2m doubles per lane).
   const int wr_off = (warp / (P2 / kWC)) * kWR;
   const int wc_off = (warp % (P2 / kWC)) * kWC;
+  const int part = lane & 1;
+  const int lr = (lane >> 1) / kWC, lc = (lane >> 1) % kWC;
   int cur_tile = -1;
-  int first = 0, wr0 = 0, wc0 = 0, lo1 = 0, lo2 = 0;
+  int first = 0, wr0 = 0, wc0 = 0;
   bool valid = true;
-  double2* gcol = nullptr;
-  const size_t plane = (size_t)n1 * n2;
-  double2 acc[W];
+  double* gcol = nullptr;
+  const size_t plane2 = (size_t)2 * n1 * n2;   // doubles per l0 plane
+  double acc[W];
 #pragma unroll
-  for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
+  for (int i = 0; i < W; ++i) acc[i] = 0.0;
   int cur = 0;
 
   auto advance = [&](int upto) {
     while (cur < upto) {
       if (cur >= W - 1 && valid) {
         const int l0 = (first + cur - M_ + 1) & (n0 - 1);
-        double2* dst = gcol + (size_t)l0 * plane;
-        if (prm.accumulate) {
-          double2 o = *dst;
-          o.x += acc[0].x;
-          o.y += acc[0].y;
-          *dst = o;
-        } else {
-          *dst = acc[0];
-        }
+        double* dst = gcol + (size_t)l0 * plane2;
+        if (prm.accumulate) *dst += acc[0];
+        else *dst = acc[0];
       }
 #pragma unroll
       for (int i = 0; i < W - 1; ++i) acc[i] = acc[i + 1];
-      acc[W - 1] = make_double2(0.0, 0.0);
+      acc[W - 1] = 0.0;
       ++cur;
     }
   };
@@ -435,82 +433,73 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
       first = L0 - M_;
       wr0 = R0 + wr_off;
       wc0 = C0 + wc_off;
-      const int l1 = wr0 + lane / kWC;
-      const int l2 = wc0 + lane % kWC;
+      const int l1 = wr0 + lr;
+      const int l2 = wc0 + lc;
       valid = l1 < n1;   // ghost rows of the last row tile when P1 does not divide n1
-      lo1 = l1 + M_ - 1;
-      lo2 = l2 + M_ - 1;
-      gcol = reinterpret_cast<double2*>(prm.grid) + (size_t)(l1 & (n1 - 1)) * n2 + l2;
+      gcol = prm.grid + 2 * ((size_t)(l1 & (n1 - 1)) * n2 + l2) + part;
       cur = 0;
 #pragma unroll
-      for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
+      for (int i = 0; i < W; ++i) acc[i] = 0.0;
     }
     const int B = hdr.B;
     const double* recs = s_rec + (size_t)stage * cap * RD;
     const uint16_t* stp = s_step + stage * cap;
-    // ---- this warp's plane-ordered list of records touching its 4 x 8 sub-patch ----
+    // ---- this warp's plane-ordered list: entry = record | plane << 9 | dr << 18 | dc << 23 with
+    //      dr = wr0 - (c1 - m + 1) + 3, dc = wc0 - (c2 - m + 1) + 3 (mod n) < 2m + 3 ----
     int nlist = 0;
     uint32_t* my = s_list + (size_t)warp * cap;
     for (int base = 0; base < B; base += 32) {
       const int e = base + lane;
       bool rel = false;
+      uint32_t entry = 0;
       if (e < B) {
         const int2 cc = *reinterpret_cast<const int2*>(recs + (size_t)e * RD);
-        const int d1 = (wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1);
-        const int d2 = (wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1);
-        rel = (d1 < W + kWR - 1) && (d2 < W + kWC - 1);
+        const uint32_t d1 = (uint32_t)((wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1));
+        const uint32_t d2 = (uint32_t)((wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1));
+        rel = (d1 < (uint32_t)(W + kWR - 1)) && (d2 < (uint32_t)(W + kWC - 1));
+        entry = (uint32_t)e | ((uint32_t)stp[e] << 9) | (d1 << 18) | (d2 << 23);
       }
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
-      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint32_t)e | ((uint32_t)stp[e] << 16);
+      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = entry;
       nlist += __popc(bal);
     }
     __syncwarp();
-    // ---- apply the records plane by plane (pairs of records share one pass over w0) ----
+    // ---- apply the records plane by plane, two records per pass over the window ----
     if (nlist > 0) {
-      auto coef = [&](int e, double& cr, double& ci) {
-        const double* r = recs + (size_t)e * RD;
-        const int2 cc = *reinterpret_cast<const int2*>(r);
-        const unsigned i1 = min((unsigned)((lo1 - cc.x) & (n1 - 1)), (unsigned)W);
-        const unsigned i2 = min((unsigned)((lo2 - cc.y) & (n2 - 1)), (unsigned)W);
-        const double2 fv = *reinterpret_cast<const double2*>(r + 2);
-        const double w12 = r[R::kW1 + i1] * r[R::kW2 + i2];
-        cr = fv.x * w12;
-        ci = fv.y * w12;
+      const int roff = lr - (kWR - 1), coff = lc - (kWC - 1);
+      auto coef = [&](uint32_t en) -> double {
+        const double* r = recs + (size_t)(en & 0x1ffu) * RD;
+        const unsigned i1 = min((unsigned)((int)((en >> 18) & 31u) + roff), (unsigned)W);
+        const unsigned i2 = min((unsigned)((int)((en >> 23) & 31u) + coff), (unsigned)W);
+        return r[2 + part] * (r[R::kW1 + i1] * r[R::kW2 + i2]);
       };
       int k = 0;
       uint32_t ent = my[0];
       while (k < nlist) {
-        const int st = (int)(ent >> 16);
+        const int st = (int)((ent >> 9) & 0x1ffu);
         advance(st);
         for (;;) {
-          const int ea = (int)(ent & 0xffffu);
+          const uint32_t ea = ent;
           ++k;
           ent = (k < nlist) ? my[k] : 0xffffffffu;
-          const bool pair = (int)(ent >> 16) == st && k < nlist;
-          const int eb = pair ? (int)(ent & 0xffffu) : ea;
+          const bool pair = k < nlist && (int)((ent >> 9) & 0x1ffu) == st;
+          const uint32_t eb = pair ? ent : ea;
           if (pair) {
             ++k;
             ent = (k < nlist) ? my[k] : 0xffffffffu;
           }
-          double ar, ai, br, bi;
-          coef(ea, ar, ai);
-          coef(eb, br, bi);
-          if (!pair) {
-            br = 0.0;
-            bi = 0.0;
-          }
-          const double* wa = recs + (size_t)ea * RD + R::kW0;
-          const double* wb = recs + (size_t)eb * RD + R::kW0;
+          const double ca = coef(ea);
+          const double cb = pair ? coef(eb) : 0.0;
+          const double* wa = recs + (size_t)(ea & 0x1ffu) * RD + R::kW0;
+          const double* wb = recs + (size_t)(eb & 0x1ffu) * RD + R::kW0;
 #pragma unroll
           for (int i = 0; i < W; i += 2) {
             const double2 xa = *reinterpret_cast<const double2*>(wa + i);
             const double2 xb = *reinterpret_cast<const double2*>(wb + i);
-            acc[i].x = fma(br, xb.x, fma(ar, xa.x, acc[i].x));
-            acc[i].y = fma(bi, xb.x, fma(ai, xa.x, acc[i].y));
-            acc[i + 1].x = fma(br, xb.y, fma(ar, xa.y, acc[i + 1].x));
-            acc[i + 1].y = fma(bi, xb.y, fma(ai, xa.y, acc[i + 1].y));
+            acc[i] = fma(cb, xb.x, fma(ca, xa.x, acc[i]));
+            acc[i + 1] = fma(cb, xb.y, fma(ca, xa.y, acc[i + 1]));
           }
-          if (!((int)(ent >> 16) == st && k < nlist)) break;
+          if (!(k < nlist && (int)((ent >> 9) & 0x1ffu) == st)) break;
         }
       }
     }
@@ -541,12 +530,12 @@ size_t sweep_smem_bytes(int cap) {
   return b + 64;
 }
 
-// CTA patch variant: 0 = 12 x 32 (12 consumer + 4 producer warps), 1 = 8 x 32 (8 + 4 warps).
+// CTA patch variant: 0 = 16 x 16 (16 consumer + 4 producer warps), 1 = 12 x 16 (12 + 4 warps).
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    v = (e && e[0] == '8') ? 1 : 0;
+    v = (e && e[0] == '1' && e[1] == '2') ? 1 : 0;
   }
   return v;
 }
@@ -556,7 +545,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   using L = SweepLayout<P1, P2, M_>;
   const size_t smem_max = (size_t)(226 * 1024);
   int cap = 64;
-  while (sweep_smem_bytes<P1, P2, M_>(cap + 64) <= smem_max) cap += 64;
+  while (sweep_smem_bytes<P1, P2, M_>(cap + 16) <= smem_max && cap + 16 < 512) cap += 16;
   const size_t smem = sweep_smem_bytes<P1, P2, M_>(cap);
   SweepParams prm;
   prm.rec = p->rec;
@@ -613,8 +602,8 @@ int run_sweep(Plan* p, const double* f) {
                                             p->group_rows);
       p->launches++;
     }
-    int rc = sweep_variant() == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
-                                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
+    int rc = sweep_variant() == 1 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
+                                  : launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
@@ -627,7 +616,7 @@ size_t record_bytes(int m) { return sizeof(double) * (6 + 3 * 2 * m); }
 
 bool sweep_supported(const Plan* p) {
   const int W = 2 * p->m;
-  const int P1 = 12, P2 = 32;   // largest patch of any variant
+  const int P1 = 16, P2 = 16;   // largest patch of any variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;
   if (p->n[1] < P1 + W - 1) return false;                     // candidate rows must be distinct
   const int bins = (P2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
