@@ -18,7 +18,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpnfft.so")
+LIB_PATH = os.environ.get("HPNFFT_LIB", os.path.join(_HERE, "libhpnfft.so"))
 
 WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
 SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}

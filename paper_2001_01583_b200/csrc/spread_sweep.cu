@@ -24,6 +24,7 @@
 // When the records of all M points do not fit in the workspace, the sorted points are processed
 // in groups ("the mass data have to be divided into several groups"): the grid is
 // zeroed once and every group's sweep accumulates (CTAs whose rows miss the group exit early).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "spread_common.cuh"
@@ -32,10 +33,16 @@ namespace hpnfft {
 
 namespace {
 
-constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 4 cols (l2) = 16 columns,
-constexpr int kWC = 4;          // two lanes per column (real part, imaginary part)
+constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 8 cols (l2) = 32 lanes
+constexpr int kWC = 8;
 constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
-constexpr int kChunk = 8;       // planes whose pencil ranges are looked up together
+#ifndef HPNFFT_SWEEP_NS
+#define HPNFFT_SWEEP_NS 3
+#endif
+#ifndef HPNFFT_SWEEP_CHUNK
+#define HPNFFT_SWEEP_CHUNK 8
+#endif
+constexpr int kChunk = HPNFFT_SWEEP_CHUNK;   // planes whose pencil ranges are looked up together
 
 // record layout in doubles: [0] c1|c2 (int2)  [1] pad  [2..3] f  [4..4+W) w0
 //                           [4+W .. 5+2W) w1 (+ zero pad)  [5+2W .. 6+3W) w2 (+ zero pad)
@@ -81,6 +88,7 @@ struct SweepParams {
   int nseg;                // n0 / S
   int cap;                 // record capacity of one shared-memory batch buffer
   int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
+  unsigned long long* prof;   // optional clock64 phase counters (HPNFFT_SWEEP_PROF=1), else null
 };
 
 }  // namespace
@@ -186,16 +194,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                    (uint32_t)__cvta_generic_to_shared(bar))
                : "memory");
 }
+// try_wait with a suspend-time hint so waiting warps sleep instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
   uint32_t ok = 0;
-  do {
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(64);
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(1000000)
         : "memory");
-  } while (!ok);
+  }
 }
 __device__ __forceinline__ void producer_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
@@ -210,7 +225,7 @@ template <int P1, int P2, int M_>
 struct SweepLayout {
   static constexpr int NW = (P1 / kWR) * (P2 / kWC);   // consumer warps
   static constexpr int NP = 4;                          // producer warps
-  static constexpr int NS = 3;                          // ring stages
+  static constexpr int NS = HPNFFT_SWEEP_NS;            // ring stages
   static constexpr int kThreads = (NW + NP) * 32;
 };
 
@@ -301,6 +316,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
           const int nch = min(kChunk, nsteps - ch0);
           const int ne = nch * np_used;
           const int per = (ne + NPT - 1) / NPT;
+          const unsigned long long p0 = prm.prof ? clock64() : 0ull;
           // (plane, pencil) ranges clipped to the group; thread owns entries [pt*per, pt*per+per)
           uint32_t local = 0;
           for (int k = 0; k < per; ++k) {
@@ -341,10 +357,13 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
             run += c;
           }
           producer_bar(NPT);
+          if (prm.prof && pt == 0) atomicAdd(prm.prof + 4, clock64() - p0);
           for (uint32_t b0 = 0; b0 < total; b0 += (uint32_t)cap) {
             const uint32_t b1 = min(total, b0 + (uint32_t)cap);
             const int B = (int)(b1 - b0);
+            const unsigned long long p1 = prm.prof ? clock64() : 0ull;
             mbar_wait(&s_empty[stage], phase ^ 1u);
+            const unsigned long long p2 = prm.prof ? clock64() : 0ull;
             uint16_t* stp = s_step + stage * cap;
             for (int k = 0; k < per; ++k) {
               const int e = pt * per + k;
@@ -369,6 +388,10 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
               cp_async16(dst + 2 * (size_t)c, prm.rec + (size_t)s_idx[e] * RD + 2 * part);
             }
             cp_async_wait_all();
+            if (prm.prof && pt == 0) {
+              atomicAdd(prm.prof + 5, p2 - p1);
+              atomicAdd(prm.prof + 6, clock64() - p2);
+            }
             if (pt == 0) s_hdr[stage] = BatchHdr{B, t, 0, 0};
             mbar_arrive(&s_full[stage]);
             next_stage();
@@ -389,41 +412,46 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
   }
 
   // =============================== consumer warps ===============================
-  // lane = 2 * (4 * r + c) + part: column (wr0 + r, wc0 + c) of the 4 x 4 sub-patch, part 0 keeps
-  // the real and part 1 the imaginary component of the 2m-node window (2m doubles per lane).
   const int wr_off = (warp / (P2 / kWC)) * kWR;
   const int wc_off = (warp % (P2 / kWC)) * kWC;
-  const int part = lane & 1;
-  const int lr = (lane >> 1) / kWC, lc = (lane >> 1) % kWC;
   int cur_tile = -1;
-  int first = 0, wr0 = 0, wc0 = 0;
+  int first = 0, wr0 = 0, wc0 = 0, lo1 = 0, lo2 = 0;
   bool valid = true;
-  double* gcol = nullptr;
-  const size_t plane2 = (size_t)2 * n1 * n2;   // doubles per l0 plane
-  double acc[W];
+  double2* gcol = nullptr;
+  const size_t plane = (size_t)n1 * n2;
+  double2 acc[W];
 #pragma unroll
-  for (int i = 0; i < W; ++i) acc[i] = 0.0;
+  for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
   int cur = 0;
 
   auto advance = [&](int upto) {
     while (cur < upto) {
       if (cur >= W - 1 && valid) {
         const int l0 = (first + cur - M_ + 1) & (n0 - 1);
-        double* dst = gcol + (size_t)l0 * plane2;
-        if (prm.accumulate) *dst += acc[0];
-        else *dst = acc[0];
+        double2* dst = gcol + (size_t)l0 * plane;
+        if (prm.accumulate) {
+          double2 o = *dst;
+          o.x += acc[0].x;
+          o.y += acc[0].y;
+          *dst = o;
+        } else {
+          *dst = acc[0];
+        }
       }
 #pragma unroll
       for (int i = 0; i < W - 1; ++i) acc[i] = acc[i + 1];
-      acc[W - 1] = 0.0;
+      acc[W - 1] = make_double2(0.0, 0.0);
       ++cur;
     }
   };
 
   int stage = 0;
   uint32_t phase = 0;
+  unsigned long long tw = 0, tl = 0, tf = 0, tA = 0;
   for (;;) {
+    const unsigned long long c0 = prm.prof ? clock64() : 0ull;
     mbar_wait(&s_full[stage], phase);
+    const unsigned long long c1 = prm.prof ? clock64() : 0ull;
     const BatchHdr hdr = s_hdr[stage];
     if (hdr.B < 0) break;
     if (hdr.tile != cur_tile) {
@@ -433,84 +461,108 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
       first = L0 - M_;
       wr0 = R0 + wr_off;
       wc0 = C0 + wc_off;
-      const int l1 = wr0 + lr;
-      const int l2 = wc0 + lc;
+      const int l1 = wr0 + lane / kWC;
+      const int l2 = wc0 + lane % kWC;
       valid = l1 < n1;   // ghost rows of the last row tile when P1 does not divide n1
-      gcol = prm.grid + 2 * ((size_t)(l1 & (n1 - 1)) * n2 + l2) + part;
+      lo1 = l1 + M_ - 1;
+      lo2 = l2 + M_ - 1;
+      gcol = reinterpret_cast<double2*>(prm.grid) + (size_t)(l1 & (n1 - 1)) * n2 + l2;
       cur = 0;
 #pragma unroll
-      for (int i = 0; i < W; ++i) acc[i] = 0.0;
+      for (int i = 0; i < W; ++i) acc[i] = make_double2(0.0, 0.0);
     }
     const int B = hdr.B;
     const double* recs = s_rec + (size_t)stage * cap * RD;
     const uint16_t* stp = s_step + stage * cap;
-    // ---- this warp's plane-ordered list: entry = record | plane << 9 | dr << 18 | dc << 23 with
-    //      dr = wr0 - (c1 - m + 1) + 3, dc = wc0 - (c2 - m + 1) + 3 (mod n) < 2m + 3 ----
+    // ---- this warp's plane-ordered list of records touching its 4 x 8 sub-patch ----
     int nlist = 0;
     uint32_t* my = s_list + (size_t)warp * cap;
     for (int base = 0; base < B; base += 32) {
       const int e = base + lane;
       bool rel = false;
-      uint32_t entry = 0;
       if (e < B) {
         const int2 cc = *reinterpret_cast<const int2*>(recs + (size_t)e * RD);
-        const uint32_t d1 = (uint32_t)((wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1));
-        const uint32_t d2 = (uint32_t)((wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1));
-        rel = (d1 < (uint32_t)(W + kWR - 1)) && (d2 < (uint32_t)(W + kWC - 1));
-        entry = (uint32_t)e | ((uint32_t)stp[e] << 9) | (d1 << 18) | (d2 << 23);
+        const int d1 = (wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1);
+        const int d2 = (wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1);
+        rel = (d1 < W + kWR - 1) && (d2 < W + kWC - 1);
       }
       const unsigned bal = __ballot_sync(0xffffffffu, rel);
-      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = entry;
+      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = (uint32_t)e | ((uint32_t)stp[e] << 16);
       nlist += __popc(bal);
     }
     __syncwarp();
-    // ---- apply the records plane by plane, two records per pass over the window ----
+    const unsigned long long c2 = prm.prof ? clock64() : 0ull;
+    // ---- apply the records plane by plane (pairs of records share one pass over w0) ----
     if (nlist > 0) {
-      const int roff = lr - (kWR - 1), coff = lc - (kWC - 1);
-      auto coef = [&](uint32_t en) -> double {
-        const double* r = recs + (size_t)(en & 0x1ffu) * RD;
-        const unsigned i1 = min((unsigned)((int)((en >> 18) & 31u) + roff), (unsigned)W);
-        const unsigned i2 = min((unsigned)((int)((en >> 23) & 31u) + coff), (unsigned)W);
-        return r[2 + part] * (r[R::kW1 + i1] * r[R::kW2 + i2]);
+      auto coef = [&](int e, double& cr, double& ci) {
+        const double* r = recs + (size_t)e * RD;
+        const int2 cc = *reinterpret_cast<const int2*>(r);
+        const unsigned i1 = min((unsigned)((lo1 - cc.x) & (n1 - 1)), (unsigned)W);
+        const unsigned i2 = min((unsigned)((lo2 - cc.y) & (n2 - 1)), (unsigned)W);
+        const double2 fv = *reinterpret_cast<const double2*>(r + 2);
+        const double w12 = r[R::kW1 + i1] * r[R::kW2 + i2];
+        cr = fv.x * w12;
+        ci = fv.y * w12;
       };
       int k = 0;
       uint32_t ent = my[0];
       while (k < nlist) {
-        const int st = (int)((ent >> 9) & 0x1ffu);
+        const int st = (int)(ent >> 16);
         advance(st);
         for (;;) {
-          const uint32_t ea = ent;
+          const int ea = (int)(ent & 0xffffu);
           ++k;
           ent = (k < nlist) ? my[k] : 0xffffffffu;
-          const bool pair = k < nlist && (int)((ent >> 9) & 0x1ffu) == st;
-          const uint32_t eb = pair ? ent : ea;
+          const bool pair = (int)(ent >> 16) == st && k < nlist;
+          const int eb = pair ? (int)(ent & 0xffffu) : ea;
           if (pair) {
             ++k;
             ent = (k < nlist) ? my[k] : 0xffffffffu;
           }
-          const double ca = coef(ea);
-          const double cb = pair ? coef(eb) : 0.0;
-          const double* wa = recs + (size_t)(ea & 0x1ffu) * RD + R::kW0;
-          const double* wb = recs + (size_t)(eb & 0x1ffu) * RD + R::kW0;
+          double ar, ai, br, bi;
+          coef(ea, ar, ai);
+          coef(eb, br, bi);
+          if (!pair) {
+            br = 0.0;
+            bi = 0.0;
+          }
+          const double* wa = recs + (size_t)ea * RD + R::kW0;
+          const double* wb = recs + (size_t)eb * RD + R::kW0;
 #pragma unroll
           for (int i = 0; i < W; i += 2) {
             const double2 xa = *reinterpret_cast<const double2*>(wa + i);
             const double2 xb = *reinterpret_cast<const double2*>(wb + i);
-            acc[i] = fma(cb, xb.x, fma(ca, xa.x, acc[i]));
-            acc[i + 1] = fma(cb, xb.y, fma(ca, xa.y, acc[i + 1]));
+            acc[i].x = fma(br, xb.x, fma(ar, xa.x, acc[i].x));
+            acc[i].y = fma(bi, xb.x, fma(ai, xa.x, acc[i].y));
+            acc[i + 1].x = fma(br, xb.y, fma(ar, xa.y, acc[i + 1].x));
+            acc[i + 1].y = fma(bi, xb.y, fma(ai, xa.y, acc[i + 1].y));
           }
-          if (!(k < nlist && (int)((ent >> 9) & 0x1ffu) == st)) break;
+          if (!((int)(ent >> 16) == st && k < nlist)) break;
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[stage]);
+    const unsigned long long c3 = prm.prof ? clock64() : 0ull;
     if (hdr.end == 1) advance(nsteps);   // tile finished: flush the remaining nodes
     if (hdr.end == 2) cur = nsteps;      // tile skipped in a multi-group pass: nothing to write
+    if (prm.prof) {
+      tw += c1 - c0;
+      tl += c2 - c1;
+      tf += c3 - c2;
+      tA += clock64() - c3;
+    }
     if (++stage == NS) {
       stage = 0;
       phase ^= 1u;
     }
+  }
+  if (prm.prof && lane == 0) {
+    atomicAdd(prm.prof + 0, tw);
+    atomicAdd(prm.prof + 1, tl);
+    atomicAdd(prm.prof + 2, tf);
+    atomicAdd(prm.prof + 3, tA);
+    atomicAdd(prm.prof + 7, 1ull);
   }
 }
 
@@ -530,12 +582,12 @@ size_t sweep_smem_bytes(int cap) {
   return b + 64;
 }
 
-// CTA patch variant: 0 = 16 x 16 (16 consumer + 4 producer warps), 1 = 12 x 16 (12 + 4 warps).
+// CTA patch variant: 0 = 12 x 32 (12 consumer + 4 producer warps), 1 = 8 x 32 (8 + 4 warps).
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    v = (e && e[0] == '1' && e[1] == '2') ? 1 : 0;
+    v = (e && e[0] == '8') ? 1 : 0;
   }
   return v;
 }
@@ -545,7 +597,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   using L = SweepLayout<P1, P2, M_>;
   const size_t smem_max = (size_t)(226 * 1024);
   int cap = 64;
-  while (sweep_smem_bytes<P1, P2, M_>(cap + 16) <= smem_max && cap + 16 < 512) cap += 16;
+  while (sweep_smem_bytes<P1, P2, M_>(cap + 64) <= smem_max) cap += 64;
   const size_t smem = sweep_smem_bytes<P1, P2, M_>(cap);
   SweepParams prm;
   prm.rec = p->rec;
@@ -563,6 +615,13 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   prm.nseg = (int)(p->n[0] / prm.seg);
   prm.cap = cap;
   prm.tile_counter = p->tile_counter;
+  static const bool prof_on = getenv("HPNFFT_SWEEP_PROF") != nullptr;
+  unsigned long long* prof = nullptr;
+  if (prof_on) {
+    cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), p->stream);
+  }
+  prm.prof = prof;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
   auto kern = k_spread_sweep<P1, P2, M_>;
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -573,6 +632,18 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   const int64_t blocks = tiles < (int64_t)sms ? tiles : (int64_t)sms;
   kern<<<(unsigned)blocks, L::kThreads, smem, p->stream>>>(prm);
   p->launches++;
+  if (prof) {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, p->stream);
+    cudaStreamSynchronize(p->stream);
+    double nw = (double)h[7];
+    fprintf(stderr,
+            "[sweep prof] cap=%d consumer warps=%.0f  per warp Mcycles: wait_full %.2f  lists %.2f  apply %.2f  "
+            "advance %.2f | producer (thread 0 sums, Mcycles): lookups+scan %.2f  wait_empty %.2f  copy %.2f\n",
+            cap, nw, h[0] / nw / 1e6, h[1] / nw / 1e6, h[2] / nw / 1e6, h[3] / nw / 1e6, h[4] / blocks / 1e6,
+            h[5] / blocks / 1e6, h[6] / blocks / 1e6);
+    cudaFree(prof);
+  }
   return check_launch(p, "spread_sweep");
 }
 
@@ -602,8 +673,8 @@ int run_sweep(Plan* p, const double* f) {
                                             p->group_rows);
       p->launches++;
     }
-    int rc = sweep_variant() == 1 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
-                                  : launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi);
+    int rc = sweep_variant() == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+                                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
@@ -616,7 +687,7 @@ size_t record_bytes(int m) { return sizeof(double) * (6 + 3 * 2 * m); }
 
 bool sweep_supported(const Plan* p) {
   const int W = 2 * p->m;
-  const int P1 = 16, P2 = 16;   // largest patch of any variant
+  const int P1 = 12, P2 = 32;   // largest patch of any variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;
   if (p->n[1] < P1 + W - 1) return false;                     // candidate rows must be distinct
   const int bins = (P2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
