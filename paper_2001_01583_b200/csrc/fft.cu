@@ -67,133 +67,143 @@ __device__ __forceinline__ void dft<8>(cplx* v) {
   v[7] = csub(e[3], o3);
 }
 
-// One Stockham stage of radix R on a tile whose column `col` holds the line; `tj` in
-// [0, n/8) is this thread's butterfly slot (8/R butterflies per thread).
-template <int LOGN, int R, int TI>
-__device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, int Ns, const cplx* __restrict__ tw) {
+// Radix plan of an n = 2^LOGN point transform: as many radix-8 stages as possible, then one
+// radix-4 or radix-2 stage, or two radix-4 stages when LOGN % 3 == 1 (and LOGN >= 4).
+__host__ __device__ constexpr int n_radix8(int logn) { return logn / 3 - ((logn % 3 == 1 && logn >= 4) ? 1 : 0); }
+__host__ __device__ constexpr int n_stages(int logn) {
+  return n_radix8(logn) + ((logn - 3 * n_radix8(logn)) == 4 ? 2 : ((logn - 3 * n_radix8(logn)) > 0 ? 1 : 0));
+}
+__host__ __device__ constexpr int radix_of(int logn, int k) {
+  return k < n_radix8(logn) ? 8 : ((logn - 3 * n_radix8(logn)) == 1 ? 2 : 4);
+}
+__host__ __device__ constexpr int ns_of(int logn, int k) { return k == 0 ? 1 : ns_of(logn, k - 1) * radix_of(logn, k - 1); }
+
+// Line context of one thread: its column in the shared tile, its global input/output line.
+struct LineIO {
+  const cplx* gin;       // element a of the line at gin[a * istride]
+  cplx* gout;            // output k' at gout[k' * ostride]
+  int64_t istride, ostride;
+  int N;                 // kept outputs
+  const double* inv_c;   // 1/c_k per kept output
+  bool valid;
+};
+
+// One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
+// shared tile.  Thread slot tj handles 8/R butterflies.  The first stage reads the line straight
+// from global memory and the last writes the pruned, scaled outputs straight to global memory,
+// so a 3-stage transform makes only two shared-memory round trips.
+// Shared-memory slot of element a of the line in column col.  Strided passes (lanes run along
+// the columns): row-major [a][col] with one padding column.  Contiguous pass (lanes run along a):
+// column-major with one padding element every 8, so the stride-8 stores of the first stage and
+// the unit-stride loads are both conflict-free.
+template <int LOGN, int TI, bool CONTIG>
+__device__ __forceinline__ int slot(int a, int col) {
+  constexpr int n = 1 << LOGN;
+  if (CONTIG) return col * (n + n / 8) + a + (a >> 3);
+  return a * (TI + 1) + col;
+}
+template <int LOGN, int TI, bool CONTIG>
+constexpr size_t tile_elems() {
+  return CONTIG ? (size_t)TI * ((1 << LOGN) + (1 << LOGN) / 8) : (size_t)(1 << LOGN) * (TI + 1);
+}
+
+template <int LOGN, int R, int Ns, int TI, bool CONTIG, bool IN_G, bool OUT_G>
+__device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const cplx* __restrict__ tw,
+                                               const LineIO& io) {
   constexpr int n = 1 << LOGN;
   constexpr int BPT = (n >= 8 ? 8 : n) / R;   // butterflies per thread
   constexpr int T = (n >= 8 ? n / 8 : 1);     // threads per column
   cplx v[BPT][R];
 #pragma unroll
   for (int b = 0; b < BPT; ++b) {
-    int j = tj + b * T;
+    const int j = tj + b * T;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[b][r] = buf[(j + r * (n / R)) * (TI + 1) + col];
+    for (int r = 0; r < R; ++r) {
+      const int a = j + r * (n / R);
+      if (IN_G) v[b][r] = io.valid ? io.gin[(int64_t)a * io.istride] : cplx{0.0, 0.0};
+      else v[b][r] = buf[slot<LOGN, TI, CONTIG>(a, col)];
+    }
   }
-  __syncthreads();
+  if (!IN_G) __syncthreads();   // everyone has read the tile before it is overwritten
 #pragma unroll
   for (int b = 0; b < BPT; ++b) {
-    int j = tj + b * T;
-    int jm = j % Ns;
+    const int j = tj + b * T;
+    const int jm = j & (Ns - 1);
     if (Ns > 1) {
-      int step = jm * (n / (Ns * R));
+      const int step = jm * (n / (Ns * R));
 #pragma unroll
       for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], tw[(step * r) & (n - 1)]);
     }
     dft<R>(v[b]);
-    int idxD = (j / Ns) * Ns * R + jm;
+    const int idxD = (j / Ns) * Ns * R + jm;
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[(idxD + r * Ns) * (TI + 1) + col] = v[b][r];
-  }
-  __syncthreads();
-}
-
-template <int LOGN, int TI>
-__device__ __forceinline__ void fft_tile(cplx* buf, int col, int tj, const cplx* __restrict__ tw) {
-  // radix plan: as many radix-8 stages as possible; the remainder is one radix-4 or radix-2
-  // stage, or two radix-4 stages when LOGN % 3 == 1 and LOGN >= 4.
-  constexpr int n8 = LOGN / 3 - ((LOGN % 3 == 1 && LOGN >= 4) ? 1 : 0);
-  constexpr int rem = LOGN - 3 * n8;
-  int Ns = 1;
-  if constexpr (n8 > 0) {
-#pragma unroll
-    for (int s = 0; s < n8; ++s) {
-      stockham_stage<LOGN, 8, TI>(buf, col, tj, Ns, tw);
-      Ns *= 8;
+    for (int r = 0; r < R; ++r) {
+      const int q = idxD + r * Ns;   // frequency index on the oversampled grid
+      if (OUT_G) {
+        const int N = io.N;
+        const bool lo = q < N / 2, hi = q >= n - N / 2;
+        if (io.valid && (lo || hi)) {
+          const int k = lo ? q + N / 2 : q - (n - N / 2);
+          const double sc = io.inv_c[k];
+          io.gout[(int64_t)k * io.ostride] = {v[b][r].x * sc, v[b][r].y * sc};
+        }
+      } else {
+        buf[slot<LOGN, TI, CONTIG>(q, col)] = v[b][r];
+      }
     }
   }
-  if constexpr (rem == 4) {
-    stockham_stage<LOGN, 4, TI>(buf, col, tj, Ns, tw);
-    Ns *= 4;
-    stockham_stage<LOGN, 4, TI>(buf, col, tj, Ns, tw);
-  } else if constexpr (rem == 2) {
-    stockham_stage<LOGN, 4, TI>(buf, col, tj, Ns, tw);
-  } else if constexpr (rem == 1) {
-    stockham_stage<LOGN, 2, TI>(buf, col, tj, Ns, tw);
-  }
+  if (!OUT_G) __syncthreads();   // the tile is complete before the next stage reads it
+}
+
+template <int LOGN, int TI, bool CONTIG, int K>
+__device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cplx* __restrict__ tw, const LineIO& io) {
+  constexpr int NS = n_stages(LOGN);
+  stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, K == NS - 1>(buf, col, tj, tw, io);
+  if constexpr (K + 1 < NS) run_stages<LOGN, TI, CONTIG, K + 1>(buf, col, tj, tw, io);
 }
 
 // Batched pruned pass.  Lines are indexed by (outer o, column i); element a of a line sits at
 //   in + (o * n + a) * inner + i                (inner > 1: strided pass)
 // and for the contiguous pass (CONTIG, inner == 1) the TI columns of a CTA are TI consecutive
 // outers.  Output k' in [0,N) goes to out + (o * N + k') * inner + i, scaled by inv_c[k'].
+// Thread mapping: strided passes put consecutive lanes on consecutive columns (coalesced rows of
+// TI complex); the contiguous pass puts consecutive lanes on consecutive butterflies of a line.
 template <int LOGN, int TI, bool CONTIG>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
            const double* __restrict__ inv_c, const cplx* __restrict__ tw) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
-  constexpr int NT = TI * T;
   extern __shared__ cplx smem[];
-  cplx* buf = smem;
   const int tid = threadIdx.x;
-
-  int64_t o, i0;
-  int cols;
+  LineIO io;
+  io.N = N;
+  io.inv_c = inv_c;
+  int col, tj;
   if (CONTIG) {
-    o = (int64_t)blockIdx.x * TI;          // first outer of this CTA
-    i0 = 0;
-    cols = (int)((outer - o) < TI ? (outer - o) : TI);
+    col = tid / T;
+    tj = tid % T;
+    const int64_t o = (int64_t)blockIdx.x * TI + col;
+    io.valid = o < outer;
+    const int64_t oc = io.valid ? o : 0;
+    io.gin = in + oc * n;
+    io.istride = 1;
+    io.gout = out + oc * (int64_t)N;
+    io.ostride = 1;
   } else {
-    int64_t tiles_per_outer = (inner + TI - 1) / TI;
-    o = blockIdx.x / tiles_per_outer;
-    i0 = (blockIdx.x % tiles_per_outer) * TI;
-    cols = (int)((inner - i0) < TI ? (inner - i0) : TI);
+    col = tid % TI;
+    tj = tid / TI;
+    const int64_t tiles_per_outer = (inner + TI - 1) / TI;
+    const int64_t o = blockIdx.x / tiles_per_outer;
+    const int64_t i = (blockIdx.x % tiles_per_outer) * TI + col;
+    io.valid = i < inner;
+    const int64_t ic = io.valid ? i : 0;
+    io.gin = in + o * (int64_t)n * inner + ic;
+    io.istride = inner;
+    io.gout = out + o * (int64_t)N * inner + ic;
+    io.ostride = inner;
   }
-
-  // ---- load the n x TI tile (coalesced along the contiguous direction) ----
-  if (CONTIG) {
-    const cplx* src = in + o * n;
-    for (int e = tid; e < TI * n; e += NT) {
-      int c = e >> LOGN, a = e & (n - 1);
-      if (c < cols) buf[a * (TI + 1) + c] = src[(int64_t)c * n + a];
-    }
-  } else {
-    const cplx* src = in + o * (int64_t)n * inner + i0;
-    for (int e = tid; e < TI * n; e += NT) {
-      int a = e / TI, c = e % TI;
-      if (c < cols) buf[a * (TI + 1) + c] = src[(int64_t)a * inner + c];
-    }
-  }
-  __syncthreads();
-
-  fft_tile<LOGN, TI>(buf, tid % TI, tid / TI, tw);
-
-  // ---- pruned, scaled store: k' in [0, N) <- grid frequency q = (k' - N/2) mod n ----
-  if (CONTIG) {
-    cplx* dst = out + o * (int64_t)N;
-    for (int e = tid; e < TI * N; e += NT) {
-      int c = e / N, k = e % N;
-      if (c < cols) {
-        int q = (k < N / 2) ? (n - N / 2 + k) : (k - N / 2);
-        cplx v = buf[q * (TI + 1) + c];
-        double s = inv_c[k];
-        dst[(int64_t)c * N + k] = {v.x * s, v.y * s};
-      }
-    }
-  } else {
-    cplx* dst = out + o * (int64_t)N * inner + i0;
-    for (int e = tid; e < TI * N; e += NT) {
-      int k = e / TI, c = e % TI;
-      if (c < cols) {
-        int q = (k < N / 2) ? (n - N / 2 + k) : (k - N / 2);
-        cplx v = buf[q * (TI + 1) + c];
-        double s = inv_c[k];
-        dst[(int64_t)k * inner + c] = {v.x * s, v.y * s};
-      }
-    }
-  }
+  run_stages<LOGN, TI, CONTIG, 0>(smem, col, tj, tw, io);
 }
 
 template <int LOGN>
@@ -207,7 +217,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
   constexpr int TI = tile_cols<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
-  size_t smem = (size_t)n * (TI + 1) * sizeof(cplx);
+  size_t smem = (contig ? tile_elems<LOGN, TI, true>() : tile_elems<LOGN, TI, false>()) * sizeof(cplx);
   int64_t blocks = contig ? (outer + TI - 1) / TI : outer * ((inner + TI - 1) / TI);
   if (blocks <= 0) return HPNFFT_OK;
   if (contig) {
