@@ -120,7 +120,8 @@ int64_t hpnfft_launch_count(hpnfft_plan_t p);
 /*
  * Per-stage device timing (CUDA events on the plan's stream) of the most recent calls, in ms:
  * out[0] keys+histogram, out[1] scan, out[2] scatter, out[3] spread, out[4] FFT pass z,
- * out[5] FFT pass y, out[6] FFT pass x + deconvolve.  Enabled by hpnfft_enable_timing(p, 1);
+ * out[5] FFT pass y, out[6] FFT pass x + deconvolve, out[7] point records (part of out[3]).
+ * Enabled by hpnfft_enable_timing(p, 1);
  * reading synchronises the stream.  Returns the number of values written (<= n).
  */
 int hpnfft_enable_timing(hpnfft_plan_t p, int on);

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("HPNFFT_LIB", os.path.join(_HERE, "libhpnfft.so"))
 
 WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
 SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}
-STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv")
+STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records")
 
 HPNFFT_OK = 0
 _ERRORS = {

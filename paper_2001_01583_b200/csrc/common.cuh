@@ -15,7 +15,7 @@ namespace hpnfft {
 constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
 constexpr int kMinM = 2;
 constexpr int kPolyDeg = 14;      // window tap polynomial degree
-constexpr int kNumStages = 7;     // timing slots, see hpnfft_stage_times
+constexpr int kNumStages = 8;     // timing slots, see hpnfft_stage_times
 
 struct Dims3 {
   int64_t v[3];

@@ -661,11 +661,13 @@ int run_sweep(Plan* p, const double* f) {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
     if (cnt > 0) {
+      stage_begin(p, 7);
       constexpr int PB = 256 / (2 * M_);
       k_point_records<M_><<<(unsigned)((cnt + PB - 1) / PB), 256, 0, p->stream>>>(
           p->xs, p->perm, f, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
       p->launches++;
       int rc = check_launch(p, "point records");
+      stage_end(p, 7);
       if (rc) return rc;
     }
     if (multi) {
