@@ -199,15 +199,17 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   rc = rc ? rc : alloc(p, &p->xs, 3 * (size_t)M);
   p->scan_tmp_elems = scan_workspace_elems(p->nbins);
   rc = rc ? rc : alloc(p, reinterpret_cast<uint32_t**>(&p->scan_tmp), (size_t)p->scan_tmp_elems);
-  rc = rc ? rc : alloc(p, &p->err_flag, 1);
+  rc = rc ? rc : alloc(p, &p->err_flag, 4);
   if (!rc) {
-    cudaError_t e = cudaMallocHost(&p->err_flag_host, sizeof(int));
+    cudaError_t e = cudaMallocHost(&p->err_flag_host, 4 * sizeof(int));
     if (e != cudaSuccess) {
       set_error("pinned allocation failed");
       rc = HPNFFT_E_NOMEM;
     }
   }
   p->bufB = p->grid;   // pass y output reuses the grid (dead after pass z)
+  p->plane_lo = 0;
+  p->plane_len = n[0];
   // records for the sweep spread: all M points if they fit in half of the free memory,
   // otherwise groups of points processed one after another
   if (!rc) {
@@ -264,12 +266,26 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   p->launches = 0;
   int rc = sort_points(p, x);
   if (rc) return rc;
-  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream),
+  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, 3 * sizeof(int), cudaMemcpyDeviceToHost,
+                                     p->stream),
                   "flag d2h");
   HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
-  if (*p->err_flag_host) {
+  if (p->err_flag_host[0]) {
     set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
     return HPNFFT_E_RANGE;
+  }
+  // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
+  {
+    const int64_t n0 = p->n[0];
+    const int64_t lo = p->err_flag_host[1], hi = p->err_flag_host[2];
+    const int64_t len = hi - lo + 2 * p->m;
+    if (p->M == 0 || hi < lo || len >= n0) {
+      p->plane_lo = 0;
+      p->plane_len = n0;
+    } else {
+      p->plane_lo = ((lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
+      p->plane_len = len;
+    }
   }
   p->points_set = true;
   return HPNFFT_OK;

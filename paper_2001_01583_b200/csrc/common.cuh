@@ -56,8 +56,12 @@ struct Plan {
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
   int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep
   int* tile_counter = nullptr;    // sweep tile scheduler counter
-  int* err_flag = nullptr;        // device range-error flag
-  int* err_flag_host = nullptr;   // pinned mirror
+  int* err_flag = nullptr;        // device [4]: range-error flag, min / max of the x-ordered cell c0
+  int* err_flag_host = nullptr;   // pinned mirror [4]
+  // occupied l0 planes (circular interval [plane_lo, plane_lo + plane_len) mod n0): planes that
+  // receive any tap of the current points.  Planes outside are zero and are skipped by the sweep
+  // and the first two FFT passes (x-slab subcells of the multi-GPU layer).
+  int64_t plane_lo = 0, plane_len = 0;
   size_t ws_bytes = 0;
 
   int64_t launches = 0;         // kernel launches since the last set_points

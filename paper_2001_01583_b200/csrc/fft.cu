@@ -86,6 +86,7 @@ struct LineIO {
   int N;                 // kept outputs
   const double* inv_c;   // 1/c_k per kept output
   bool valid;
+  int a_lo, a_len;       // elements a with (a - a_lo) mod n < a_len are loaded, the others are 0
 };
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
@@ -120,7 +121,9 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int a = j + r * (n / R);
-      if (IN_G) v[b][r] = io.valid ? io.gin[(int64_t)a * io.istride] : cplx{0.0, 0.0};
+      if (IN_G)
+        v[b][r] = (io.valid && ((a - io.a_lo) & (n - 1)) < io.a_len) ? io.gin[(int64_t)a * io.istride]
+                                                                      : cplx{0.0, 0.0};
       else v[b][r] = buf[slot<LOGN, TI, CONTIG>(a, col)];
     }
   }
@@ -171,7 +174,8 @@ __device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cpl
 template <int LOGN, int TI, bool CONTIG>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
-           const double* __restrict__ inv_c, const cplx* __restrict__ tw) {
+           const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
+           int a_len) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
   extern __shared__ cplx smem[];
@@ -179,13 +183,15 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
   LineIO io;
   io.N = N;
   io.inv_c = inv_c;
+  io.a_lo = a_lo;
+  io.a_len = a_len;
   int col, tj;
   if (CONTIG) {
     col = tid / T;
     tj = tid % T;
     const int64_t o = (int64_t)blockIdx.x * TI + col;
     io.valid = o < outer;
-    const int64_t oc = io.valid ? o : 0;
+    const int64_t oc = io.valid ? (o_start + o) % o_total : 0;
     io.gin = in + oc * n;
     io.istride = 1;
     io.gout = out + oc * (int64_t)N;
@@ -194,7 +200,7 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     col = tid % TI;
     tj = tid / TI;
     const int64_t tiles_per_outer = (inner + TI - 1) / TI;
-    const int64_t o = blockIdx.x / tiles_per_outer;
+    const int64_t o = (o_start + blockIdx.x / tiles_per_outer) % o_total;
     const int64_t i = (blockIdx.x % tiles_per_outer) * TI + col;
     io.valid = i < inner;
     const int64_t ic = io.valid ? i : 0;
@@ -213,7 +219,8 @@ constexpr int tile_cols() {
 
 template <int LOGN>
 static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
-                         const double* inv_c, const cplx* tw, bool contig) {
+                         const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
+                         int a_lo, int a_len) {
   constexpr int TI = tile_cols<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
@@ -224,32 +231,35 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     auto kern = k_fft_pass<LOGN, TI, true>;
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
-    kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw);
+    kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
+                                                     a_len);
   } else {
     auto kern = k_fft_pass<LOGN, TI, false>;
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
-    kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw);
+    kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
+                                                     a_len);
   }
   p->launches++;
   return check_launch(p, "fft pass");
 }
 
 static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t outer, int64_t inner, int N,
-                       const double* inv_c, const double* tw, bool contig) {
+                       const double* inv_c, const double* tw, bool contig, int64_t o_start, int64_t o_total,
+                       int a_lo, int a_len) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
   cplx* co = reinterpret_cast<cplx*>(out);
   const cplx* ct = reinterpret_cast<const cplx*>(tw);
   switch (logn) {
-    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig);
-    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig);
+    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
     default:
       set_error("FFT length not supported");
       return HPNFFT_E_UNSUPPORTED;
@@ -259,17 +269,22 @@ static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t
 int fft_and_deconvolve(Plan* p, double* fhat) {
   const int64_t n0 = p->n[0], n1 = p->n[1];
   const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
+  // only the occupied l0 planes are transformed by passes z and y; pass x treats the others as 0
+  const int64_t plo = p->plane_lo, plen = p->plane_len;
   int rc;
   stage_begin(p, 4);
-  rc = launch_pass(p, p->logn[2], p->grid, p->bufA, n0 * n1, 1, (int)N2, p->inv_c[2], p->twiddle[2], true);
+  rc = launch_pass(p, p->logn[2], p->grid, p->bufA, plen * n1, 1, (int)N2, p->inv_c[2], p->twiddle[2], true,
+                   plo * n1, n0 * n1, 0, (int)p->n[2]);
   stage_end(p, 4);
   if (rc) return rc;
   stage_begin(p, 5);
-  rc = launch_pass(p, p->logn[1], p->bufA, p->bufB, n0, N2, (int)N1, p->inv_c[1], p->twiddle[1], false);
+  rc = launch_pass(p, p->logn[1], p->bufA, p->bufB, plen, N2, (int)N1, p->inv_c[1], p->twiddle[1], false, plo, n0,
+                   0, (int)n1);
   stage_end(p, 5);
   if (rc) return rc;
   stage_begin(p, 6);
-  rc = launch_pass(p, p->logn[0], p->bufB, fhat, 1, N1 * N2, (int)N0, p->inv_c[0], p->twiddle[0], false);
+  rc = launch_pass(p, p->logn[0], p->bufB, fhat, 1, N1 * N2, (int)N0, p->inv_c[0], p->twiddle[0], false, 0, 1,
+                   (int)plo, (int)plen);
   stage_end(p, 6);
   (void)N0;
   return rc;

@@ -17,6 +17,18 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
                        uint32_t* __restrict__ count, uint32_t* __restrict__ key, uint32_t* __restrict__ rank,
                        int* __restrict__ err) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // occupied range of the x-ordered plane index c0x = (c0 + n0/2) mod n0 (monotone in x0):
+  // warp min/max, one atomic per warp
+  unsigned cx = 0xffffffffu, cxm = 0u;
+  if (j < M) {
+    const int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x[3 * j])) & (n0 - 1);
+    cx = cxm = (unsigned)((c0 + n0 / 2) & (n0 - 1));
+  }
+  const unsigned wmin = __reduce_min_sync(0xffffffffu, cx), wmax = __reduce_max_sync(0xffffffffu, cxm);
+  if ((threadIdx.x & 31) == 0 && wmin != 0xffffffffu) {
+    atomicMin(err + 1, (int)wmin);
+    atomicMax(err + 2, (int)wmax);
+  }
   if (j >= M) return;
   double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
   if (!(fabs(x0) <= 0.5 && fabs(x1) <= 0.5 && fabs(x2) <= 0.5)) {
@@ -150,6 +162,8 @@ int sort_points(Plan* p, const double* x) {
   const int64_t M = p->M;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count, 0, sizeof(uint32_t) * (p->nbins + 1), p->stream), "memset bins");
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag, 0, sizeof(int), p->stream), "memset flag");
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag + 1, 0x7f, sizeof(int), p->stream), "memset min");
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag + 2, 0xff, sizeof(int), p->stream), "memset max");
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   stage_begin(p, 0);

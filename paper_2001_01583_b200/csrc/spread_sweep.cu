@@ -85,7 +85,8 @@ struct SweepParams {
   int n0, n1, n2;
   int nb2;                 // n2 / 8
   int seg;                 // S: planes per segment
-  int nseg;                // n0 / S
+  int nseg;                // segments covering the occupied planes
+  int plane_lo, plane_len; // occupied l0 planes (circular interval)
   int cap;                 // record capacity of one shared-memory batch buffer
   int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
   unsigned long long* prof;   // optional clock64 phase counters (HPNFFT_SWEEP_PROF=1), else null
@@ -257,7 +258,6 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
   const int npc = n2 / P2, npr = (n1 + P1 - 1) / P1;
   const int ntiles = npc * npr * prm.nseg;
-  const int nsteps = prm.seg + W - 1;   // planes cur = L0 - m .. L0 + S + m - 2 of a tile
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -274,7 +274,12 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
     const int segi = rest / npr;
     R0 = pr * P1;
     C0 = pc * P2;
-    L0 = segi * prm.seg;
+    L0 = prm.plane_lo + segi * prm.seg;
+  };
+  // planes cur = L0 - m .. L0 + S' + m - 2 of a tile, S' = its segment length
+  auto tile_steps = [&](int t) -> int {
+    const int segi = (t / npc) / npr;
+    return min(prm.seg, prm.plane_len - segi * prm.seg) + W - 1;
   };
   auto tile_skip = [&](int R0) -> bool {   // multi-group pass: rows of the tile miss the group
     if (!prm.accumulate) return false;
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
       int R0, C0, L0;
       tile_geom(t, R0, C0, L0);
       const int first = L0 - M_;
+      const int nsteps = tile_steps(t);
       const bool skip = tile_skip(R0);
       if (!skip) {
         const int b2lo = (C0 - M_ >= 0) ? (C0 - M_) / kBinW : -((M_ - C0 + kBinW - 1) / kBinW);
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
   const int wr_off = (warp / (P2 / kWC)) * kWR;
   const int wc_off = (warp % (P2 / kWC)) * kWC;
   int cur_tile = -1;
-  int first = 0, wr0 = 0, wc0 = 0, lo1 = 0, lo2 = 0;
+  int first = 0, wr0 = 0, wc0 = 0, lo1 = 0, lo2 = 0, nsteps = 0;
   bool valid = true;
   double2* gcol = nullptr;
   const size_t plane = (size_t)n1 * n2;
@@ -459,6 +465,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
       int R0, C0, L0;
       tile_geom(cur_tile, R0, C0, L0);
       first = L0 - M_;
+      nsteps = tile_steps(cur_tile);
       wr0 = R0 + wr_off;
       wc0 = C0 + wc_off;
       const int l1 = wr0 + lane / kWC;
@@ -611,8 +618,10 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
   prm.n1 = (int)p->n[1];
   prm.n2 = (int)p->n[2];
   prm.nb2 = (int)(p->n[2] / kBinW);
-  prm.seg = (int)(p->n[0] < 256 ? p->n[0] : 256);
-  prm.nseg = (int)(p->n[0] / prm.seg);
+  prm.plane_lo = (int)p->plane_lo;
+  prm.plane_len = (int)p->plane_len;
+  prm.seg = (int)(p->plane_len < 256 ? p->plane_len : 256);
+  prm.nseg = (int)((p->plane_len + prm.seg - 1) / prm.seg);
   prm.cap = cap;
   prm.tile_counter = p->tile_counter;
   static const bool prof_on = getenv("HPNFFT_SWEEP_PROF") != nullptr;

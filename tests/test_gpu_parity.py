@@ -242,3 +242,34 @@ def test_sweep_multi_group_accumulate(dist, monkeypatch):
     f = inputs.uniform_values(M, seed=14)
     g = gpu_adjoint(x, f, N, method="sweep")
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("lo,hi", [(-0.5, -0.375), (-0.1, 0.1), (0.3, 0.5), (0.49, 0.5), (-0.01, 0.0),
+                                   (-0.5, 0.5)])
+@pytest.mark.parametrize("method", ["auto", "atomic"])
+def test_thin_slabs_prune_planes(lo, hi, method):
+    """Points confined to an x0 slab (the multi-GPU subcells): the sweep and the first
+    two FFT passes only touch the occupied l0 planes; results must not change."""
+    N, M = (64, 32, 64), 20000
+    x = inputs.uniform_points(M, seed=15)
+    x[:, 0] = lo + (hi - lo) * (x[:, 0] + 0.5)
+    x[-1, 0] = hi if hi == 0.5 else x[-1, 0]
+    f = inputs.uniform_values(M, seed=15)
+    g = gpu_adjoint(x, f, N, method=method)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+def test_plan_reuse_shrinking_and_growing_slabs():
+    """Plane pruning is recomputed at every set_points (stale planes must never leak in)."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (64, 32, 64), 5000
+    plan = hp.Plan(N, M, device=dev)
+    for lo, hi in [(-0.5, 0.5), (0.1, 0.2), (-0.5, 0.5), (-0.3, -0.29)]:
+        x = inputs.uniform_points(M, seed=16)
+        x[:, 0] = lo + (hi - lo) * (x[:, 0] + 0.5)
+        f = inputs.uniform_values(M, seed=16)
+        plan.set_points(torch.from_numpy(x).to(dev))
+        g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+        assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    plan.close()
