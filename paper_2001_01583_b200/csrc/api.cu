@@ -32,25 +32,25 @@ int check_launch(Plan* p, const char* what) {
   return HPNFFT_OK;
 }
 
+// Each stage call owns a begin/end pair of pool events; stages may nest (records inside spread).
 void stage_begin(Plan* p, int slot) {
-  if (!p->timing) return;
-  if ((int)p->ev.size() < p->ev_used + 2) {
-    cudaEvent_t a, b;
+  if (!p->timing || slot < 0 || slot >= kNumStages) return;
+  while ((int)p->ev.size() < p->ev_used + 2) {
+    cudaEvent_t a;
     cudaEventCreate(&a);
-    cudaEventCreate(&b);
     p->ev.push_back(a);
-    p->ev.push_back(b);
   }
   cudaEventRecord(p->ev[p->ev_used], p->stream);
-  (void)slot;
+  p->ev_open[slot] = p->ev_used;
+  p->ev_used += 2;
 }
 
-// each begin/end pair occupies two consecutive pool events; ev_slot[pair] is its stage id
 void stage_end(Plan* p, int slot) {
-  if (!p->timing) return;
-  cudaEventRecord(p->ev[p->ev_used + 1], p->stream);
-  p->ev_used += 2;
+  if (!p->timing || slot < 0 || slot >= kNumStages || p->ev_open[slot] < 0) return;
+  cudaEventRecord(p->ev[p->ev_open[slot] + 1], p->stream);
   p->ev_slot.push_back(slot);
+  p->ev_pair.push_back(p->ev_open[slot]);
+  p->ev_open[slot] = -1;
 }
 
 int64_t scan_workspace_elems(int64_t nbins);
@@ -199,9 +199,9 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   rc = rc ? rc : alloc(p, &p->xs, 3 * (size_t)M);
   p->scan_tmp_elems = scan_workspace_elems(p->nbins);
   rc = rc ? rc : alloc(p, reinterpret_cast<uint32_t**>(&p->scan_tmp), (size_t)p->scan_tmp_elems);
-  rc = rc ? rc : alloc(p, &p->err_flag, 4);
+  rc = rc ? rc : alloc(p, &p->err_flag, 1 + 2 * kRangeSlots);
   if (!rc) {
-    cudaError_t e = cudaMallocHost(&p->err_flag_host, 4 * sizeof(int));
+    cudaError_t e = cudaMallocHost(&p->err_flag_host, (1 + 2 * kRangeSlots) * sizeof(int));
     if (e != cudaSuccess) {
       set_error("pinned allocation failed");
       rc = HPNFFT_E_NOMEM;
@@ -266,8 +266,8 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   p->launches = 0;
   int rc = sort_points(p, x);
   if (rc) return rc;
-  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, 3 * sizeof(int), cudaMemcpyDeviceToHost,
-                                     p->stream),
+  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, (1 + 2 * kRangeSlots) * sizeof(int),
+                                     cudaMemcpyDeviceToHost, p->stream),
                   "flag d2h");
   HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
   if (p->err_flag_host[0]) {
@@ -277,7 +277,11 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
   {
     const int64_t n0 = p->n[0];
-    const int64_t lo = p->err_flag_host[1], hi = p->err_flag_host[2];
+    int64_t lo = 0x7fffffff, hi = -1;
+    for (int sl = 0; sl < kRangeSlots; ++sl) {
+      lo = lo < p->err_flag_host[1 + 2 * sl] ? lo : p->err_flag_host[1 + 2 * sl];
+      hi = hi > p->err_flag_host[2 + 2 * sl] ? hi : p->err_flag_host[2 + 2 * sl];
+    }
     const int64_t len = hi - lo + 2 * p->m;
     if (p->M == 0 || hi < lo || len >= n0) {
       p->plane_lo = 0;
@@ -383,7 +387,7 @@ int hpnfft_stage_times(hpnfft_plan_t h, float* out, int nout) {
   int cnt[kNumStages] = {0};
   for (size_t pair = 0; pair < p->ev_slot.size(); ++pair) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, p->ev[2 * pair], p->ev[2 * pair + 1]);
+    cudaEventElapsedTime(&ms, p->ev[p->ev_pair[pair]], p->ev[p->ev_pair[pair] + 1]);
     int sl = p->ev_slot[pair];
     if (sl >= 0 && sl < kNumStages) {
       acc[sl] += ms;
@@ -391,6 +395,7 @@ int hpnfft_stage_times(hpnfft_plan_t h, float* out, int nout) {
     }
   }
   p->ev_slot.clear();
+  p->ev_pair.clear();
   p->ev_used = 0;
   int w = 0;
   for (int s = 0; s < kNumStages && w < nout; ++s, ++w) out[w] = cnt[s] ? (float)(acc[s] / cnt[s]) : 0.0f;

@@ -16,6 +16,7 @@ constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMa
 constexpr int kMinM = 2;
 constexpr int kPolyDeg = 14;      // window tap polynomial degree
 constexpr int kNumStages = 8;     // timing slots, see hpnfft_stage_times
+constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction
 
 struct Dims3 {
   int64_t v[3];
@@ -56,8 +57,9 @@ struct Plan {
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
   int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep
   int* tile_counter = nullptr;    // sweep tile scheduler counter
-  int* err_flag = nullptr;        // device [4]: range-error flag, min / max of the x-ordered cell c0
-  int* err_flag_host = nullptr;   // pinned mirror [4]
+  int* err_flag = nullptr;        // device [1 + 2 kRangeSlots]: range-error flag, then slot pairs of
+                                  // min / max of the x-ordered cell c0
+  int* err_flag_host = nullptr;   // pinned mirror
   // occupied l0 planes (circular interval [plane_lo, plane_lo + plane_len) mod n0): planes that
   // receive any tap of the current points.  Planes outside are zero and are skipped by the sweep
   // and the first two FFT passes (x-slab subcells of the multi-GPU layer).
@@ -71,6 +73,8 @@ struct Plan {
   std::vector<cudaEvent_t> ev;  // pool, kNumStages+1 events per call
   int ev_used = 0;
   std::vector<int> ev_slot;     // stage id of each recorded begin/end pair
+  std::vector<int> ev_pair;     // pool index of the pair's begin event
+  int ev_open[kNumStages] = {-1, -1, -1, -1, -1, -1, -1, -1};
   double stage_ms_acc[kNumStages] = {0};
   int stage_calls[kNumStages] = {0};
 };

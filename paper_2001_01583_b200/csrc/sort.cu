@@ -13,6 +13,12 @@
 
 namespace hpnfft {
 
+__global__ void k_range_init(int* err) {
+  const int t = threadIdx.x;
+  if (t == 0) err[0] = 0;                                 // range-error flag
+  else err[t] = (t & 1) ? 0x7fffffff : -1;                // slot minima / maxima
+}
+
 __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2,
                        uint32_t* __restrict__ count, uint32_t* __restrict__ key, uint32_t* __restrict__ rank,
                        int* __restrict__ err) {
@@ -24,10 +30,25 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
     const int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x[3 * j])) & (n0 - 1);
     cx = cxm = (unsigned)((c0 + n0 / 2) & (n0 - 1));
   }
+  // block min/max, then one atomic pair per block into one of kRangeSlots slot pairs
+  __shared__ unsigned s_min[8], s_max[8];
   const unsigned wmin = __reduce_min_sync(0xffffffffu, cx), wmax = __reduce_max_sync(0xffffffffu, cxm);
-  if ((threadIdx.x & 31) == 0 && wmin != 0xffffffffu) {
-    atomicMin(err + 1, (int)wmin);
-    atomicMax(err + 2, (int)wmax);
+  if ((threadIdx.x & 31) == 0) {
+    s_min[threadIdx.x >> 5] = wmin;
+    s_max[threadIdx.x >> 5] = wmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned bmin = 0xffffffffu, bmax = 0u;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      bmin = min(bmin, s_min[w]);
+      bmax = max(bmax, s_max[w]);
+    }
+    if (bmin != 0xffffffffu) {
+      const int slot = (int)(blockIdx.x % kRangeSlots);
+      atomicMin(err + 1 + 2 * slot, (int)bmin);
+      atomicMax(err + 2 + 2 * slot, (int)bmax);
+    }
   }
   if (j >= M) return;
   double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
@@ -161,9 +182,8 @@ int64_t scan_workspace_elems(int64_t nbins) { return scan_tmp_need(nbins + 1); }
 int sort_points(Plan* p, const double* x) {
   const int64_t M = p->M;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count, 0, sizeof(uint32_t) * (p->nbins + 1), p->stream), "memset bins");
-  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag, 0, sizeof(int), p->stream), "memset flag");
-  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag + 1, 0x7f, sizeof(int), p->stream), "memset min");
-  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->err_flag + 2, 0xff, sizeof(int), p->stream), "memset max");
+  k_range_init<<<1, 2 * kRangeSlots + 1, 0, p->stream>>>(p->err_flag);
+  p->launches++;
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   stage_begin(p, 0);

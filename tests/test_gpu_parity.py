@@ -273,3 +273,24 @@ def test_plan_reuse_shrinking_and_growing_slabs():
         g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
         assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
     plan.close()
+
+
+def test_stage_timing_and_launch_count():
+    """Per-stage CUDA-event timing (nested records stage inside spread) and the launch counter."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (64, 64, 64), 50000
+    plan = hp.Plan(N, M, device=dev)
+    x, f = inputs.uniform_points(M, seed=17), inputs.uniform_values(M, seed=17)
+    xd, fd = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
+    plan.enable_timing(True)
+    for _ in range(3):
+        plan.set_points(xd)
+        plan.adjoint(fd)
+    t = plan.stage_times()
+    assert set(t) == set(hp.STAGES)
+    assert all(v > 0 for v in t.values())
+    assert t["records"] < t["spread"]
+    assert plan.launch_count() >= 8
+    plan.enable_timing(False)
+    plan.close()
