@@ -418,6 +418,176 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
   }
 
   // =============================== consumer warps ===============================
+#ifndef HPNFFT_SWEEP_DFMA
+  // FP64 tensor-core consumer (DMMA m8n8k4).  A warp owns a 4 x 8 sub-patch of columns; its
+  // accumulator is the 16 x 64 real matrix C[node row][2 x complex column] held as 2 x 8 DMMA
+  // C-fragments.  Node rows are cyclic (row = l0-node mod 16), so the 2m-node sliding window needs
+  // no data movement: a finished node row is stored and zeroed.  Four records per k-step:
+  //   C += A (16 x 4: w0 of each record placed at its plane's cyclic offset)
+  //      x B (4 x 64: f w1[i1] w2[i2] of each record for every column, 0 outside its footprint)
+  // i.e. 16 DMMA (4096 FMA) per k-step instead of 4 x 24 DFMA per lane; records of up to
+  // 16 - 2m + 1 consecutive planes share a k-step.
+  static_assert(2 * M_ <= 16, "cyclic 16-row window");
+  const int wr_off = (warp / (P2 / kWC)) * kWR;
+  const int wc_off = (warp % (P2 / kWC)) * kWC;
+  const int g = lane >> 2, t = lane & 3;
+  const int part = g & 1;                 // B: real (0) or imaginary (1) part of the column
+  const int bc0 = g >> 1;                 // B: column offset inside a half n-tile pair
+  int cur_tile = -1;
+  int first = 0, wr0 = 0, wc0 = 0, nsteps = 0;
+  double cfr[2][8][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
+  int cur = 0;                            // planes < cur are flushed
+  const size_t plane = (size_t)n1 * n2;
+
+  auto flush_plane = [&](int sp) {        // plane sp (relative) done: node sp - m + 1 is final
+    const int rho = (sp - M_ + 1) & 15;
+    const bool mine = g == (rho & 7);
+    const bool write = sp >= W - 1;
+    const int l0 = (first + sp - M_ + 1) & (n0 - 1);
+    double2* base = reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      double v0, v1;
+      if (rho < 8) { v0 = cfr[0][nt][0]; v1 = cfr[0][nt][1]; }
+      else { v0 = cfr[1][nt][0]; v1 = cfr[1][nt][1]; }
+      const int q = 4 * nt + t;           // complex column of this lane's pair (re, im)
+      const int l1 = wr0 + (q >> 3), l2 = wc0 + (q & 7);
+      if (mine && write && l1 < n1) {
+        double2* dst = base + (size_t)l1 * n2 + l2;
+        if (prm.accumulate) {
+          double2 o = *dst;
+          o.x += v0;
+          o.y += v1;
+          *dst = o;
+        } else {
+          *dst = make_double2(v0, v1);
+        }
+      }
+      if (mine) {
+        if (rho < 8) { cfr[0][nt][0] = 0.0; cfr[0][nt][1] = 0.0; }
+        else { cfr[1][nt][0] = 0.0; cfr[1][nt][1] = 0.0; }
+      }
+    }
+  };
+  auto advance = [&](int upto) {
+    while (cur < upto) {
+      flush_plane(cur);
+      ++cur;
+    }
+  };
+
+  int stage = 0;
+  uint32_t phase = 0;
+  unsigned long long tw = 0, tl = 0, tf = 0, tA = 0;
+  for (;;) {
+    const unsigned long long c0 = prm.prof ? clock64() : 0ull;
+    mbar_wait(&s_full[stage], phase);
+    const unsigned long long c1 = prm.prof ? clock64() : 0ull;
+    const BatchHdr hdr = s_hdr[stage];
+    if (hdr.B < 0) break;
+    if (hdr.tile != cur_tile) {
+      cur_tile = hdr.tile;
+      int R0, C0, L0;
+      tile_geom(cur_tile, R0, C0, L0);
+      first = L0 - M_;
+      nsteps = tile_steps(cur_tile);
+      wr0 = R0 + wr_off;
+      wc0 = C0 + wc_off;
+      cur = 0;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
+    }
+    const int B = hdr.B;
+    const double* recs = s_rec + (size_t)stage * cap * RD;
+    const uint16_t* stp = s_step + stage * cap;
+    // ---- plane-ordered list: entry = record | plane << 9 | d1 << 18 | d2 << 23 with
+    //      d1 = wr0 - (c1-m+1) + 3 < 2m + 3, d2 = wc0 - (c2-m+1) + 7 < 2m + 7 ----
+    int nlist = 0;
+    uint32_t* my = s_list + (size_t)warp * cap;
+    for (int base = 0; base < B; base += 32) {
+      const int e = base + lane;
+      bool rel = false;
+      uint32_t entry = 0;
+      if (e < B) {
+        const int2 cc = *reinterpret_cast<const int2*>(recs + (size_t)e * RD);
+        const uint32_t d1 = (uint32_t)((wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1));
+        const uint32_t d2 = (uint32_t)((wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1));
+        rel = (d1 < (uint32_t)(W + kWR - 1)) && (d2 < (uint32_t)(W + kWC - 1));
+        entry = (uint32_t)e | ((uint32_t)stp[e] << 9) | (d1 << 18) | (d2 << 23);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, rel);
+      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = entry;
+      nlist += __popc(bal);
+    }
+    __syncwarp();
+    const unsigned long long c2 = prm.prof ? clock64() : 0ull;
+    // ---- k-steps of up to 4 records spanning at most 16 - 2m + 1 planes ----
+    for (int k = 0; k < nlist;) {
+      const uint32_t e0 = my[k];
+      const int st0 = (int)((e0 >> 9) & 0x1ffu);
+      const uint32_t en = (k + t < nlist) ? my[k + t] : 0xffffffffu;
+      const int st = (int)((en >> 9) & 0x1ffu);
+      const bool ok = (k + t < nlist) && (st - st0 <= 16 - W);
+      const unsigned okm = __ballot_sync(0xffffffffu, ok) & 0xfu;   // lanes 0..3 decide
+      const int cnt = __popc(okm);                                  // prefix by plane order
+      advance(st0);
+      // this lane's record: k + t (lanes with t >= cnt contribute zeros)
+      const bool act = t < cnt;
+      const double* r = recs + (size_t)(act ? (en & 0x1ffu) : 0u) * RD;
+      const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
+      // A fragments: rows 8 mt + g hold node (row - (st - m + 1)) mod 16 of this record
+      double afr[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int i = (8 * mt + g - (st - M_ + 1)) & 15;
+        afr[mt] = (act && i < W) ? r[R::kW0 + i] : 0.0;
+      }
+      // B fragments: column q = 4 nt + g/2 (row q/8 = nt/2, col q%8 = 4 (nt&1) + g/2), part g&1
+      const double fp = act ? r[2 + part] : 0.0;
+      double fw1[4];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const unsigned i1 = min((unsigned)(d1 - (kWR - 1) + rr), (unsigned)W);
+        fw1[rr] = fp * r[R::kW1 + i1];
+      }
+      const unsigned ia = min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W);
+      const unsigned ib = min((unsigned)(d2 - (kWC - 1) + 4 + bc0), (unsigned)W);
+      const double w2a = r[R::kW2 + ia], w2b = r[R::kW2 + ib];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const double bfr = fw1[nt >> 1] * ((nt & 1) ? w2b : w2a);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+              : "+d"(cfr[mt][nt][0]), "+d"(cfr[mt][nt][1])
+              : "d"(afr[mt]), "d"(bfr));
+        }
+      }
+      k += cnt;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[stage]);
+    const unsigned long long c3 = prm.prof ? clock64() : 0ull;
+    if (hdr.end == 1) advance(nsteps);   // tile finished: flush the remaining nodes
+    if (hdr.end == 2) cur = nsteps;      // tile skipped in a multi-group pass: nothing to write
+    if (prm.prof) {
+      tw += c1 - c0;
+      tl += c2 - c1;
+      tf += c3 - c2;
+      tA += clock64() - c3;
+    }
+    if (++stage == NS) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+#else
   const int wr_off = (warp / (P2 / kWC)) * kWR;
   const int wc_off = (warp % (P2 / kWC)) * kWC;
   int cur_tile = -1;
@@ -564,6 +734,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
       phase ^= 1u;
     }
   }
+#endif
   if (prm.prof && lane == 0) {
     atomicAdd(prm.prof + 0, tw);
     atomicAdd(prm.prof + 1, tl);
