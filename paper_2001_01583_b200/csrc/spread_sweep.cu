@@ -33,8 +33,13 @@ namespace hpnfft {
 
 namespace {
 
+#ifdef HPNFFT_SWEEP_DFMA
 constexpr int kWR = 4;          // warp sub-patch: 4 rows (l1) x 8 cols (l2) = 32 lanes
 constexpr int kWC = 8;
+#else
+constexpr int kWR = 4;          // warp sub-patch of the DMMA consumer: 4 rows (l1) x 4 cols (l2)
+constexpr int kWC = 4;
+#endif
 constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 #ifndef HPNFFT_SWEEP_NS
 #define HPNFFT_SWEEP_NS 3
@@ -90,6 +95,7 @@ struct SweepParams {
   int cap;                 // record capacity of one shared-memory batch buffer
   int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
   unsigned long long* prof;   // optional clock64 phase counters (HPNFFT_SWEEP_PROF=1), else null
+  int debug;               // measurement only (HPNFFT_SWEEP_DEBUG): 1 = skip the MMAs, 2 = skip apply
 };
 
 }  // namespace
@@ -213,6 +219,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+// TMA bulk copy global -> shared, completion counted on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem)),
+      "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void producer_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
 struct BatchHdr {
@@ -261,7 +281,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(&s_full[i], NPT);
+      mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], NW);
     }
   }
@@ -323,27 +343,39 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
           const int ne = nch * np_used;
           const int per = (ne + NPT - 1) / NPT;
           const unsigned long long p0 = prm.prof ? clock64() : 0ull;
-          // (plane, pencil) ranges clipped to the group; thread owns entries [pt*per, pt*per+per)
-          uint32_t local = 0;
-          for (int k = 0; k < per; ++k) {
-            const int e = pt * per + k;
-            if (e >= ne) break;
-            const int sidx = e / np_used, pidx = e - sidx * np_used;
-            const int r = pidx / nq, q = pidx - r * nq;
+          // (plane, pencil) ranges clipped to the group, pencil-major: thread -> pencil, all planes
+          // of the chunk (independent loads, consecutive bins); stored plane-major for the scan
+          for (int pp = pt; pp < np_used; pp += NPT) {
+            const int r = pp / nq, q = pp - r * nq;
             const int c1 = (R0 - M_ + r) & (n1 - 1);
             int b2 = (b2lo + q) % prm.nb2;
             if (b2 < 0) b2 += prm.nb2;
-            const int c0 = (first + ch0 + sidx) & (n0 - 1);
-            const size_t bin = ((size_t)c1 * prm.nb2 + b2) * n0 + c0;
-            uint32_t lo = __ldg(prm.start + bin), hi = __ldg(prm.start + bin + 1);
-            lo = max(lo, prm.g0);
-            hi = min(hi, prm.g1);
-            const uint32_t cnt = hi > lo ? hi - lo : 0u;
-            s_beg[e] = lo - prm.g0;
-            s_off[e] = cnt;
-            local += cnt;
+            const size_t pbase = ((size_t)c1 * prm.nb2 + b2) * n0;
+            uint32_t lo[kChunk], hi[kChunk];
+#pragma unroll
+            for (int sidx = 0; sidx < kChunk; ++sidx) {
+              if (sidx < nch) {
+                const size_t bin = pbase + ((first + ch0 + sidx) & (n0 - 1));
+                lo[sidx] = __ldg(prm.start + bin);
+                hi[sidx] = __ldg(prm.start + bin + 1);
+              }
+            }
+#pragma unroll
+            for (int sidx = 0; sidx < kChunk; ++sidx) {
+              if (sidx < nch) {
+                const uint32_t l = max(lo[sidx], prm.g0), h = min(hi[sidx], prm.g1);
+                s_beg[sidx * np_used + pp] = l - prm.g0;
+                s_off[sidx * np_used + pp] = h > l ? h - l : 0u;
+              }
+            }
           }
-          // exclusive scan over the producer threads
+          producer_bar(NPT);
+          // exclusive scan in (plane-major, pencil-minor) order; thread owns entries [pt*per, +per)
+          uint32_t local = 0;
+          for (int k = 0; k < per; ++k) {
+            const int e = pt * per + k;
+            if (e < ne) local += s_off[e];
+          }
           const uint32_t incl = warp_incl_scan(local, lane);
           if (lane == 31) s_misc[pw] = incl;
           producer_bar(NPT);
@@ -370,7 +402,12 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
             const unsigned long long p1 = prm.prof ? clock64() : 0ull;
             mbar_wait(&s_empty[stage], phase ^ 1u);
             const unsigned long long p2 = prm.prof ? clock64() : 0ull;
+            if (pt == 0) mbar_expect_tx(&s_full[stage], (uint32_t)B * (uint32_t)(RD * sizeof(double)));
+            producer_bar(NPT);
+            // one TMA bulk copy per (plane, pencil) range: its records are contiguous in HBM and
+            // land in consecutive batch slots
             uint16_t* stp = s_step + stage * cap;
+            double* dst = s_rec + (size_t)stage * cap * RD;
             for (int k = 0; k < per; ++k) {
               const int e = pt * per + k;
               if (e >= ne) break;
@@ -381,65 +418,63 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
               const uint32_t k0 = off < b0 ? b0 - off : 0u;
               const uint32_t k1 = min(cnt, b1 - off);
               const uint16_t step = (uint16_t)(ch0 + e / np_used);
-              for (uint32_t kk = k0; kk < k1; ++kk) {
-                s_idx[off + kk - b0] = beg + kk;
-                stp[off + kk - b0] = step;
-              }
+              for (uint32_t kk = k0; kk < k1; ++kk) stp[off + kk - b0] = step;
+              bulk_copy_g2s(dst + (size_t)(off + k0 - b0) * RD, prm.rec + (size_t)(beg + k0) * RD,
+                            (k1 - k0) * (uint32_t)(RD * sizeof(double)), &s_full[stage]);
             }
-            producer_bar(NPT);
-            double* dst = s_rec + (size_t)stage * cap * RD;
-            const int nchunk = B * R::kChunks16;
-            for (int c = pt; c < nchunk; c += NPT) {
-              const int e = c / R::kChunks16, part = c - e * R::kChunks16;
-              cp_async16(dst + 2 * (size_t)c, prm.rec + (size_t)s_idx[e] * RD + 2 * part);
-            }
-            cp_async_wait_all();
+            producer_bar(NPT);   // all copies issued and plane ids written
             if (prm.prof && pt == 0) {
               atomicAdd(prm.prof + 5, p2 - p1);
               atomicAdd(prm.prof + 6, clock64() - p2);
             }
-            if (pt == 0) s_hdr[stage] = BatchHdr{B, t, 0, 0};
-            mbar_arrive(&s_full[stage]);
+            if (pt == 0) {
+              s_hdr[stage] = BatchHdr{B, t, 0, 0};
+              mbar_arrive(&s_full[stage]);
+            }
             next_stage();
-            producer_bar(NPT);   // s_idx is rewritten by the next batch
           }
         }
       }
       // end-of-tile marker (consumers flush every node of the tile unless it is skipped)
       mbar_wait(&s_empty[stage], phase ^ 1u);
-      if (pt == 0) s_hdr[stage] = BatchHdr{0, t, skip ? 2 : 1, 0};
-      mbar_arrive(&s_full[stage]);
+      if (pt == 0) {
+        s_hdr[stage] = BatchHdr{0, t, skip ? 2 : 1, 0};
+        mbar_arrive(&s_full[stage]);
+      }
       next_stage();
     }
     mbar_wait(&s_empty[stage], phase ^ 1u);
-    if (pt == 0) s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
-    mbar_arrive(&s_full[stage]);
+    if (pt == 0) {
+      s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
+      mbar_arrive(&s_full[stage]);
+    }
     return;
   }
 
   // =============================== consumer warps ===============================
 #ifndef HPNFFT_SWEEP_DFMA
-  // FP64 tensor-core consumer (DMMA m8n8k4).  A warp owns a 4 x 8 sub-patch of columns; its
-  // accumulator is the 16 x 64 real matrix C[node row][2 x complex column] held as 2 x 8 DMMA
+  // FP64 tensor-core consumer (DMMA m8n8k4).  A warp owns a 4 x 4 sub-patch of columns; its
+  // accumulator is the 16 x 32 real matrix C[node row][2 x complex column] held as 2 x 4 DMMA
   // C-fragments.  Node rows are cyclic (row = l0-node mod 16), so the 2m-node sliding window needs
   // no data movement: a finished node row is stored and zeroed.  Four records per k-step:
   //   C += A (16 x 4: w0 of each record placed at its plane's cyclic offset)
   //      x B (4 x 64: f w1[i1] w2[i2] of each record for every column, 0 outside its footprint)
-  // i.e. 16 DMMA (4096 FMA) per k-step instead of 4 x 24 DFMA per lane; records of up to
+  // i.e. 8 DMMA (2048 FMA) per k-step instead of 4 x 24 DFMA per lane; records of up to
   // 16 - 2m + 1 consecutive planes share a k-step.
   static_assert(2 * M_ <= 16, "cyclic 16-row window");
   const int wr_off = (warp / (P2 / kWC)) * kWR;
   const int wc_off = (warp % (P2 / kWC)) * kWC;
   const int g = lane >> 2, t = lane & 3;
+  constexpr int NT = kWR * kWC / 4;       // n-tiles of 8 real columns (4 complex)
   const int part = g & 1;                 // B: real (0) or imaginary (1) part of the column
-  const int bc0 = g >> 1;                 // B: column offset inside a half n-tile pair
+  const int bc0 = g >> 1;                 // B: column c of complex column q = 4 nt + g/2 (row nt)
   int cur_tile = -1;
   int first = 0, wr0 = 0, wc0 = 0, nsteps = 0;
-  double cfr[2][8][2];
+  double cfr[2][NT][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
+    for (int b = 0; b < NT; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
   int cur = 0;                            // planes < cur are flushed
   const size_t plane = (size_t)n1 * n2;
 
@@ -450,12 +485,12 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
     const int l0 = (first + sp - M_ + 1) & (n0 - 1);
     double2* base = reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
       double v0, v1;
       if (rho < 8) { v0 = cfr[0][nt][0]; v1 = cfr[0][nt][1]; }
       else { v0 = cfr[1][nt][0]; v1 = cfr[1][nt][1]; }
       const int q = 4 * nt + t;           // complex column of this lane's pair (re, im)
-      const int l1 = wr0 + (q >> 3), l2 = wc0 + (q & 7);
+      const int l1 = wr0 + q / kWC, l2 = wc0 + q % kWC;
       if (mine && write && l1 < n1) {
         double2* dst = base + (size_t)l1 * n2 + l2;
         if (prm.accumulate) {
@@ -501,7 +536,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
+        for (int b = 0; b < NT; ++b) cfr[a][b][0] = cfr[a][b][1] = 0.0;
     }
     const int B = hdr.B;
     const double* recs = s_rec + (size_t)stage * cap * RD;
@@ -528,7 +563,7 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
     __syncwarp();
     const unsigned long long c2 = prm.prof ? clock64() : 0ull;
     // ---- k-steps of up to 4 records spanning at most 16 - 2m + 1 planes ----
-    for (int k = 0; k < nlist;) {
+    for (int k = 0; k < (prm.debug == 2 ? 0 : nlist);) {
       const uint32_t e0 = my[k];
       const int st0 = (int)((e0 >> 9) & 0x1ffu);
       const uint32_t en = (k + t < nlist) ? my[k + t] : 0xffffffffu;
@@ -548,20 +583,19 @@ __global__ void __launch_bounds__(SweepLayout<P1, P2, M_>::kThreads, 1) k_spread
         const int i = (8 * mt + g - (st - M_ + 1)) & 15;
         afr[mt] = (act && i < W) ? r[R::kW0 + i] : 0.0;
       }
-      // B fragments: column q = 4 nt + g/2 (row q/8 = nt/2, col q%8 = 4 (nt&1) + g/2), part g&1
+      // B fragments: complex column q = 4 nt + g/2 = (row nt, col g/2) of the 4 x 4 sub-patch,
+      // part g & 1; value f_part w1[i1(nt)] w2[i2(g/2)]
       const double fp = act ? r[2 + part] : 0.0;
-      double fw1[4];
+      const unsigned i2 = min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W);
+      const double fw2 = fp * r[R::kW2 + i2];
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const unsigned i1 = min((unsigned)(d1 - (kWR - 1) + rr), (unsigned)W);
-        fw1[rr] = fp * r[R::kW1 + i1];
-      }
-      const unsigned ia = min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W);
-      const unsigned ib = min((unsigned)(d2 - (kWC - 1) + 4 + bc0), (unsigned)W);
-      const double w2a = r[R::kW2 + ia], w2b = r[R::kW2 + ib];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const double bfr = fw1[nt >> 1] * ((nt & 1) ? w2b : w2a);
+      for (int nt = 0; nt < NT; ++nt) {
+        const unsigned i1 = min((unsigned)(d1 - (kWR - 1) + nt), (unsigned)W);
+        const double bfr = fw2 * r[R::kW1 + i1];
+        if (prm.debug == 1) {   // measurement only: keep the operands alive, skip the MMAs
+          cfr[0][nt][0] += afr[0] * bfr;
+          continue;
+        }
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -761,11 +795,16 @@ size_t sweep_smem_bytes(int cap) {
 }
 
 // CTA patch variant: 0 = 12 x 32 (12 consumer + 4 producer warps), 1 = 8 x 32 (8 + 4 warps).
+// CTA patch variant: 0 = 12 x 32, 1 = 8 x 32, 2 = 16 x 32 columns (consumer warps = patch / warp
+// sub-patch), each with 4 producer warps; HPNFFT_SWEEP_PATCH = "12x32" | "8x32" | "16x32".
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    v = (e && e[0] == '8') ? 1 : 0;
+    if (e && e[0] == '8') v = 1;
+    else if (e && e[0] == '1' && e[1] == '6') v = 2;
+    else if (e && e[0] == '1' && e[1] == '2') v = 0;
+    else v = 0;
   }
   return v;
 }
@@ -802,6 +841,8 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* rows, bool 
     cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), p->stream);
   }
   prm.prof = prof;
+  static const int dbg = getenv("HPNFFT_SWEEP_DEBUG") ? atoi(getenv("HPNFFT_SWEEP_DEBUG")) : 0;
+  prm.debug = dbg;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
   auto kern = k_spread_sweep<P1, P2, M_>;
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -855,8 +896,17 @@ int run_sweep(Plan* p, const double* f) {
                                             p->group_rows);
       p->launches++;
     }
-    int rc = sweep_variant() == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
-                                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
+    const int var = sweep_variant();
+    int rc;
+#ifdef HPNFFT_SWEEP_DFMA
+    rc = var == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+       : var == 2 ? launch_sweep_group<16, 32, M_>(p, g0, g1, p->group_rows, multi)
+                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
+#else
+    // 4 x 4 warp sub-patches: 12 x 32 = 24 consumer warps, 8 x 32 = 16 (+ 4 producer warps)
+    rc = var == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+                  : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
+#endif
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
