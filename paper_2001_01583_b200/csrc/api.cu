@@ -184,6 +184,9 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (int64_t(1) << (s2 + 1)) <= n[2]) ++s2;
   p->nbins = n[1] * (n[2] >> s2) * n[0];
+  // plane chunk of the sweep: CH planes of cells touch CH + 2m - 1 <= 16 node planes (the DMMA
+  // accumulator's cyclic window), see spread_sweep.cu
+  p->chunk_log = m <= 6 ? 2 : (m == 7 ? 1 : 0);
   int rc = HPNFFT_OK;
   rc = rc ? rc : alloc(p, &p->grid, 2 * (size_t)cells);
   rc = rc ? rc : alloc(p, &p->bufA, 2 * (size_t)(n[0] * n[1] * N[2]));

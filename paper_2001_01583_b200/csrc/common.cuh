@@ -45,7 +45,8 @@ struct Plan {
   double* twiddle[3] = {nullptr, nullptr, nullptr}; // exp(-2 pi i t/n_t), t < n_t (complex)
   double* poly = nullptr;       // window tap polynomials [2m][kPolyDeg+1]
   // bin sort
-  int64_t nbins = 0;            // n1 * (n2/8) * n0 bins, key = (c1 * nb2 + c2/8) * n0 + c0
+  int64_t nbins = 0;            // n1 * (n2/8) * n0 bins (sort.cu: key order plane chunk, c1, c2/8, c0)
+  int chunk_log = 2;            // log2 of the sweep's plane chunk CH (4 planes for m <= 6)
   uint32_t* bin_count = nullptr;  // [nbins + 1], becomes exclusive prefix (bin_start)
   uint32_t* key = nullptr;        // [M]
   uint32_t* rank = nullptr;       // [M] arrival rank inside the bin
@@ -53,9 +54,9 @@ struct Plan {
   double* xs = nullptr;           // [M][3] sorted coordinates
   void* scan_tmp = nullptr;       // block sums for the scan
   int64_t scan_tmp_elems = 0;
-  double* rec = nullptr;          // point records for the sweep spread [rec_group][6 + 6m]
+  double* rec = nullptr;          // point records for the sweep spread [rec_group][22 + 4m]
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
-  int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep
+  int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep (chunk range)
   int* tile_counter = nullptr;    // sweep tile scheduler counter
   int* err_flag = nullptr;        // device [1 + 2 kRangeSlots]: range-error flag, then slot pairs of
                                   // min / max of the x-ordered cell c0

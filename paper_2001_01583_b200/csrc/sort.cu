@@ -2,11 +2,12 @@
 //
 // Not in the paper (its CUNFFT spreads points in input order, one thread per point,
 // PAPER.md:162-164); the B200 design sorts the points once so the spread kernel can sweep
-// the grid with register-resident windows.
+// the grid with register/tensor-core resident windows.
 //   u_t = n_t x_t (exact for power-of-two n_t), c_t = floor(u_t) mod n_t  (integer cell)
-//   bin  = (c1 * nb2 + (c2 >> s2)) * n0 + c0       nb2 = n2 >> s2, s2 = log2(min(8, n2))
-// i.e. "pencils" of (one c1 row, 8 consecutive c2) with the c0 index fastest, so the points a
-// sweep CTA needs for its current c0 plane are contiguous per pencil.
+//   key = (((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc | (c0 & (CH - 1)),
+//   CH = 2^lc planes per chunk, nb2 = n2 >> s2, s2 = log2(min(8, n2))
+// so the points of one plane chunk and one c1 row are contiguous across consecutive c2 bins:
+// a sweep CTA fetches the records of its (chunk, row) with one bulk copy.
 // Counting sort: histogram with arrival ranks (atomicAdd) -> exclusive scan -> scatter.
 // The order inside a bin is the atomic arrival order (not deterministic; Q21).
 #include "common.cuh"
@@ -19,7 +20,7 @@ __global__ void k_range_init(int* err) {
   else err[t] = (t & 1) ? 0x7fffffff : -1;                // slot minima / maxima
 }
 
-__global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2,
+__global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
                        uint32_t* __restrict__ count, uint32_t* __restrict__ key, uint32_t* __restrict__ rank,
                        int* __restrict__ err) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -60,7 +61,7 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
   int64_t c1 = (int64_t)floor(__dmul_rn((double)n1, x1)) & (n1 - 1);
   int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
   int64_t nb2 = n2 >> s2;
-  uint32_t k = (uint32_t)((c1 * nb2 + (c2 >> s2)) * n0 + c0);
+  uint32_t k = (uint32_t)(((((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc) | (c0 & ((1 << lc) - 1)));
   key[j] = k;
   rank[j] = atomicAdd(&count[k], 1u);
 }
@@ -188,7 +189,8 @@ int sort_points(Plan* p, const double* x) {
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   stage_begin(p, 0);
   if (M > 0) {
-    k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->n[0], p->n[1], p->n[2], s2, p->bin_count,
+    k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->n[0], p->n[1], p->n[2], s2, p->chunk_log,
+                                                               p->bin_count,
                                                                p->key, p->rank, p->err_flag);
     p->launches++;
     int rc = check_launch(p, "keys");
