@@ -69,7 +69,7 @@ struct SweepCfg {
   static constexpr int W = 2 * M_;                         // taps per dimension
   static constexpr int NW = (P1 / kWR) * (P2 / kWC);       // consumer warps
   static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
-  static constexpr int kThreads = (NW + 1) * 32;           // + one producer warp
+  static constexpr int kThreads = (NW + 2) * 32;           // + copy warp + list warp
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
   static_assert(kRows <= 32, "one producer lane per candidate row");
 };
@@ -242,7 +242,7 @@ template <int P1, int P2, int M_>
 __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
   using C = SweepCfg<P1, P2, M_>;
   return sizeof(double) * ((size_t)C::NS * cap * Rec<2 * M_>::kDoubles + Rec<2 * M_>::kDoubles) +
-         (sizeof(uint64_t) * 2 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NW * cap + 16;
+         (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NW * (cap + 1) + 16;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -260,20 +260,24 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
   const int cap = prm.cap;
   double* s_rec = reinterpret_cast<double*>(smem_raw);                            // [NS][cap][RD]
   double* s_zero = s_rec + (size_t)NS * cap * RD;                                 // [RD] zeros
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_zero + RD);                    // [NS]
-  uint64_t* s_empty = s_full + NS;                                                // [NS]
-  BatchHdr* s_hdr = reinterpret_cast<BatchHdr*>(s_empty + NS);                    // [NS]
-  uint32_t* s_list = reinterpret_cast<uint32_t*>(s_hdr + NS);                     // [NW][cap]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_zero + RD);                    // [NS] lists ready
+  uint64_t* s_empty = s_full + NS;                                                // [NS] stage free
+  uint64_t* s_landed = s_empty + NS;                                              // [NS] records landed
+  BatchHdr* s_hdr = reinterpret_cast<BatchHdr*>(s_landed + NS);                   // [NS]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_hdr + NS);                      // [NS][NW]
+  uint32_t* s_list = s_cnt + NS * NW;                                             // [NS][NW][cap]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
   const int nchunks0 = n0 / CH;   // plane chunks around the circle
   const int npc = n2 / P2, npr = (n1 + P1 - 1) / P1;
+  (void)C::kRows;
   const int ntiles = npc * npr * prm.nseg;
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&s_full[i], 1);
+      mbar_init(&s_landed[i], 1);
       mbar_init(&s_empty[i], NW);
     }
   }
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
             const unsigned long long p1 = prm.prof ? clock64() : 0ull;
             mbar_wait(&s_empty[stage], phase ^ 1u);
             const unsigned long long p2 = prm.prof ? clock64() : 0ull;
-            if (lane == 0) mbar_expect_tx(&s_full[stage], (uint32_t)B * (uint32_t)(RD * sizeof(double)));
+            if (lane == 0) mbar_expect_tx(&s_landed[stage], (uint32_t)B * (uint32_t)(RD * sizeof(double)));
             __syncwarp();
             double* dst = s_rec + (size_t)stage * cap * RD;
             // the part of each run inside [b0, b1) -> consecutive ring slots, one bulk copy
@@ -383,13 +387,13 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
               const uint32_t k0 = off < b0 ? b0 - off : 0u;
               const uint32_t k1 = min(len, b1 - off);
               bulk_copy_g2s(dst + (size_t)(off + k0 - b0) * RD, prm.rec + (size_t)(beg + k0) * RD,
-                            (k1 - k0) * (uint32_t)(RD * sizeof(double)), &s_full[stage]);
+                            (k1 - k0) * (uint32_t)(RD * sizeof(double)), &s_landed[stage]);
             };
             issue(off0, beg0, len0);
             issue(off1, beg1, len1);
             if (lane == 0) {
               s_hdr[stage] = BatchHdr{B, t, ci, 0};
-              mbar_arrive(&s_full[stage]);
+              mbar_arrive(&s_landed[stage]);
             }
             if (prm.prof && lane == 0) {
               atomicAdd(prm.prof + 5, p2 - p1);
@@ -403,14 +407,75 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
       mbar_wait(&s_empty[stage], phase ^ 1u);
       if (lane == 0) {
         s_hdr[stage] = BatchHdr{0, t, skip ? 0 : nch, skip ? 2 : 1};
-        mbar_arrive(&s_full[stage]);
+        mbar_arrive(&s_landed[stage]);
       }
       next_stage();
     }
     mbar_wait(&s_empty[stage], phase ^ 1u);
     if (lane == 0) {
       s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
-      mbar_arrive(&s_full[stage]);
+      mbar_arrive(&s_landed[stage]);
+    }
+    return;
+  }
+
+  if (warp == NW + 1) {
+    // ============================ list warp ============================
+    // Once a stage's records have landed, sort them into one list per consumer warp: the records
+    // whose 2m x 2m column footprint meets the warp's 4 x 4 sub-patch, entry = record | (c0 mod
+    // CH) << 9 | d1 << 18 | d2 << 23 with d1 = (warp row) - (c1 - m + 1) + 3 < 2m + 3 and
+    // d2 = (warp col) - (c2 - m + 1) + 3 < 2m + 3.  (Each consumer warp scanning the whole batch
+    // itself would keep the FP64 tensor pipe idle while all of them do it at the same time.)
+    constexpr int NWC = P2 / kWC;   // consumer warps per sub-patch row
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&s_landed[stage], phase);
+      const BatchHdr hdr = s_hdr[stage];
+      int cnt[NW];   // list lengths (0 for tile-end markers)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) cnt[w] = 0;
+      if (hdr.B > 0) {
+        int R0, C0, L0, S_, a_lo, nch;
+        tile_geom(hdr.tile, R0, C0, L0, S_, a_lo, nch);
+        const double* recs = s_rec + (size_t)stage * cap * RD;
+        uint32_t* lists = s_list + (size_t)stage * NW * cap;
+        for (int base = 0; base < hdr.B; base += 32) {
+          const int e = base + lane;
+          int dr = -1000, dc = -1000;   // footprint origin relative to the patch origin
+          uint32_t ebase = 0;
+          if (e < hdr.B) {
+            const int4 cc = *reinterpret_cast<const int4*>(recs + (size_t)e * RD);
+            dr = ((cc.x - M_ + 1 - R0 + W) & (n1 - 1)) - W;
+            dc = ((cc.y - M_ + 1 - C0 + W) & (n2 - 1)) - W;
+            ebase = (uint32_t)e | ((uint32_t)(cc.z & (CH - 1)) << 9);
+          }
+#pragma unroll
+          for (int wr = 0; wr < P1 / kWR; ++wr) {
+            const uint32_t d1 = (uint32_t)(kWR * wr - dr + (kWR - 1));
+            const bool relr = d1 < (uint32_t)(W + kWR - 1);
+#pragma unroll
+            for (int wc = 0; wc < NWC; ++wc) {
+              const uint32_t d2 = (uint32_t)(kWC * wc - dc + (kWC - 1));
+              const bool rel = relr && d2 < (uint32_t)(W + kWC - 1);
+              const unsigned bal = __ballot_sync(0xffffffffu, rel);
+              const int w = wr * NWC + wc;
+              if (rel) lists[(size_t)w * cap + cnt[w] + __popc(bal & ((1u << lane) - 1))] = ebase | (d1 << 18) | (d2 << 23);
+              cnt[w] += __popc(bal);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        if (lane == w % 32) s_cnt[stage * NW + w] = (uint32_t)cnt[w];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_full[stage]);
+      if (hdr.B < 0) break;
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1u;
+      }
     }
     return;
   }
@@ -500,26 +565,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
     const int step0 = hdr.chunk * CH;
     advance(step0);                       // earlier chunks are complete
     const double* recs = s_rec + (size_t)stage * cap * RD;
-    // ---- this warp's records: entry = record | (c0 mod CH) << 9 | d1 << 18 | d2 << 23 with
-    //      d1 = wr0 - (c1-m+1) + 3 < 2m + 3, d2 = wc0 - (c2-m+1) + 3 < 2m + 3 ----
-    int nlist = 0;
-    uint32_t* my = s_list + (size_t)warp * cap;
-    for (int base = 0; base < B; base += 32) {
-      const int e = base + lane;
-      bool rel = false;
-      uint32_t entry = 0;
-      if (e < B) {
-        const int4 cc = *reinterpret_cast<const int4*>(recs + (size_t)e * RD);
-        const uint32_t d1 = (uint32_t)((wr0 - (cc.x - M_ + 1) + (kWR - 1)) & (n1 - 1));
-        const uint32_t d2 = (uint32_t)((wc0 - (cc.y - M_ + 1) + (kWC - 1)) & (n2 - 1));
-        rel = (d1 < (uint32_t)(W + kWR - 1)) && (d2 < (uint32_t)(W + kWC - 1));
-        entry = (uint32_t)e | ((uint32_t)(cc.z & (CH - 1)) << 9) | (d1 << 18) | (d2 << 23);
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, rel);
-      if (rel) my[nlist + __popc(bal & ((1u << lane) - 1))] = entry;
-      nlist += __popc(bal);
-    }
-    __syncwarp();
+    // ---- this warp's list (built by the list warp) ----
+    int nlist = (int)s_cnt[stage * NW + warp];
+    const uint32_t* my = s_list + ((size_t)stage * NW + warp) * cap;
     const unsigned long long q2 = prm.prof ? clock64() : 0ull;
 #if HPNFFT_SWEEP_DEBUG == 2
     nlist = 0;   // measurement only: skip apply
@@ -584,13 +632,13 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
 
 namespace {
 
-// CTA patch variant: 0 = 12 x 32 (24 consumer warps), 1 = 8 x 32 (16), 2 = 16 x 16 (16);
-// HPNFFT_SWEEP_PATCH = "12x32" | "8x32" | "16x16".
+// CTA patch variant: 0 = 8 x 32 (16 consumer warps), 1 = 12 x 32 (24), 2 = 16 x 16 (16);
+// HPNFFT_SWEEP_PATCH = "8x32" | "12x32" | "16x16".
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    if (e && e[0] == '8') v = 1;
+    if (e && e[0] == '1' && e[1] == '2') v = 1;
     else if (e && e[0] == '1' && e[1] == '6') v = 2;
     else v = 0;
   }
@@ -693,9 +741,9 @@ int run_sweep(Plan* p, const double* f) {
       p->launches++;
     }
     const int var = sweep_variant();
-    const int rc = var == 1 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+    const int rc = var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                            : launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi);
+                            : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
@@ -710,7 +758,7 @@ bool sweep_supported(const Plan* p) {
   const int W = 2 * p->m;
   const int P1 = 16, P2 = 32;   // largest extent of any patch variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;
-  if (p->n[1] < P1 + W - 1) return false;                     // candidate rows must be distinct
+  if (p->n[1] < P1 + W) return false;                         // candidate rows must be distinct
   const int bins = (P2 + W - 1 + kBinW - 1) / kBinW + 1;      // candidate c2 bins must be distinct
   if (p->n[2] / kBinW < bins) return false;
   if (p->n[0] < 16 || p->n[0] < 2 * W) return false;
