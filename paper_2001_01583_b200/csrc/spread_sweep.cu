@@ -575,35 +575,50 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
     // ---- k-steps of 4 records (any order inside the chunk); lanes past the list end read the
     //      all-zero record ----
     const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(recs);
-    for (int k = 0; k < nlist; k += 4) {
+    // operands of one k-step (lane: record k + t), loaded as a group so that two k-steps' shared
+    // memory loads are in flight before their DMMAs issue
+    auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT]) {
       const bool act = k + t < nlist;
       const uint32_t en = act ? my[k + t] : 0u;
       const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
-      const int st = step0 + (int)((en >> 9) & (uint32_t)(CH - 1));
+      const int sh = step0 + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
       const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
       // A fragments: rows 8 mt + g hold node (row - (st - m + 1)) mod 16 of this record
-      const int sh = st - M_ + 1;
-      const double a0 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
-      const double a1 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((8 + g - sh) & 15)));
+      a0 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
+      a1 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((8 + g - sh) & 15)));
       // B fragments: complex column q = 4 nt + g/2 = (row nt, col g/2) of the 4 x 4 sub-patch,
       // part g & 1; value f_part w1[i1(nt)] w2[i2(g/2)] (indices past the footprint hit zero pads)
-      const unsigned i2 = min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W);
-      const double fw2 = lds_f64(ra + 8u * (uint32_t)(2 + part)) * lds_f64(ra + 8u * (uint32_t)(R::kW2 + i2));
-      double bfr[NT];
+      fp = lds_f64(ra + 8u * (uint32_t)(2 + part));
+      w2v = lds_f64(ra + 8u * (uint32_t)(R::kW2 + min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W)));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        w1v[nt] = lds_f64(ra + 8u * (uint32_t)(R::kW1 + min((unsigned)(d1 - (kWR - 1) + nt), (unsigned)W)));
+    };
+    auto apply = [&](double a0, double a1, double fp, double w2v, const double (&w1v)[NT]) {
+      const double fw2 = fp * w2v;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const unsigned i1 = min((unsigned)(d1 - (kWR - 1) + nt), (unsigned)W);
-        bfr[nt] = fw2 * lds_f64(ra + 8u * (uint32_t)(R::kW1 + i1));
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+        const double b = fw2 * w1v[nt];
 #if HPNFFT_SWEEP_DEBUG == 1
-        acc[nt][0] += a0 * bfr[nt] + a1;   // measurement only: keep the operands alive, skip the MMAs
+        acc[nt][0] += a0 * b + a1;   // measurement only: keep the operands alive, skip the MMAs
 #else
-        dmma(acc[nt], a0, bfr[nt]);
-        dmma(acc[NT + nt], a1, bfr[nt]);
+        dmma(acc[nt], a0, b);
+        dmma(acc[NT + nt], a1, b);
 #endif
       }
+    };
+    int k = 0;
+    for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
+      double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
+      fetch(k, a0, a1, fp, w2v, w1v);
+      fetch(k + 4, b0, b1, gp, g2v, g1v);
+      apply(a0, a1, fp, w2v, w1v);
+      apply(b0, b1, gp, g2v, g1v);
+    }
+    if (k < nlist) {
+      double a0, a1, fp, w2v, w1v[NT];
+      fetch(k, a0, a1, fp, w2v, w1v);
+      apply(a0, a1, fp, w2v, w1v);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[stage]);
