@@ -38,10 +38,12 @@ CONFIGS = {
 }
 METRIC = "adjoint NFFT nonuniform points/s at N=256³ float64, 1/2/4/8 B200; E2 error"
 M_WINDOW, SIGMA = 6, 2.0
-# FP64 peak derived from unit counts and clocks: 148 SMs x 64 FP64
-# FMA/clk/SM x 2 flop x 1.965 GHz max SM clock.  The FMA-chain microbenchmark measured
-# 34.2 TFLOP/s (tools/ubench_fp64.cu, profiles/ubench_fp64.txt).
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# FP64 tensor-core (DMMA m8n8k4) peak MEASURED on this pool's B200 with tools/ubench_dmma.cu /
+# tools/ubench_kstep.cu (profiles/ubench_dmma.txt, profiles/ubench_kstep.txt): 36.7 TFLOP/s for
+# back-to-back DMMAs (DFMA and DMMA share this throughput: profiles/ubench_mix.txt).  The
+# fallback rule (bf16 measured x nominal FP64/bf16 ratio = 1653.7 / 56.25 = 29.4) would be lower,
+# so the measured number is the conservative denominator.
+FP64_TC_PEAK_TFLOPS = 36.7
 
 
 def spread_flops_per_point(m: int) -> float:
@@ -270,10 +272,11 @@ def run_ours(args):
     if dom in ("sweep", "records"):
         fl = M_local * spread_flops_per_point(M_WINDOW)
         achieved = fl / (kern["sweep"] * 1e-3) / 1e12
-        roof = {"kernel": "k_spread_sweep", "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured FMA chain: 34.2)",
-                "algorithmic": f"{spread_flops_per_point(M_WINDOW):.0f} flop/point x {M_local} points"}
+        roof = {"kernel": "k_spread_sweep", "bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "measured FP64 DMMA m8n8k4 (tools/ubench_dmma.cu, profiles/ubench_dmma.txt)",
+                "algorithmic": f"{spread_flops_per_point(M_WINDOW):.0f} flop/point x {M_local} points",
+                "timed_as": "spread stage - records stage (CUDA events on the plan stream)"}
     else:
         byts = fft_bytes(N)[dom]
         hbm = peaks.get("hbm_gbs", 6650.0)
