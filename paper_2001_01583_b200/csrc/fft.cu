@@ -216,24 +216,36 @@ template <int LOGN>
 constexpr int tile_cols() {
   return (1 << LOGN) >= 1024 ? 4 : ((4096 >> LOGN) > 64 ? 64 : (4096 >> LOGN));
 }
+#ifndef HPNFFT_FFT_CONTIG_LINES
+#define HPNFFT_FFT_CONTIG_LINES 2
+#endif
+// contiguous pass: lines per CTA (fewer, smaller CTAs keep more of them resident so that their
+// global-load phases overlap)
+template <int LOGN>
+constexpr int tile_cols_contig() {
+  return tile_cols<LOGN>() < HPNFFT_FFT_CONTIG_LINES ? tile_cols<LOGN>() : HPNFFT_FFT_CONTIG_LINES;
+}
 
 template <int LOGN>
 static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
                          const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
                          int a_lo, int a_len) {
   constexpr int TI = tile_cols<LOGN>();
+  constexpr int TC = tile_cols_contig<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
-  size_t smem = (contig ? tile_elems<LOGN, TI, true>() : tile_elems<LOGN, TI, false>()) * sizeof(cplx);
-  int64_t blocks = contig ? (outer + TI - 1) / TI : outer * ((inner + TI - 1) / TI);
-  if (blocks <= 0) return HPNFFT_OK;
+  if (outer <= 0 || inner <= 0) return HPNFFT_OK;
   if (contig) {
-    auto kern = k_fft_pass<LOGN, TI, true>;
+    const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(cplx);
+    const int64_t blocks = (outer + TC - 1) / TC;
+    auto kern = k_fft_pass<LOGN, TC, true>;
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
-    kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
-                                                     a_len);
+    kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
+                                                                            o_start, o_total, a_lo, a_len);
   } else {
+    const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
+    const int64_t blocks = outer * ((inner + TI - 1) / TI);
     auto kern = k_fft_pass<LOGN, TI, false>;
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");

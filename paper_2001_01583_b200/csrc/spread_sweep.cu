@@ -71,6 +71,7 @@ struct SweepCfg {
   static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
   static constexpr int kThreads = (NW + 2) * 32;           // + copy warp + list warp
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
+  static constexpr int kCtasPerSm = NW <= 8 ? 2 : 1;        // small patches: 2 resident CTAs
   static_assert(kRows <= 32, "one producer lane per candidate row");
 };
 
@@ -222,11 +223,12 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
-// D = A (8x4, row) x B (4x8, col) + D on the FP64 tensor core; c = this lane's D pair
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-      : "+d"(c[0]), "+d"(c[1])
-      : "d"(a), "d"(b));
+// D = A (16x4, row) x B (4x8, col) + D on the FP64 tensor core.  Lane (g = lane/4, t = lane%4):
+// a0 = A[g][t], a1 = A[g+8][t], b = B[t][g], c = {D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]}
+__device__ __forceinline__ void dmma16(double (&c)[4], double a0, double a1, double b) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
 }
 
 struct BatchHdr {
@@ -248,7 +250,8 @@ __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
 // ------------------------------------------------------------------------------------------
 // A4: the warp-specialised persistent sweep (see the file header).
 template <int P1, int P2, int M_>
-__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sweep(SweepParams prm) {
+__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, SweepCfg<P1, P2, M_>::kCtasPerSm)
+    k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
   using R = Rec<2 * M_>;
   constexpr int W = C::W, NW = C::NW, NS = C::NS;
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
 
   // =============================== consumer warps ===============================
   // A warp owns a 4 x 4 sub-patch of columns; its accumulator is the 16 x 32 real matrix
-  // C[node row][2 x complex column] held as 2 x 4 DMMA C-fragments.  Node rows are cyclic
+  // C[node row][2 x complex column] held as 4 DMMA m16n8k4 C-fragments.  Node rows are cyclic
   // (row = relative node mod 16), so the sliding window needs no data movement: a finished node
   // row is stored and zeroed.  Four records per k-step:
   //   C += A (16 x 4: w0 of each record placed at its cell's cyclic offset)
@@ -495,46 +498,50 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
   const int bc0 = g >> 1;                 // B: column c of complex column q = 4 nt + g/2 (row nt)
   int cur_tile = -1;
   int first = 0, off = 0, S = 0, wr0 = 0, wc0 = 0, nsteps = 0;
-  double acc[2 * NT][2];                  // [mt * NT + nt][c-fragment pair]
+  double acc[NT][4];                      // m16n8k4 C-fragment per n-tile: rows g (0, 1), g + 8 (2, 3)
 #pragma unroll
-  for (int a = 0; a < 2 * NT; ++a) acc[a][0] = acc[a][1] = 0.0;
+  for (int a = 0; a < NT; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.0;
   int cur = 0;                            // steps (cells first + s) < cur are flushed
-  const size_t plane = (size_t)n1 * n2;
 
-  // step sp (cell first + sp) done: node first + sp - m + 1 is final; stored if it lies in the
-  // tile's node planes [L0, L0 + S) (node - L0 = sp - m + 1 - off)
-  auto flush_plane = [&](int sp) {
-    const int rho = (sp - M_ + 1) & 15;
-    const bool mine = g == (rho & 7);
-    const int rel = sp - M_ + 1 - off;
-    const bool write = rel >= 0 && rel < S;
-    const int l0 = (first + sp - M_ + 1) & (n0 - 1);
-    double2* base = reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane;
+  // Flush steps [cur, upto): after step sp (cell first + sp) node first + sp - m + 1 is final
+  // (accumulator row (sp - m + 1) mod 16).  In blocks of at most 16 steps, each lane stores its
+  // rows g and g + 8 if they belong to a step of the block: nodes inside the tile's planes
+  // [L0, L0 + S) (node - L0 = sp - m + 1 - off) go to the grid, then the row is zeroed.
+  const size_t plane = (size_t)n1 * n2;
+  auto advance = [&](int upto) {
+#if HPNFFT_SWEEP_DEBUG == 3
+    cur = upto > cur ? upto : cur;   // measurement only: no flush
+    return;
+#endif
+    while (cur < upto) {
+      const int nb = min(16, upto - cur);
+      const int row0 = (cur - M_ + 1) & 15;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const double v0 = rho < 8 ? acc[nt][0] : acc[NT + nt][0];
-      const double v1 = rho < 8 ? acc[nt][1] : acc[NT + nt][1];
-      const int q = 4 * nt + t;           // complex column of this lane's pair (re, im)
-      const int l1 = wr0 + q / kWC, l2 = wc0 + q % kWC;
-      if (mine && write && l1 < n1) {
-        double2* dst = base + (size_t)l1 * n2 + l2;
-        if (prm.accumulate) {
-          double2 o = *dst;
-          o.x += v0;
-          o.y += v1;
-          *dst = o;
-        } else {
-          *dst = make_double2(v0, v1);
+      for (int h = 0; h < 2; ++h) {
+        const int ds = (g + 8 * h - row0) & 15;     // step offset of this lane's row in the block
+        if (ds < nb) {
+          const int sp = cur + ds;
+          const int rel = sp - M_ + 1 - off;
+          const int l0 = (first + sp - M_ + 1) & (n0 - 1);
+          double2* base = reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0 * n2 + (wc0 + t);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {   // complex column (row nt, col t) of the sub-patch
+            if (rel >= 0 && rel < S && wr0 + nt < n1) {
+              double2* dst = base + (size_t)nt * n2;
+              if (prm.accumulate) {
+                double2 o = *dst;
+                o.x += acc[nt][2 * h];
+                o.y += acc[nt][2 * h + 1];
+                *dst = o;
+              } else {
+                *dst = make_double2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+              }
+            }
+            acc[nt][2 * h] = acc[nt][2 * h + 1] = 0.0;
+          }
         }
       }
-      if (mine && rho < 8) acc[nt][0] = acc[nt][1] = 0.0;
-      if (mine && rho >= 8) acc[NT + nt][0] = acc[NT + nt][1] = 0.0;
-    }
-  };
-  auto advance = [&](int upto) {
-    while (cur < upto) {
-      flush_plane(cur);
-      ++cur;
+      cur += nb;
     }
   };
 
@@ -559,11 +566,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
       wc0 = C0 + wc_off;
       cur = 0;
 #pragma unroll
-      for (int a = 0; a < 2 * NT; ++a) acc[a][0] = acc[a][1] = 0.0;
+      for (int a = 0; a < NT; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.0;
     }
-    const int B = hdr.B;
     const int step0 = hdr.chunk * CH;
-    advance(step0);                       // earlier chunks are complete
     const double* recs = s_rec + (size_t)stage * cap * RD;
     // ---- this warp's list (built by the list warp) ----
     int nlist = (int)s_cnt[stage * NW + warp];
@@ -602,12 +607,28 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
 #if HPNFFT_SWEEP_DEBUG == 1
         acc[nt][0] += a0 * b + a1;   // measurement only: keep the operands alive, skip the MMAs
 #else
-        dmma(acc[nt], a0, b);
-        dmma(acc[NT + nt], a1, b);
+        dmma16(acc[nt], a0, a1, b);
 #endif
       }
     };
+    // the first k-step's operand loads are issued before the flush of the earlier chunks, whose
+    // accumulator reads wait for this warp's in-flight DMMAs
+    double p0, p1, pf, p2v, p1v[NT];
+    if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v);
+    advance(step0);                       // earlier chunks are complete
     int k = 0;
+    if (nlist > 0) {
+      if (nlist > 4) {
+        double b0, b1, gp, g2v, g1v[NT];
+        fetch(4, b0, b1, gp, g2v, g1v);
+        apply(p0, p1, pf, p2v, p1v);
+        apply(b0, b1, gp, g2v, g1v);
+        k = 8;
+      } else {
+        apply(p0, p1, pf, p2v, p1v);
+        k = 4;
+      }
+    }
     for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
       double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
       fetch(k, a0, a1, fp, w2v, w1v);
@@ -636,6 +657,14 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, 1) k_spread_sw
       phase ^= 1u;
     }
   }
+#if HPNFFT_SWEEP_DEBUG == 3
+  {  // keep the accumulators alive
+    double z = 0.0;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) z += acc[a][0] + acc[a][1] + acc[a][2] + acc[a][3];
+    if (z == 1234.5678) prm.grid[0] = z;
+  }
+#endif
   if (prm.prof && lane == 0) {
     atomicAdd(prm.prof + 0, tw);
     atomicAdd(prm.prof + 1, tl);
@@ -655,6 +684,7 @@ int sweep_variant() {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
     if (e && e[0] == '1' && e[1] == '2') v = 1;
     else if (e && e[0] == '1' && e[1] == '6') v = 2;
+    else if (e && e[0] == '8' && e[2] == '1') v = 3;
     else v = 0;
   }
   return v;
@@ -664,7 +694,7 @@ template <int P1, int P2, int M_>
 int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, bool accumulate) {
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
-  const size_t smem_max = (size_t)(227 * 1024);
+  const size_t smem_max = C::kCtasPerSm == 1 ? (size_t)(227 * 1024) : (size_t)(113 * 1024);
   int cap = 32;
   while (cap + 32 <= 511 && sweep_smem_bytes_of<P1, P2, M_>(cap + 32) <= smem_max) cap += 32;
   const size_t smem = sweep_smem_bytes_of<P1, P2, M_>(cap);
@@ -706,7 +736,8 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int64_t blocks = tiles < (int64_t)sms ? tiles : (int64_t)sms;
+  const int64_t slots = (int64_t)sms * C::kCtasPerSm;
+  const int64_t blocks = tiles < slots ? tiles : slots;
   kern<<<(unsigned)blocks, C::kThreads, smem, p->stream>>>(prm);
   p->launches++;
   if (prof) {
@@ -756,7 +787,8 @@ int run_sweep(Plan* p, const double* f) {
       p->launches++;
     }
     const int var = sweep_variant();
-    const int rc = var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
+    const int rc = var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
+                 : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
                             : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
