@@ -53,7 +53,7 @@ enum {
   HPNFFT_E_RANGE = -3,              /* a point coordinate outside [-0.5, 0.5] (or NaN) */
   HPNFFT_E_NOMEM = -4,              /* device allocation failed */
   HPNFFT_E_CUDA = -5,               /* CUDA runtime/launch error (plan becomes sticky-failed) */
-  HPNFFT_E_NCCL = -6,               /* reserved for the NCCL layer */
+  HPNFFT_E_NCCL = -6,               /* NCCL missing or an NCCL call failed (multi-GPU plans) */
   HPNFFT_E_STATE = -7,              /* call out of order (adjoint before set_points) or failed plan */
   HPNFFT_E_DEGENERATE_WINDOW = -8   /* a Fourier weight c_k is not finite or below 1e-300 */
 };
@@ -120,7 +120,9 @@ int64_t hpnfft_launch_count(hpnfft_plan_t p);
 /*
  * Per-stage device timing (CUDA events on the plan's stream) of the most recent calls, in ms:
  * out[0] keys+histogram, out[1] scan, out[2] scatter, out[3] spread, out[4] FFT pass z,
- * out[5] FFT pass y, out[6] FFT pass x + deconvolve, out[7] point records (part of out[3]).
+ * out[5] FFT pass y, out[6] FFT pass x + deconvolve, out[7] point records (part of out[3]),
+ * out[8] multi-GPU exchange (the collective, or the halo exchange for HPNFFT_DIST_GRID_SLAB),
+ * out[9] HPNFFT_DIST_GRID_SLAB pack + all-to-all.
  * Enabled by hpnfft_enable_timing(p, 1);
  * reading synchronises the stream.  Returns the number of values written (<= n).
  */
@@ -129,6 +131,53 @@ int hpnfft_stage_times(hpnfft_plan_t p, float* out, int n);
 
 /* Library version string. */
 const char* hpnfft_version(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU (A7 of SURVEY.md §8(a), §8(e)): one process per GPU, NCCL over NVLink/NVSwitch.
+ * By Eq. 8 (§3) fhat is linear in the point set: every rank transforms its own
+ * points (the paper's subcells) and the partial results are combined by one
+ * exchange step ("Accumulate", Alg. 3).  NCCL is loaded at run time
+ * (dlopen "libnccl.so.2", so the process shares torch's copy when torch is loaded); a missing
+ * NCCL makes hpnfft_get_unique_id / hpnfft_plan_dist return HPNFFT_E_NCCL.
+ *
+ * Modes (what hpnfft_adjoint leaves in fhat on rank r of P):
+ *   HPNFFT_DIST_ALLREDUCE    : the full fhat [N0][N1][N2] on every rank (ncclAllReduce).
+ *   HPNFFT_DIST_REDUCE_ROOT0 : the full fhat on rank 0 (ncclReduce, Alg. 3's semantics); the
+ *                              buffer of the other ranks holds their own partial transform.
+ *   HPNFFT_DIST_REDUCE_SCATTER : fhat[r N0/P .. (r+1) N0/P)[N1][N2] (k0 slab r; N0 % P == 0).
+ *   HPNFFT_DIST_GRID_SLAB    : SURVEY.md §8(e) option G.  Rank r owns the x-ordered cell planes
+ *       c0x in [r n0/P, (r+1) n0/P), c0x = (floor(n0 x0) + n0/2) mod n0 (the equal-size x-slab
+ *       [-1/2 + r/P, -1/2 + (r+1)/P)); all its points must lie there (else
+ *       set_points returns HPNFFT_E_RANGE).  The rank spreads into its planes plus the m - 1
+ *       planes below and m above, sends those halos to its neighbours (ncclSend/Recv) and adds
+ *       theirs, runs the z and y FFT passes on its own planes only, exchanges blocks all-to-all
+ *       (grouped ncclSend/Recv) and runs the x pass on its k1 slab: fhat[N0][r N1/P .. (r+1)
+ *       N1/P)[N2] (row-major [N0][N1/P][N2]).  Requires P a power of two, N1 % P == 0 and
+ *       n0 / P >= 2m.
+ */
+enum {
+  HPNFFT_DIST_ALLREDUCE = 0,
+  HPNFFT_DIST_REDUCE_ROOT0 = 1,
+  HPNFFT_DIST_REDUCE_SCATTER = 2,
+  HPNFFT_DIST_GRID_SLAB = 3
+};
+
+/* 128-byte NCCL unique id (HOST buffer), created on one rank and given to all ranks by the
+ * caller (any channel, e.g. torch.distributed broadcast). */
+int hpnfft_get_unique_id(unsigned char id[128]);
+
+/*
+ * Create the plan of rank `rank` of `nranks` (arguments as hpnfft_plan; M = this rank's point
+ * count).  Initialises an NCCL communicator over the caller's current CUDA device from `id`
+ * (HOST, 128 bytes); all ranks must call this collectively.  mode = HPNFFT_DIST_*.
+ * Errors: E_INVALID (bad rank/nranks/mode/id), E_UNSUPPORTED (mode constraints above),
+ * E_NCCL (NCCL missing or its initialisation failed), plus those of hpnfft_plan.
+ */
+int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_local, int m, double sigma,
+                     int window, void* stream, int nranks, int rank, const unsigned char id[128], int mode);
+
+/* Shape (HOST int64[3]) of the fhat block hpnfft_adjoint writes on this rank (see the modes). */
+int hpnfft_output_shape(hpnfft_plan_t p, int64_t shape[3]);
 
 #ifdef __cplusplus
 }

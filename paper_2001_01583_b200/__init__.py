@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("HPNFFT_LIB", os.path.join(_HERE, "libhpnfft.so"))
 
 WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
 SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}
-STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records")
+STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records", "exchange", "alltoall")
+DIST_MODES = {"allreduce": 0, "reduce": 1, "reduce_scatter": 2, "grid_slab": 3}
 
 HPNFFT_OK = 0
 _ERRORS = {
@@ -79,6 +80,13 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_stage_times.restype = ctypes.c_int
     lib.hpnfft_version.argtypes = []
     lib.hpnfft_version.restype = ctypes.c_char_p
+    lib.hpnfft_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.hpnfft_get_unique_id.restype = ctypes.c_int
+    lib.hpnfft_plan_dist.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
+                                     ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
+    lib.hpnfft_plan_dist.restype = ctypes.c_int
+    lib.hpnfft_output_shape.argtypes = [vp, i64p]
+    lib.hpnfft_output_shape.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -98,10 +106,22 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-class Plan:
-    """One adjoint NFFT plan (hpnfft_plan): fixed N, M, m, sigma and window."""
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id for hpnfft_plan_dist (create on one rank, share with all)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().hpnfft_get_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None):
+
+class Plan:
+    """One adjoint NFFT plan (hpnfft_plan): fixed N, M, m, sigma and window.
+
+    dist=(nranks, rank, unique_id, mode) makes it rank `rank` of a multi-GPU plan
+    (hpnfft_plan_dist; mode one of DIST_MODES or its integer); M is then this rank's point count
+    and adjoint() returns this rank's block of fhat (out_shape).
+    """
+
+    def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None, dist=None):
         import torch
 
         lib = load_library()
@@ -117,9 +137,20 @@ class Plan:
         arr = (ctypes.c_int64 * len(self.N))(*self.N)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _check(lib.hpnfft_plan(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window,
-                                   _stream_ptr(stream)))
+            if dist is None:
+                _check(lib.hpnfft_plan(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window,
+                                       _stream_ptr(stream)))
+            else:
+                nranks, rank, uid, mode = dist
+                mode = DIST_MODES[mode] if isinstance(mode, str) else int(mode)
+                if len(uid) != 128:
+                    raise ValueError("unique id must be 128 bytes")
+                _check(lib.hpnfft_plan_dist(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma,
+                                            self.window, _stream_ptr(stream), int(nranks), int(rank), uid, mode))
         self._h = h
+        shp = (ctypes.c_int64 * 3)()
+        _check(lib.hpnfft_output_shape(h, shp))
+        self.out_shape = tuple(int(v) for v in shp)
 
     # -- stream plumbing: every call runs on the caller's current torch stream (or the fixed one)
     def _sync_stream(self):
@@ -143,9 +174,10 @@ class Plan:
             raise TypeError("f must be a CUDA complex128 tensor with M elements")
         f = f.contiguous()
         if out is None:
-            out = torch.empty(self.N, dtype=torch.complex128, device=f.device)
-        elif not (out.is_cuda and out.dtype == torch.complex128 and tuple(out.shape) == self.N and out.is_contiguous()):
-            raise TypeError("out must be a contiguous CUDA complex128 tensor of shape N")
+            out = torch.empty(self.out_shape, dtype=torch.complex128, device=f.device)
+        elif not (out.is_cuda and out.dtype == torch.complex128 and tuple(out.shape) == self.out_shape
+                  and out.is_contiguous()):
+            raise TypeError(f"out must be a contiguous CUDA complex128 tensor of shape {self.out_shape}")
         self._sync_stream()
         _check(load_library().hpnfft_adjoint(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr())))
         return out
@@ -164,7 +196,7 @@ class Plan:
         self.set_points(x)
         fh = self.adjoint(f)
         if out_host is None:
-            out_host = torch.empty(self.N, dtype=torch.complex128, pin_memory=True)
+            out_host = torch.empty(self.out_shape, dtype=torch.complex128, pin_memory=True)
         out_host.copy_(fh, non_blocking=True)
         return out_host
 

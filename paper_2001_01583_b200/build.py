@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         raise RuntimeError("nvcc failed")
     if verbose:
         print(log)
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-ldl"])
     return lib
 
 

@@ -55,6 +55,20 @@ void stage_end(Plan* p, int slot) {
 
 int64_t scan_workspace_elems(int64_t nbins);
 
+// A3 + A4: the sweep when the grid allows it, else the generic atomic kernel (timing slot 3)
+int spread(Plan* p, const double* f) {
+  if (p->spread_method == HPNFFT_SPREAD_SWEEP && !sweep_supported(p)) {
+    set_error("sweep spread kernel not supported for this grid");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  const bool sweep = (p->spread_method == HPNFFT_SPREAD_SWEEP) ||
+                     (p->spread_method == HPNFFT_SPREAD_AUTO && sweep_supported(p));
+  stage_begin(p, 3);
+  const int rc = sweep ? spread_sweep(p, f) : spread_atomic(p, f);
+  stage_end(p, 3);
+  return rc;
+}
+
 static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 static void free_plan(Plan* p) {
@@ -79,6 +93,7 @@ static void free_plan(Plan* p) {
   cudaFree(p->tile_counter);
   cudaFree(p->err_flag);
   if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
+  dist_free(p);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   delete p;
 }
@@ -293,6 +308,15 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
       p->plane_lo = ((lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
       p->plane_len = len;
     }
+    if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
+      // grid-slab plans spread exactly their own cell planes plus the halo the taps reach
+      if (p->M > 0 && hi >= lo && (lo < p->slab_lo || hi >= p->slab_lo + p->slab_len)) {
+        set_error("a point lies outside this rank's grid slab (HPNFFT_DIST_GRID_SLAB)");
+        return HPNFFT_E_RANGE;
+      }
+      p->plane_lo = ((p->slab_lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
+      p->plane_len = p->slab_len + 2 * p->m - 1;
+    }
   }
   p->points_set = true;
   return HPNFFT_OK;
@@ -316,16 +340,8 @@ int hpnfft_adjoint(hpnfft_plan_t h, const double* f, double* fhat) {
     set_error("f or fhat is NULL");
     return HPNFFT_E_INVALID;
   }
-  int rc;
-  stage_begin(p, 3);
-  bool sweep = (p->spread_method == HPNFFT_SPREAD_SWEEP) ||
-               (p->spread_method == HPNFFT_SPREAD_AUTO && sweep_supported(p));
-  if (p->spread_method == HPNFFT_SPREAD_SWEEP && !sweep_supported(p)) {
-    set_error("sweep spread kernel not supported for this grid");
-    return HPNFFT_E_UNSUPPORTED;
-  }
-  rc = sweep ? spread_sweep(p, f) : spread_atomic(p, f);
-  stage_end(p, 3);
+  if (p->dist_mode >= 0) return dist_adjoint(p, f, fhat);
+  int rc = spread(p, f);
   if (rc) return rc;
   return fft_and_deconvolve(p, fhat);
 }

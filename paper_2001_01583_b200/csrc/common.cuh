@@ -15,7 +15,7 @@ namespace hpnfft {
 constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
 constexpr int kMinM = 2;
 constexpr int kPolyDeg = 14;      // window tap polynomial degree
-constexpr int kNumStages = 8;     // timing slots, see hpnfft_stage_times
+constexpr int kNumStages = 10;     // timing slots, see hpnfft_stage_times
 constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction
 
 struct Dims3 {
@@ -69,13 +69,21 @@ struct Plan {
 
   int64_t launches = 0;         // kernel launches since the last set_points
 
+  // ---- multi-GPU (hpnfft_plan_dist; csrc/dist.cu) ----
+  int dist_mode = -1;           // HPNFFT_DIST_* or -1 for a single-GPU plan
+  int nranks = 1, dist_rank = 0;
+  void* comm = nullptr;         // ncclComm_t
+  int64_t slab_lo = 0, slab_len = 0;   // GRID_SLAB: owned x-ordered cell planes c0x in [lo, lo + len)
+  double* halo = nullptr;       // GRID_SLAB: received halo planes [2m - 1][n1][n2] complex
+  double* partial = nullptr;    // REDUCE_SCATTER: this rank's full partial fhat
+
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pool, kNumStages+1 events per call
   int ev_used = 0;
   std::vector<int> ev_slot;     // stage id of each recorded begin/end pair
   std::vector<int> ev_pair;     // pool index of the pair's begin event
-  int ev_open[kNumStages] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  int ev_open[kNumStages] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   double stage_ms_acc[kNumStages] = {0};
   int stage_calls[kNumStages] = {0};
 };
@@ -98,6 +106,13 @@ int spread_sweep(Plan* p, const double* f);
 bool sweep_supported(const Plan* p);
 size_t record_bytes(int m);
 int fft_and_deconvolve(Plan* p, double* fhat);
+// one batched pruned FFT pass along dimension dim (fft.cu, see k_fft_pass)
+int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
+             int64_t o_start, int64_t o_total, int a_lo, int a_len);
+// multi-GPU exchange steps (dist.cu)
+int dist_adjoint(Plan* p, const double* f, double* fhat);
+void dist_free(Plan* p);
+int spread(Plan* p, const double* f);
 
 }  // namespace hpnfft
 

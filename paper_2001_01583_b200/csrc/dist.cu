@@ -1,0 +1,375 @@
+// dist.cu -- A7 of SURVEY.md §8(a) / §8(e): the multi-GPU exchange steps, NCCL over NVLink.
+//
+// By Eq. 8 (§3) fhat is linear in the point set, so every rank transforms its
+// own points (the paper's equal-size subcells) and the partial results are summed
+// ("Accumulate", Alg. 3; the paper's binomial tree of MPI Send/Recv becomes
+// one NCCL collective).  Modes (include/hpnfft.h):
+//   ALLREDUCE / REDUCE_ROOT0 / REDUCE_SCATTER : SURVEY.md §8(e) option A, sum of the partial fhat;
+//   GRID_SLAB : option G, sum of the overlapping grid halos + a distributed pruned FFT:
+//       spread (own cell planes + halo) -> halo send/recv + add -> FFT z, y on own planes ->
+//       pack -> all-to-all -> FFT x (+ deconvolve) on this rank's k1 slab.
+// NCCL is resolved at run time with dlopen("libnccl.so.2"): inside a torch process this is the
+// copy torch already loaded; the library has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <string.h>
+
+#include <string>
+
+#include "common.cuh"
+
+namespace hpnfft {
+
+namespace {
+
+// ---- the subset of the NCCL C API used here (stable ABI since NCCL 2.7) ----
+struct NcclUid {
+  char internal[128];
+};
+typedef void* NcclComm;
+typedef int NcclResult;                 // ncclSuccess = 0
+constexpr int kNcclFloat64 = 8;         // ncclFloat64
+constexpr int kNcclSum = 0;             // ncclSum
+
+struct NcclApi {
+  NcclResult (*GetUniqueId)(NcclUid*);
+  NcclResult (*CommInitRank)(NcclComm*, int, NcclUid, int);
+  NcclResult (*CommDestroy)(NcclComm);
+  NcclResult (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t);
+  NcclResult (*Reduce)(const void*, void*, size_t, int, int, int, NcclComm, cudaStream_t);
+  NcclResult (*ReduceScatter)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t);
+  NcclResult (*Send)(const void*, size_t, int, int, NcclComm, cudaStream_t);
+  NcclResult (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t);
+  NcclResult (*GroupStart)();
+  NcclResult (*GroupEnd)();
+  const char* (*GetErrorString)(NcclResult);
+  bool ok;
+};
+
+const NcclApi* nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    memset(&a, 0, sizeof(a));
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    bool ok = true;
+    auto get = [&](const char* name) {
+      void* f = dlsym(h, name);
+      ok = ok && f != nullptr;
+      return f;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(get("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(get("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(get("ncclCommDestroy"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(get("ncclAllReduce"));
+    a.Reduce = reinterpret_cast<decltype(a.Reduce)>(get("ncclReduce"));
+    a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(get("ncclReduceScatter"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(get("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(get("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(get("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(get("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(get("ncclGetErrorString"));
+    a.ok = ok;
+    return a;
+  }();
+  return &api;
+}
+
+int nccl_fail(Plan* p, NcclResult r, const char* what) {
+  const NcclApi* a = nccl();
+  const char* txt = (a->ok && a->GetErrorString) ? a->GetErrorString(r) : "?";
+  return fail(p, HPNFFT_E_NCCL, std::string(what) + ": " + txt);
+}
+
+#define HPNFFT_NCCL_TRY(p, expr, what)         \
+  do {                                         \
+    NcclResult r_ = (expr);                    \
+    if (r_ != 0) return nccl_fail((p), r_, (what)); \
+  } while (0)
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// memory plane of the x-ordered cell plane c0x (c0x = (c0 + n0/2) mod n0)
+inline int64_t mem_plane(int64_t c0x, int64_t n0) { return ((c0x + n0 / 2) % n0 + n0) % n0; }
+
+struct PlaneMap {
+  int count;
+  int plane[16];   // destination memory plane of received halo plane j
+};
+
+// grid[plane[j]] += halo[j], all planes of one halo exchange in one launch (blockIdx.y = j)
+__global__ void k_halo_add(double2* __restrict__ grid, const double2* __restrict__ halo, int64_t plane_elems,
+                           PlaneMap map) {
+  const int j = blockIdx.y;
+  if (j >= map.count) return;
+  double2* dst = grid + (size_t)map.plane[j] * plane_elems;
+  const double2* src = halo + (size_t)j * plane_elems;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < plane_elems; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = dst[e];
+    const double2 b = src[e];
+    a.x += b.x;
+    a.y += b.y;
+    dst[e] = a;
+  }
+}
+
+// send[s][p][k1l][k2] = B[(l0 + p) mod n0][s * N1P + k1l][k2]: destination-major blocks of the
+// y-pass output, so that every block of the all-to-all is contiguous
+__global__ void k_pack(const double2* __restrict__ B, double2* __restrict__ send, int64_t l0, int64_t n0, int64_t L,
+                       int64_t N1, int64_t N1P, int64_t N2, int P) {
+  const int64_t per_dest = L * N1P * N2;
+  const int64_t total = per_dest * P;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / per_dest;
+    int64_t r = e - s * per_dest;
+    const int64_t pl = r / (N1P * N2);
+    r -= pl * (N1P * N2);
+    const int64_t k1l = r / N2, k2 = r - k1l * N2;
+    const int64_t plane = (l0 + pl) % n0;
+    send[e] = B[(plane * N1 + s * N1P + k1l) * N2 + k2];
+  }
+}
+
+// GRID_SLAB step 1: every rank adds the halo planes its neighbours' points reached
+int halo_exchange(Plan* p) {
+  const NcclApi* a = nccl();
+  const int P = p->nranks, r = p->dist_rank, m = p->m;
+  const int64_t n0 = p->n[0], pe = p->n[1] * p->n[2];   // complex elements per plane
+  const int lower = (r - 1 + P) % P, upper = (r + 1) % P;
+  const int64_t lo = p->slab_lo, L = p->slab_len;
+  double2* grid = reinterpret_cast<double2*>(p->grid);
+  double2* halo = reinterpret_cast<double2*>(p->halo);
+  NcclComm comm = p->comm;
+  HPNFFT_NCCL_TRY(p, a->GroupStart(), "ncclGroupStart");
+  // my lower halo (m - 1 planes below my slab) -> rank r-1; my upper halo (m planes) -> rank r+1
+  for (int j = 0; j < m - 1; ++j)
+    HPNFFT_NCCL_TRY(p, a->Send(grid + mem_plane(lo - (m - 1) + j, n0) * pe, 2 * pe, kNcclFloat64, lower, comm, p->stream),
+                    "ncclSend halo");
+  for (int j = 0; j < m; ++j)
+    HPNFFT_NCCL_TRY(p, a->Send(grid + mem_plane(lo + L + j, n0) * pe, 2 * pe, kNcclFloat64, upper, comm, p->stream),
+                    "ncclSend halo");
+  // rank r+1's lower halo = my top m - 1 planes; rank r-1's upper halo = my bottom m planes
+  for (int j = 0; j < m - 1; ++j)
+    HPNFFT_NCCL_TRY(p, a->Recv(halo + (int64_t)j * pe, 2 * pe, kNcclFloat64, upper, comm, p->stream), "ncclRecv halo");
+  for (int j = 0; j < m; ++j)
+    HPNFFT_NCCL_TRY(p, a->Recv(halo + (int64_t)(m - 1 + j) * pe, 2 * pe, kNcclFloat64, lower, comm, p->stream),
+                    "ncclRecv halo");
+  HPNFFT_NCCL_TRY(p, a->GroupEnd(), "ncclGroupEnd");
+  PlaneMap map;
+  map.count = 2 * m - 1;
+  for (int j = 0; j < m - 1; ++j) map.plane[j] = (int)mem_plane(lo + L - (m - 1) + j, n0);
+  for (int j = 0; j < m; ++j) map.plane[m - 1 + j] = (int)mem_plane(lo + j, n0);
+  dim3 g((unsigned)((pe + 255) / 256 < 512 ? (pe + 255) / 256 : 512), (unsigned)map.count);
+  k_halo_add<<<g, 256, 0, p->stream>>>(grid, halo, pe, map);
+  p->launches++;
+  return check_launch(p, "halo add");
+}
+
+// GRID_SLAB steps 2-4: FFT z and y on the own planes, all-to-all, FFT x on the own k1 slab
+int slab_fft(Plan* p, double* fhat) {
+  const NcclApi* a = nccl();
+  const int P = p->nranks, r = p->dist_rank;
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  const int64_t N1 = p->N[1], N2 = p->N[2], N1P = N1 / P;
+  const int64_t L = p->slab_len, l0 = mem_plane(p->slab_lo, n0);
+  int rc;
+  stage_begin(p, 4);
+  rc = fft_pass(p, 2, p->grid, p->bufA, L * n1, 1, true, l0 * n1, n0 * n1, 0, (int)n2);
+  stage_end(p, 4);
+  if (rc) return rc;
+  stage_begin(p, 5);
+  rc = fft_pass(p, 1, p->bufA, p->bufB, L, N2, false, l0, n0, 0, (int)n1);
+  stage_end(p, 5);
+  if (rc) return rc;
+  stage_begin(p, 9);
+  const int64_t blk = L * N1P * N2;   // complex elements per (source, destination) block
+  double2* send = reinterpret_cast<double2*>(p->bufA);
+  double2* recv = reinterpret_cast<double2*>(p->grid);   // [n0][N1P][N2] in memory-plane order
+  {
+    const int64_t total = blk * P;
+    const int64_t blocks = (total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096;
+    k_pack<<<(unsigned)blocks, 256, 0, p->stream>>>(reinterpret_cast<const double2*>(p->bufB), send, l0, n0, L, N1,
+                                                     N1P, N2, P);
+    p->launches++;
+    rc = check_launch(p, "pack");
+    if (rc) return rc;
+  }
+  HPNFFT_NCCL_TRY(p, a->GroupStart(), "ncclGroupStart");
+  for (int s = 0; s < P; ++s) {
+    if (s == r) continue;
+    const int64_t dst_plane = mem_plane((int64_t)s * L, n0);   // first memory plane of rank s's slab
+    HPNFFT_NCCL_TRY(p, a->Send(send + s * blk, 2 * blk, kNcclFloat64, s, p->comm, p->stream), "ncclSend a2a");
+    HPNFFT_NCCL_TRY(p, a->Recv(recv + dst_plane * N1P * N2, 2 * blk, kNcclFloat64, s, p->comm, p->stream),
+                    "ncclRecv a2a");
+  }
+  HPNFFT_NCCL_TRY(p, a->GroupEnd(), "ncclGroupEnd");
+  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(recv + l0 * N1P * N2, send + r * blk, sizeof(double2) * blk,
+                                     cudaMemcpyDeviceToDevice, p->stream),
+                  "a2a self block");
+  stage_end(p, 9);
+  stage_begin(p, 6);
+  rc = fft_pass(p, 0, p->grid, fhat, 1, N1P * N2, false, 0, 1, 0, (int)n0);
+  stage_end(p, 6);
+  return rc;
+}
+
+}  // namespace
+
+int dist_adjoint(Plan* p, const double* f, double* fhat) {
+  const NcclApi* a = nccl();
+  const int64_t nk = p->N[0] * p->N[1] * p->N[2];
+  int rc;
+  if (p->nranks == 1) {   // nothing to exchange
+    rc = spread(p, f);
+    return rc ? rc : fft_and_deconvolve(p, fhat);
+  }
+  switch (p->dist_mode) {
+    case HPNFFT_DIST_ALLREDUCE:
+    case HPNFFT_DIST_REDUCE_ROOT0:
+      rc = spread(p, f);
+      if (!rc) rc = fft_and_deconvolve(p, fhat);
+      if (rc) return rc;
+      stage_begin(p, 8);
+      if (p->dist_mode == HPNFFT_DIST_ALLREDUCE)
+        HPNFFT_NCCL_TRY(p, a->AllReduce(fhat, fhat, 2 * nk, kNcclFloat64, kNcclSum, p->comm, p->stream), "ncclAllReduce");
+      else
+        HPNFFT_NCCL_TRY(p, a->Reduce(fhat, fhat, 2 * nk, kNcclFloat64, kNcclSum, 0, p->comm, p->stream), "ncclReduce");
+      stage_end(p, 8);
+      return HPNFFT_OK;
+    case HPNFFT_DIST_REDUCE_SCATTER:
+      rc = spread(p, f);
+      if (!rc) rc = fft_and_deconvolve(p, p->partial);
+      if (rc) return rc;
+      stage_begin(p, 8);
+      HPNFFT_NCCL_TRY(p, a->ReduceScatter(p->partial, fhat, 2 * nk / p->nranks, kNcclFloat64, kNcclSum, p->comm, p->stream),
+                      "ncclReduceScatter");
+      stage_end(p, 8);
+      return HPNFFT_OK;
+    case HPNFFT_DIST_GRID_SLAB:
+      rc = spread(p, f);
+      if (rc) return rc;
+      stage_begin(p, 8);
+      rc = halo_exchange(p);
+      stage_end(p, 8);
+      if (rc) return rc;
+      return slab_fft(p, fhat);
+    default:
+      set_error("unknown distribution mode");
+      return HPNFFT_E_INVALID;
+  }
+}
+
+void dist_free(Plan* p) {
+  if (p->comm && nccl()->ok) nccl()->CommDestroy(p->comm);
+  p->comm = nullptr;
+  cudaFree(p->halo);
+  cudaFree(p->partial);
+  p->halo = p->partial = nullptr;
+}
+
+}  // namespace hpnfft
+
+using namespace hpnfft;
+
+extern "C" {
+
+int hpnfft_get_unique_id(unsigned char id[128]) {
+  if (!id) {
+    set_error("id is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  const NcclApi* a = nccl();
+  if (!a->ok) {
+    set_error("NCCL (libnccl.so.2) could not be loaded");
+    return HPNFFT_E_NCCL;
+  }
+  NcclUid u;
+  const NcclResult r = a->GetUniqueId(&u);
+  if (r != 0) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  memcpy(id, u.internal, 128);
+  return HPNFFT_OK;
+}
+
+int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_local, int m, double sigma, int window,
+                     void* stream, int nranks, int rank, const unsigned char id[128], int mode) {
+  if (!out) {
+    set_error("hpnfft_plan_dist: out is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id) {
+    set_error("hpnfft_plan_dist: need 0 <= rank < nranks and a unique id");
+    return HPNFFT_E_INVALID;
+  }
+  if (mode < HPNFFT_DIST_ALLREDUCE || mode > HPNFFT_DIST_GRID_SLAB) {
+    set_error("hpnfft_plan_dist: unknown mode");
+    return HPNFFT_E_INVALID;
+  }
+  hpnfft_plan_t h = nullptr;
+  int rc = hpnfft_plan(&h, d, N, M_local, m, sigma, window, stream);
+  if (rc) return rc;
+  Plan* p = reinterpret_cast<Plan*>(h);
+  const int64_t n0 = p->n[0];
+  if (mode == HPNFFT_DIST_REDUCE_SCATTER && p->N[0] % nranks) {
+    hpnfft_destroy(h);
+    set_error("HPNFFT_DIST_REDUCE_SCATTER needs N0 % nranks == 0");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1 &&
+      (!is_pow2(nranks) || p->N[1] % nranks || n0 / nranks < 2 * m || n0 % nranks)) {
+    hpnfft_destroy(h);
+    set_error("HPNFFT_DIST_GRID_SLAB needs nranks a power of two, N1 % nranks == 0 and n0 / nranks >= 2m");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  const NcclApi* a = nccl();
+  if (!a->ok) {
+    hpnfft_destroy(h);
+    set_error("NCCL (libnccl.so.2) could not be loaded");
+    return HPNFFT_E_NCCL;
+  }
+  p->dist_mode = mode;
+  p->nranks = nranks;
+  p->dist_rank = rank;
+  p->slab_len = n0 / nranks;
+  p->slab_lo = (int64_t)rank * p->slab_len;
+  if (nranks > 1) {
+    NcclUid u;
+    memcpy(u.internal, id, 128);
+    NcclComm comm = nullptr;
+    const NcclResult r = a->CommInitRank(&comm, nranks, u, rank);
+    if (r != 0) {
+      rc = nccl_fail(nullptr, r, "ncclCommInitRank");
+      hpnfft_destroy(h);
+      return rc;
+    }
+    p->comm = comm;
+  }
+  cudaError_t e = cudaSuccess;
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1)
+    e = cudaMalloc(&p->halo, sizeof(double) * 2 * (size_t)(2 * m - 1) * (size_t)(p->n[1] * p->n[2]));
+  if (mode == HPNFFT_DIST_REDUCE_SCATTER && nranks > 1)
+    e = cudaMalloc(&p->partial, sizeof(double) * 2 * (size_t)(p->N[0] * p->N[1] * p->N[2]));
+  if (e != cudaSuccess) {
+    hpnfft_destroy(h);
+    set_error("device allocation of the exchange buffers failed");
+    return HPNFFT_E_NOMEM;
+  }
+  *out = h;
+  return HPNFFT_OK;
+}
+
+int hpnfft_output_shape(hpnfft_plan_t h, int64_t shape[3]) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p || !shape) {
+    set_error("NULL argument");
+    return HPNFFT_E_INVALID;
+  }
+  shape[0] = p->N[0];
+  shape[1] = p->N[1];
+  shape[2] = p->N[2];
+  if (p->dist_mode == HPNFFT_DIST_REDUCE_SCATTER) shape[0] = p->N[0] / p->nranks;
+  if (p->dist_mode == HPNFFT_DIST_GRID_SLAB) shape[1] = p->N[1] / p->nranks;
+  return HPNFFT_OK;
+}
+
+}  // extern "C"

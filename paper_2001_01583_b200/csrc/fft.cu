@@ -278,6 +278,12 @@ static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t
   }
 }
 
+int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
+             int64_t o_start, int64_t o_total, int a_lo, int a_len) {
+  return launch_pass(p, p->logn[dim], in, out, outer, inner, (int)p->N[dim], p->inv_c[dim], p->twiddle[dim], contig,
+                     o_start, o_total, a_lo, a_len);
+}
+
 int fft_and_deconvolve(Plan* p, double* fhat) {
   const int64_t n0 = p->n[0], n1 = p->n[1];
   const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];

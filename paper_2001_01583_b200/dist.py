@@ -6,19 +6,22 @@ PAPER.md:174-200, a binomial tree of MPI Send/Recv).  Here every rank is one GPU
 
 * the subcells are x-slabs (dimension 0): equal-size as the paper states (PAPER.md:93,
   "subcells with same size") or equal-count (quantiles, for clustered inputs);
-* each rank runs the single-GPU path (``Plan``) on its slab;
-* the partial fhat are summed with one collective over torch.distributed (NCCL over
-  NVLink/NVSwitch on GPUs): ``allreduce`` (every rank gets fhat), ``reduce`` (rank 0 gets
-  fhat, Alg. 3's semantics) or ``reduce_scatter`` (fhat left distributed over k0 slabs).
+* each rank runs the library's multi-GPU plan (``hpnfft_plan_dist``): the exchange runs inside
+  libhpnfft.so with NCCL over NVLink/NVSwitch — ``allreduce`` (every rank gets fhat),
+  ``reduce`` (rank 0 gets fhat, Alg. 3's semantics), ``reduce_scatter`` (k0 slabs) or
+  ``grid_slab`` (SURVEY.md §8(e) option G: grid halo exchange + distributed FFT, k1 slabs;
+  the points must be partitioned by ``grid_slab_mask``).  torch.distributed only carries the
+  128-byte NCCL unique id from rank 0 to the others.
 
-The collective and the partition are host logic that is exercised on CPU with the gloo
-backend in tests/test_dist_gloo.py; the local transform is injectable for those tests.
+The partition and the result layout are host logic exercised on CPU with the gloo backend in
+tests/test_dist_gloo.py, where the local transform is injected (``local_fn``) and the exchange
+is emulated with torch.distributed collectives.
 """
 from __future__ import annotations
 
 from typing import Callable, Optional
 
-MODES = ("allreduce", "reduce", "reduce_scatter")
+MODES = ("allreduce", "reduce", "reduce_scatter", "grid_slab")
 
 
 def slab_bounds(rank: int, world: int):
@@ -52,6 +55,21 @@ def slab_mask(x, rank: int, world: int, edges=None):
     return m
 
 
+def grid_slab_rank(x, world: int, n0: int):
+    """Owner rank of each point for ``grid_slab`` plans: its x-ordered cell plane
+    c0x = (floor(n0 x0) + n0/2) mod n0 lies in [r n0/P, (r+1) n0/P) (the equal-size x-slab
+    [-1/2 + r/P, -1/2 + (r+1)/P), decided with the library's exact cell rule)."""
+    import torch
+
+    c0 = torch.floor(x[:, 0] * float(n0)).to(torch.int64) % n0
+    c0x = (c0 + n0 // 2) % n0
+    return torch.div(c0x, n0 // world, rounding_mode="floor")
+
+
+def grid_slab_mask(x, rank: int, world: int, n0: int):
+    return grid_slab_rank(x, world, n0) == rank
+
+
 def equal_count_edges(x, world: int):
     """Slab edges at the x0 quantiles so every rank owns ~M/world points (load balance)."""
     import torch
@@ -69,7 +87,7 @@ class DistPlan:
     """Distributed adjoint NFFT: local Plan on this rank's points + one collective on fhat.
 
     group   : torch.distributed process group (None = WORLD)
-    mode    : "allreduce" | "reduce" | "reduce_scatter"
+    mode    : "allreduce" | "reduce" | "reduce_scatter" | "grid_slab"
     local_fn: optional callable (x_local, f_local) -> partial fhat tensor; defaults to the GPU
               Plan (the only product path).  Tests inject the CPU oracle here to check the
               partition/collective logic with the gloo backend.
@@ -88,12 +106,18 @@ class DistPlan:
         self.rank = dist.get_rank(group)
         self.local_fn = local_fn
         self.plan = None
-        if local_fn is None:
-            from . import Plan
-
-            self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device)
         if mode == "reduce_scatter" and self.N[0] % self.world:
             raise ValueError("reduce_scatter needs N0 divisible by the world size")
+        if mode == "grid_slab" and self.N[1] % self.world:
+            raise ValueError("grid_slab needs N1 divisible by the world size")
+        if local_fn is None:
+            from . import Plan, get_unique_id
+
+            uid = [get_unique_id() if self.rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(uid, src=src, group=group)
+            self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device,
+                             dist=(self.world, self.rank, uid[0], mode))
 
     def set_points(self, x):
         self._x = x
@@ -101,16 +125,20 @@ class DistPlan:
             self.plan.set_points(x)
 
     def partial(self, f):
-        """This rank's partial fhat_rank(k) (Eq. 8 term), before the collective."""
-        if self.plan is not None:
-            return self.plan.adjoint(f)
+        """This rank's partial fhat_rank(k) (Eq. 8 term) from the injected local transform."""
         return self.local_fn(self._x, f)
 
     def adjoint(self, f):
-        """fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate of Alg. 3)."""
+        """fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate of Alg. 3).
+
+        Library plans run the whole exchange in libhpnfft.so (NCCL); with ``local_fn`` the
+        exchange is emulated with torch.distributed collectives (CPU tests)."""
         import torch
         import torch.distributed as dist
 
+        if self.plan is not None:
+            out = self.plan.adjoint(f)
+            return None if (self.mode == "reduce" and self.rank != 0) else out
         fh = self.partial(f)
         if self.world == 1:
             return fh
@@ -120,6 +148,10 @@ class DistPlan:
         if self.mode == "reduce":
             dist.reduce(fh, dst=0, op=dist.ReduceOp.SUM, group=self.group)
             return fh if self.rank == 0 else None
+        if self.mode == "grid_slab":   # rank r receives fhat[:, k1 slab r, :]
+            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
+            cols = self.N[1] // self.world
+            return fh[:, self.rank * cols:(self.rank + 1) * cols].contiguous()
         # reduce_scatter: rank r receives fhat[k0 slab r] (N0 / world planes)
         rows = self.N[0] // self.world
         if dist.get_backend(self.group) == "gloo":   # gloo has no reduce_scatter: reduce + slice

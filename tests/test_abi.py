@@ -89,3 +89,16 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), fn
                 assert "liboracle" not in txt, fn
+
+
+def test_dist_plan_validation_is_host_side(lib):
+    """hpnfft_plan_dist rejects bad rank/nranks/mode/id before touching CUDA or NCCL."""
+    h = ctypes.c_void_p()
+    arr = (ctypes.c_int64 * 3)(16, 16, 16)
+    uid = b"\0" * 128
+    assert lib.hpnfft_plan_dist(ctypes.byref(h), 3, arr, 10, 6, 2.0, 0, None, 0, 0, uid, 0) == -1
+    assert lib.hpnfft_plan_dist(ctypes.byref(h), 3, arr, 10, 6, 2.0, 0, None, 2, 2, uid, 0) == -1
+    assert lib.hpnfft_plan_dist(ctypes.byref(h), 3, arr, 10, 6, 2.0, 0, None, 2, 0, uid, 9) == -1
+    assert lib.hpnfft_plan_dist(ctypes.byref(h), 3, arr, 10, 6, 2.0, 0, None, 2, 0, None, 0) == -1
+    assert h.value is None
+    assert lib.hpnfft_output_shape(None, None) == -1

@@ -32,12 +32,15 @@ def _worker(rank, world, port, mode, equal_count, outq):
     try:
         import inputs
         import oracle
-        from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, slab_mask
+        from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, grid_slab_mask, slab_mask
 
         x = torch.from_numpy(inputs.clustered_points(M, s=0.08) if equal_count else inputs.uniform_points(M))
         f = torch.from_numpy(inputs.uniform_values(M))
         edges = equal_count_edges(x, world) if equal_count else None
-        mask = slab_mask(x, rank, world, edges)
+        if mode == "grid_slab":
+            mask = grid_slab_mask(x, rank, world, 2 * N[0])
+        else:
+            mask = slab_mask(x, rank, world, edges)
         xl, fl = x[mask], f[mask]
 
         def local(xx, ff):
@@ -76,7 +79,7 @@ def reference():
     return oracle.nfft_adjoint(x, f, N)
 
 
-@pytest.mark.parametrize("mode", ["allreduce", "reduce", "reduce_scatter"])
+@pytest.mark.parametrize("mode", ["allreduce", "reduce", "reduce_scatter", "grid_slab"])
 def test_dist_modes_sum_partials(mode, reference):
     import oracle
 
@@ -88,6 +91,9 @@ def test_dist_modes_sum_partials(mode, reference):
     elif mode == "reduce":
         assert oracle.rel_l2_error(res[0][1], reference) < 1e-14
         assert res[1][1] is None
+    elif mode == "grid_slab":   # rank r holds fhat[:, k1 slab r, :]
+        full = np.concatenate([r[1] for r in res], axis=1)
+        assert oracle.rel_l2_error(full, reference) < 1e-14
     else:
         full = np.concatenate([r[1] for r in res], axis=0)
         assert oracle.rel_l2_error(full, reference) < 1e-14
@@ -111,3 +117,15 @@ def test_slab_mask_is_partition():
     for world in (1, 2, 3, 4, 8):
         owners = torch.stack([slab_mask(x, r, world) for r in range(world)]).sum(0)
         assert torch.all(owners == 1)
+
+
+def test_grid_slab_rank_follows_the_cell_planes():
+    """grid_slab owners: x-ordered cell plane c0x = (floor(n0 x0) + n0/2) mod n0 in the rank's
+    n0/P planes, i.e. the equal-size slab [-1/2 + r/P, -1/2 + (r+1)/P); x0 = 1/2
+    is x0 = -1/2 by periodicity and belongs to rank 0."""
+    from paper_2001_01583_b200.dist import grid_slab_rank
+
+    n0, world = 32, 4
+    x0 = torch.tensor([-0.5, -0.25 - 1e-12, -0.25, 0.0, 0.2499999, 0.25, 0.49, 0.5], dtype=torch.float64)
+    x = torch.stack([x0, torch.zeros_like(x0), torch.zeros_like(x0)], 1)
+    assert grid_slab_rank(x, world, n0).tolist() == [0, 0, 1, 2, 2, 3, 3, 0]

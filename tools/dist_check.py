@@ -1,7 +1,8 @@
 """Multi-GPU parity check (run under torchrun, one process per GPU, NCCL).
 
-Every rank builds the same seeded point set, keeps its x-slab (equal-size or equal-count),
-runs the GPU plan on it and the partial fhat are summed by DistPlan (NCCL collective).  Rank 0
+Every rank builds the same seeded point set, keeps its x-slab (equal-size, equal-count, or the
+cell-aligned grid slab), runs the library's multi-GPU plan (hpnfft_plan_dist: NCCL inside
+libhpnfft.so) and the distributed result is gathered on rank 0, which
 compares with a single-GPU transform of all points (<= 1e-13) and with sampled direct NDFT
 values from the oracle (<= 1e-9).  Exit code 0 on success.
 """
@@ -17,7 +18,7 @@ import torch.distributed as dist  # noqa: E402
 import inputs  # noqa: E402
 import inputs.device as idev  # noqa: E402
 import paper_2001_01583_b200 as hp  # noqa: E402
-from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, slab_mask  # noqa: E402
+from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, grid_slab_mask, slab_mask  # noqa: E402
 
 
 def main():
@@ -26,22 +27,27 @@ def main():
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     rank, world = dist.get_rank(), dist.get_world_size()
-    N, M = (64, 64, 64), 400000
+    N = tuple(int(v) for v in os.environ.get("DIST_CHECK_N", "64,64,64").split(","))
+    M = int(os.environ.get("DIST_CHECK_M", "400000"))
     ok = True
     for dist_kind, part, mode in [("uniform", "equal_size", "allreduce"), ("clustered", "equal_count", "allreduce"),
-                                  ("uniform", "equal_size", "reduce"), ("uniform", "equal_size", "reduce_scatter")]:
+                                  ("uniform", "equal_size", "reduce"), ("uniform", "equal_size", "reduce_scatter"),
+                                  ("uniform", "grid", "grid_slab"), ("clustered", "grid", "grid_slab")]:
         x = idev.uniform_points(M, device=dev) if dist_kind == "uniform" else idev.clustered_points(M, device=dev)
         f = idev.uniform_values(M, device=dev)
         edges = equal_count_edges(x, world) if part == "equal_count" else None
-        mask = slab_mask(x, rank, world, edges)
+        if part == "grid":
+            mask = grid_slab_mask(x, rank, world, 2 * N[0])
+        else:
+            mask = slab_mask(x, rank, world, edges)
         xl, fl = x[mask].contiguous(), f[mask].contiguous()
         dp = DistPlan(N, xl.shape[0], mode=mode, device=dev)
         dp.set_points(xl)
         out = dp.adjoint(fl)
-        if mode == "reduce_scatter":
+        if mode in ("reduce_scatter", "grid_slab"):
             parts = [torch.empty_like(out) for _ in range(world)]
             dist.all_gather(parts, out)
-            out = torch.cat(parts, 0)
+            out = torch.cat(parts, 0 if mode == "reduce_scatter" else 1)
         if rank == 0:
             ref_plan = hp.Plan(N, M, device=dev)
             ref_plan.set_points(x)
@@ -51,9 +57,9 @@ def main():
 
             xh = x.cpu().numpy()
             fhh = f.cpu().numpy()
-            ks = np.array([[0, 0, 0], [5, -7, 31], [-32, 12, -3], [17, 17, -32]])
+            ks = np.array([[0, 0, 0], [5, -7, N[2] // 2 - 1], [-N[0] // 2, 12, -3], [17, 17, -N[2] // 2]])
             sref = oracle.ndft_direct(xh, fhh, N, ks=ks)
-            got = np.array([out[tuple(k + 32)].item() for k in ks])
+            got = np.array([out[tuple(k + np.array(N) // 2)].item() for k in ks])
             e2 = oracle.rel_l2_error(got, sref)
             print(f"[{dist_kind}/{part}/{mode}] world={world} local M={xl.shape[0]} "
                   f"E2(dist vs 1-GPU)={e:.2e} E2(vs NDFT, sampled)={e2:.2e}", flush=True)
