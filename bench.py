@@ -37,6 +37,13 @@ CONFIGS = {
     "5": {"N": (512, 512, 512), "M": 10 ** 9},
 }
 METRIC = "adjoint NFFT nonuniform points/s at N=256³ float64, 1/2/4/8 B200; E2 error"
+EXCHANGE_TEXT = {
+    "allreduce": "option A: ncclAllReduce of fhat inside libhpnfft.so",
+    "reduce": "option A: ncclReduce of fhat to rank 0 inside libhpnfft.so",
+    "reduce_scatter": "option A: ncclReduceScatter of fhat (k0 slabs) inside libhpnfft.so",
+    "grid_slab": "option G: grid halo ncclSend/Recv + distributed pruned FFT (all-to-all) inside libhpnfft.so, "
+                 "fhat left in k1 slabs",
+}
 M_WINDOW, SIGMA = 6, 2.0
 # FP64 tensor-core (DMMA m8n8k4) peak MEASURED on this pool's B200 with tools/ubench_dmma.cu /
 # tools/ubench_kstep.cu (profiles/ubench_dmma.txt, profiles/ubench_kstep.txt): 36.7 TFLOP/s for
@@ -145,14 +152,18 @@ def make_inputs(cfg, dist_kind, device):
     return x, f
 
 
-def slab_select(x, f, rank, ws, partition="equal_size"):
-    """This rank's x-slab subcell: equal-size slabs, or equal-count slabs."""
-    from paper_2001_01583_b200.dist import equal_count_edges, slab_mask
+def slab_select(x, f, rank, ws, partition="equal_size", exchange="allreduce", n0=512):
+    """This rank's x-slab subcell: equal-size slabs, equal-count slabs, or the
+    cell-aligned equal-size slabs of the grid_slab exchange (option G)."""
+    from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_mask, slab_mask
 
     if ws == 1:
         return x, f
-    edges = equal_count_edges(x, ws) if partition == "equal_count" else None
-    mask = slab_mask(x, rank, ws, edges)
+    if exchange == "grid_slab":
+        mask = grid_slab_mask(x, rank, ws, n0)
+    else:
+        edges = equal_count_edges(x, ws) if partition == "equal_count" else None
+        mask = slab_mask(x, rank, ws, edges)
     return x[mask].contiguous(), f[mask].contiguous()
 
 
@@ -172,20 +183,24 @@ def run_ours(args):
     N = cfg["N"]
     M_total = cfg["M"]
     x_all, f_all = make_inputs(cfg, args.dist, dev)
-    x, f = slab_select(x_all, f_all, rank, ws, args.partition)
+    x, f = slab_select(x_all, f_all, rank, ws, args.partition, args.exchange, int(SIGMA * N[0]))
     del x_all, f_all
     M_local = x.shape[0]
     torch.cuda.synchronize()
 
-    plan = hp.Plan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", device=dev)
+    if ws > 1:   # the library's multi-GPU plan: the exchange runs inside libhpnfft.so (NCCL)
+        from paper_2001_01583_b200.dist import DistPlan
+
+        dplan = DistPlan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", mode=args.exchange, device=dev)
+        plan = dplan.plan
+    else:
+        plan = hp.Plan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", device=dev)
     plan.set_spread_method(args.method)
-    out = torch.empty(N, dtype=torch.complex128, device=dev)
+    out = torch.empty(plan.out_shape, dtype=torch.complex128, device=dev)
 
     def step():
         plan.set_points(x)
         plan.adjoint(f, out=out)
-        if ws > 1:
-            tdist.all_reduce(out)
 
     for _ in range(args.warmup):
         step()
@@ -225,14 +240,10 @@ def run_ours(args):
     # ---- e2e: the public API with HOST buffers (pinned), H2D + transform + D2H each step ----
     xh = x.cpu().pin_memory()
     fh = f.cpu().pin_memory()
-    oh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+    oh = torch.empty(plan.out_shape, dtype=torch.complex128, pin_memory=True)
 
     def e2e_step():
-        res = plan.transform_host(xh, fh, oh)
-        if ws > 1:
-            d = res.to(dev, non_blocking=True)
-            tdist.all_reduce(d)
-            res.copy_(d, non_blocking=True)
+        plan.transform_host(xh, fh, oh)
 
     for _ in range(max(1, min(args.warmup, 2))):
         e2e_step()
@@ -314,8 +325,11 @@ def run_ours(args):
             "config": {"workload": f"BASELINE config {args.config}: d=3, N={N[0]}^3, M={M_total}, "
                                    f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}",
                        "N": list(N), "M": M_total, "m": M_WINDOW, "sigma": SIGMA, "window": "kaiser_bessel",
-                       "points": args.dist, "partition": f"{args.partition} x-slabs x{ws}",
-                       "exchange": "ncclAllReduce(fhat)" if ws > 1 else "none",
+                       "points": args.dist, "partition": (f"cell-aligned equal-size x-slabs x{ws}" if args.exchange == "grid_slab"
+                                     else f"{args.partition} x-slabs x{ws}"),
+                       "exchange": (EXCHANGE_TEXT[args.exchange] if ws > 1 else "none"),
+                       "fhat_layout": ("full on every rank" if ws == 1 or args.exchange == "allreduce"
+                                       else f"distributed: block {list(plan.out_shape)} per rank"),
                        "spread_method": args.method,
                        "l2": "inputs larger than L2 (x 240 MB, f 160 MB, grid 2.1 GB); no flush"},
             "e2e": {"value": M_total / (e2e_ms * 1e-3), "unit": "points/s", "h2d_bytes_per_step": h2d,
@@ -424,6 +438,8 @@ def main():
     ap.add_argument("--method", default="auto", choices=["auto", "atomic", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", default="equal_size", choices=["equal_size", "equal_count"])
+    ap.add_argument("--exchange", default="grid_slab", choices=["allreduce", "reduce", "reduce_scatter", "grid_slab"],
+                    help="multi-GPU exchange (SURVEY.md §8(e)); grid_slab = option G")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -292,6 +292,11 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
     set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
     return HPNFFT_E_RANGE;
   }
+  if (p->dist_err) {   // a cross-GPU barrier of an earlier grid-slab transform timed out
+    int e = 0;
+    cudaMemcpy(&e, p->dist_err, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e) return fail(p, HPNFFT_E_NCCL, "a cross-GPU barrier timed out (peer rank missing)");
+  }
   // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
   {
     const int64_t n0 = p->n[0];

@@ -76,6 +76,15 @@ struct Plan {
   int64_t slab_lo = 0, slab_len = 0;   // GRID_SLAB: owned x-ordered cell planes c0x in [lo, lo + len)
   double* halo = nullptr;       // GRID_SLAB: received halo planes [2m - 1][n1][n2] complex
   double* partial = nullptr;    // REDUCE_SCATTER: this rank's full partial fhat
+  // GRID_SLAB over NVLink peer memory (CUDA IPC): the ranks' grids and barrier flags
+  bool p2p = false;
+  double** peer_grid = nullptr;       // device array [nranks] (own grid at dist_rank)
+  double* peer_grid_host[16] = {};    // host copies (opened IPC pointers, closed at destroy)
+  uint32_t* flags = nullptr;          // device [64]: barrier epochs written by the peers
+  uint32_t** peer_flags = nullptr;    // device array [nranks]
+  uint32_t* peer_flags_host[16] = {};
+  uint32_t epoch = 0;
+  int* dist_err = nullptr;            // device flag: a cross-GPU barrier timed out
 
   // timing
   bool timing = false;
@@ -107,8 +116,9 @@ bool sweep_supported(const Plan* p);
 size_t record_bytes(int m);
 int fft_and_deconvolve(Plan* p, double* fhat);
 // one batched pruned FFT pass along dimension dim (fft.cu, see k_fft_pass)
+// (peers: device array of nranks output pointers for the grid-slab y pass over NVLink; NP = N/P)
 int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
-             int64_t o_start, int64_t o_total, int a_lo, int a_len);
+             int64_t o_start, int64_t o_total, int a_lo, int a_len, double* const* peers = nullptr, int NP = 1);
 // multi-GPU exchange steps (dist.cu)
 int dist_adjoint(Plan* p, const double* f, double* fhat);
 void dist_free(Plan* p);

@@ -13,7 +13,10 @@
 #include <dlfcn.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -37,6 +40,7 @@ struct NcclApi {
   NcclResult (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t);
   NcclResult (*Reduce)(const void*, void*, size_t, int, int, int, NcclComm, cudaStream_t);
   NcclResult (*ReduceScatter)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t);
+  NcclResult (*AllGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t);
   NcclResult (*Send)(const void*, size_t, int, int, NcclComm, cudaStream_t);
   NcclResult (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t);
   NcclResult (*GroupStart)();
@@ -64,6 +68,7 @@ const NcclApi* nccl() {
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(get("ncclAllReduce"));
     a.Reduce = reinterpret_cast<decltype(a.Reduce)>(get("ncclReduce"));
     a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(get("ncclReduceScatter"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(get("ncclAllGather"));
     a.Send = reinterpret_cast<decltype(a.Send)>(get("ncclSend"));
     a.Recv = reinterpret_cast<decltype(a.Recv)>(get("ncclRecv"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(get("ncclGroupStart"));
@@ -140,20 +145,34 @@ int halo_exchange(Plan* p) {
   double2* grid = reinterpret_cast<double2*>(p->grid);
   double2* halo = reinterpret_cast<double2*>(p->halo);
   NcclComm comm = p->comm;
+  // a run of k x-ordered planes starting at c0x is at most two memory-contiguous pieces
+  auto runs = [&](int64_t c0x, int k, auto&& fn) {
+    const int64_t first = mem_plane(c0x, n0);
+    const int k0 = (int)(first + k <= n0 ? k : n0 - first);
+    fn(first, 0, k0);
+    if (k0 < k) fn(0, k0, k - k0);
+  };
   HPNFFT_NCCL_TRY(p, a->GroupStart(), "ncclGroupStart");
   // my lower halo (m - 1 planes below my slab) -> rank r-1; my upper halo (m planes) -> rank r+1
-  for (int j = 0; j < m - 1; ++j)
-    HPNFFT_NCCL_TRY(p, a->Send(grid + mem_plane(lo - (m - 1) + j, n0) * pe, 2 * pe, kNcclFloat64, lower, comm, p->stream),
-                    "ncclSend halo");
-  for (int j = 0; j < m; ++j)
-    HPNFFT_NCCL_TRY(p, a->Send(grid + mem_plane(lo + L + j, n0) * pe, 2 * pe, kNcclFloat64, upper, comm, p->stream),
-                    "ncclSend halo");
-  // rank r+1's lower halo = my top m - 1 planes; rank r-1's upper halo = my bottom m planes
-  for (int j = 0; j < m - 1; ++j)
-    HPNFFT_NCCL_TRY(p, a->Recv(halo + (int64_t)j * pe, 2 * pe, kNcclFloat64, upper, comm, p->stream), "ncclRecv halo");
-  for (int j = 0; j < m; ++j)
-    HPNFFT_NCCL_TRY(p, a->Recv(halo + (int64_t)(m - 1 + j) * pe, 2 * pe, kNcclFloat64, lower, comm, p->stream),
-                    "ncclRecv halo");
+  int rcode = 0;
+  runs(lo - (m - 1), m - 1, [&](int64_t plane, int, int k) {
+    if (!rcode) rcode = a->Send(grid + plane * pe, 2 * pe * k, kNcclFloat64, lower, comm, p->stream);
+  });
+  runs(lo + L, m, [&](int64_t plane, int, int k) {
+    if (!rcode) rcode = a->Send(grid + plane * pe, 2 * pe * k, kNcclFloat64, upper, comm, p->stream);
+  });
+  // rank r+1's lower halo -> halo[0, m-1); rank r-1's upper halo -> halo[m-1, 2m-1), received in
+  // the sender's piece structure (the same x-ordered plane run, so the same split)
+  runs(lo + L - (m - 1), m - 1, [&](int64_t, int j, int k) {
+    if (!rcode) rcode = a->Recv(halo + (int64_t)j * pe, 2 * pe * k, kNcclFloat64, upper, comm, p->stream);
+  });
+  runs(lo, m, [&](int64_t, int j, int k) {
+    if (!rcode) rcode = a->Recv(halo + (int64_t)(m - 1 + j) * pe, 2 * pe * k, kNcclFloat64, lower, comm, p->stream);
+  });
+  if (rcode) {
+    a->GroupEnd();
+    return nccl_fail(p, rcode, "halo send/recv");
+  }
   HPNFFT_NCCL_TRY(p, a->GroupEnd(), "ncclGroupEnd");
   PlaneMap map;
   map.count = 2 * m - 1;
@@ -213,6 +232,166 @@ int slab_fft(Plan* p, double* fhat) {
   return rc;
 }
 
+// ---------------------------------------------------------------------------------------------
+// GRID_SLAB over NVLink peer memory: the grids of all ranks are mapped into every rank (CUDA IPC
+// handles exchanged once with ncclAllGather), the halo is PULLED from the neighbours' grids and
+// added locally, and the y FFT pass stores its outputs straight into the destination ranks'
+// buffers (the all-to-all is fused into the FFT epilogue).  Cross-GPU ordering comes from a
+// flag barrier in peer memory (release/acquire at system scope) between the phases.
+__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// every rank writes `epoch` into its slot of every rank's flags, then waits for all slots of its
+// own flags; gives up after 5 s (sets *err) instead of hanging the GPU
+__global__ void k_xbarrier(uint32_t* const* peer_flags, int P, int r, uint32_t epoch, int* err) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int s = 0; s < P; ++s) st_release_sys(peer_flags[s] + r, epoch);
+  const uint32_t* mine = peer_flags[r];
+  const uint64_t t0 = globaltimer();
+  for (int s = 0; s < P; ++s) {
+    while (ld_acquire_sys(mine + s) < epoch) {
+      if (globaltimer() - t0 > 5000000000ull) {
+        *err = 1;
+        return;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// my owned planes += the same memory planes of the neighbours' grids (their halo regions)
+__global__ void k_halo_pull(double2* __restrict__ grid, const double2* __restrict__ from_upper,
+                            const double2* __restrict__ from_lower, int64_t plane_elems, PlaneMap map, int n_upper) {
+  const int j = blockIdx.y;
+  if (j >= map.count) return;
+  const size_t off = (size_t)map.plane[j] * plane_elems;
+  double2* dst = grid + off;
+  const double2* src = (j < n_upper ? from_upper : from_lower) + off;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < plane_elems; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = dst[e];
+    const double2 b = src[e];
+    a.x += b.x;
+    a.y += b.y;
+    dst[e] = a;
+  }
+}
+
+int xbarrier(Plan* p) {
+  ++p->epoch;
+  k_xbarrier<<<1, 32, 0, p->stream>>>(p->peer_flags, p->nranks, p->dist_rank, p->epoch, p->dist_err);
+  p->launches++;
+  return check_launch(p, "cross-GPU barrier");
+}
+
+int slab_adjoint_p2p(Plan* p, double* fhat) {
+  const int P = p->nranks, r = p->dist_rank, m = p->m;
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2], pe = n1 * n2;
+  const int64_t N1 = p->N[1], N2 = p->N[2], N1P = N1 / P;
+  const int64_t lo = p->slab_lo, L = p->slab_len, l0 = mem_plane(lo, n0);
+  int rc;
+  // 1. halo: after every rank's sweep, pull the neighbours' halo planes into my own planes
+  stage_begin(p, 8);
+  rc = xbarrier(p);
+  if (rc) return rc;
+  {
+    PlaneMap map;
+    map.count = 2 * m - 1;
+    for (int j = 0; j < m - 1; ++j) map.plane[j] = (int)mem_plane(lo + L - (m - 1) + j, n0);   // from rank r+1
+    for (int j = 0; j < m; ++j) map.plane[m - 1 + j] = (int)mem_plane(lo + j, n0);           // from rank r-1
+    dim3 g((unsigned)((pe + 255) / 256 < 512 ? (pe + 255) / 256 : 512), (unsigned)map.count);
+    k_halo_pull<<<g, 256, 0, p->stream>>>(reinterpret_cast<double2*>(p->grid),
+                                         reinterpret_cast<const double2*>(p->peer_grid_host[(r + 1) % P]),
+                                         reinterpret_cast<const double2*>(p->peer_grid_host[(r - 1 + P) % P]), pe, map,
+                                         m - 1);
+    p->launches++;
+    rc = check_launch(p, "halo pull");
+    if (rc) return rc;
+  }
+  stage_end(p, 8);
+  // 2. z pass on the own planes (the grid is read for the last time)
+  stage_begin(p, 4);
+  rc = fft_pass(p, 2, p->grid, p->bufA, L * n1, 1, true, l0 * n1, n0 * n1, 0, (int)n2);
+  stage_end(p, 4);
+  if (rc) return rc;
+  // 3. every rank has finished reading its grid: the y pass stores into the destination ranks'
+  //    grids ([n0][N1/P][N2] receive layout) over NVLink, then everyone waits for everyone
+  stage_begin(p, 9);
+  rc = xbarrier(p);
+  stage_end(p, 9);
+  if (rc) return rc;
+  stage_begin(p, 5);
+  rc = fft_pass(p, 1, p->bufA, p->grid, L, N2, false, l0, n0, 0, (int)n1, p->peer_grid, (int)N1P);
+  if (!rc) rc = xbarrier(p);
+  stage_end(p, 5);
+  if (rc) return rc;
+  // 4. x pass on the own k1 slab
+  stage_begin(p, 6);
+  rc = fft_pass(p, 0, p->grid, fhat, 1, N1P * N2, false, 0, 1, 0, (int)n0);
+  stage_end(p, 6);
+  return rc;
+}
+
+// map the peers' grids and barrier flags (CUDA IPC, handles exchanged with ncclAllGather);
+// returns false (and leaves p->p2p unset) when peer memory is not available
+bool setup_p2p(Plan* p) {
+  const NcclApi* a = nccl();
+  const int P = p->nranks, r = p->dist_rank;
+  if (P > 16) return false;
+  if (cudaMalloc(&p->flags, 64 * sizeof(uint32_t)) != cudaSuccess) return false;
+  cudaMemset(p->flags, 0, 64 * sizeof(uint32_t));
+  cudaMalloc(&p->dist_err, sizeof(int));
+  cudaMemset(p->dist_err, 0, sizeof(int));
+  cudaIpcMemHandle_t h[2];
+  if (cudaIpcGetMemHandle(&h[0], p->grid) != cudaSuccess || cudaIpcGetMemHandle(&h[1], p->flags) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  unsigned char* dbuf = nullptr;
+  const size_t hb = sizeof(h);
+  if (cudaMalloc(&dbuf, hb * (P + 1)) != cudaSuccess) return false;
+  cudaMemcpy(dbuf + hb * P, h, hb, cudaMemcpyHostToDevice);
+  bool ok = a->AllGather(dbuf + hb * P, dbuf, hb, 0 /* ncclInt8 */, p->comm, p->stream) == 0;
+  std::vector<unsigned char> all(hb * P);
+  ok = ok && cudaStreamSynchronize(p->stream) == cudaSuccess &&
+       cudaMemcpy(all.data(), dbuf, hb * P, cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(dbuf);
+  for (int s = 0; s < P && ok; ++s) {
+    if (s == r) {
+      p->peer_grid_host[s] = p->grid;
+      p->peer_flags_host[s] = p->flags;
+      continue;
+    }
+    cudaIpcMemHandle_t hs[2];
+    memcpy(hs, all.data() + hb * s, hb);
+    void* g = nullptr;
+    void* fl = nullptr;
+    ok = cudaIpcOpenMemHandle(&g, hs[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+         cudaIpcOpenMemHandle(&fl, hs[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    p->peer_grid_host[s] = static_cast<double*>(g);
+    p->peer_flags_host[s] = static_cast<uint32_t*>(fl);
+  }
+  if (ok) {
+    ok = cudaMalloc(&p->peer_grid, sizeof(double*) * P) == cudaSuccess &&
+         cudaMalloc(&p->peer_flags, sizeof(uint32_t*) * P) == cudaSuccess &&
+         cudaMemcpy(p->peer_grid, p->peer_grid_host, sizeof(double*) * P, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(p->peer_flags, p->peer_flags_host, sizeof(uint32_t*) * P, cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  cudaGetLastError();
+  return ok;
+}
+
 }  // namespace
 
 int dist_adjoint(Plan* p, const double* f, double* fhat) {
@@ -248,6 +427,7 @@ int dist_adjoint(Plan* p, const double* f, double* fhat) {
     case HPNFFT_DIST_GRID_SLAB:
       rc = spread(p, f);
       if (rc) return rc;
+      if (p->p2p) return slab_adjoint_p2p(p, fhat);
       stage_begin(p, 8);
       rc = halo_exchange(p);
       stage_end(p, 8);
@@ -260,6 +440,21 @@ int dist_adjoint(Plan* p, const double* f, double* fhat) {
 }
 
 void dist_free(Plan* p) {
+  for (int s = 0; s < 16; ++s) {
+    if (s == p->dist_rank) continue;
+    if (p->peer_grid_host[s]) cudaIpcCloseMemHandle(p->peer_grid_host[s]);
+    if (p->peer_flags_host[s]) cudaIpcCloseMemHandle(p->peer_flags_host[s]);
+    p->peer_grid_host[s] = nullptr;
+    p->peer_flags_host[s] = nullptr;
+  }
+  cudaFree(p->peer_grid);
+  cudaFree(p->peer_flags);
+  cudaFree(p->flags);
+  cudaFree(p->dist_err);
+  p->peer_grid = nullptr;
+  p->peer_flags = nullptr;
+  p->flags = nullptr;
+  p->dist_err = nullptr;
   if (p->comm && nccl()->ok) nccl()->CommDestroy(p->comm);
   p->comm = nullptr;
   cudaFree(p->halo);
@@ -353,6 +548,10 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
     hpnfft_destroy(h);
     set_error("device allocation of the exchange buffers failed");
     return HPNFFT_E_NOMEM;
+  }
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1) {
+    const char* env = getenv("HPNFFT_DIST_P2P");
+    p->p2p = !(env && env[0] == '0') && setup_p2p(p);
   }
   *out = h;
   return HPNFFT_OK;

@@ -87,6 +87,11 @@ struct LineIO {
   const double* inv_c;   // 1/c_k per kept output
   bool valid;
   int a_lo, a_len;       // elements a with (a - a_lo) mod n < a_len are loaded, the others are 0
+  // peer-memory output (multi-GPU grid-slab y pass): output k of line (o, i) is stored over
+  // NVLink into rank k / NP's buffer at ((o NP + k mod NP) ostride + i); null = local output
+  cplx* const* peers;
+  int NP;
+  int64_t line_o, line_i;
 };
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
@@ -148,7 +153,9 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
         if (io.valid && (lo || hi)) {
           const int k = lo ? q + N / 2 : q - (n - N / 2);
           const double sc = io.inv_c[k];
-          io.gout[(int64_t)k * io.ostride] = {v[b][r].x * sc, v[b][r].y * sc};
+          cplx* dst = io.peers ? io.peers[k / io.NP] + ((io.line_o * io.NP + k % io.NP) * io.ostride + io.line_i)
+                               : io.gout + (int64_t)k * io.ostride;
+          *dst = {v[b][r].x * sc, v[b][r].y * sc};
         }
       } else {
         buf[slot<LOGN, TI, CONTIG>(q, col)] = v[b][r];
@@ -175,7 +182,7 @@ template <int LOGN, int TI, bool CONTIG>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
            const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
-           int a_len) {
+           int a_len, cplx* const* peers, int NP) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
   extern __shared__ cplx smem[];
@@ -185,6 +192,8 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
   io.inv_c = inv_c;
   io.a_lo = a_lo;
   io.a_len = a_len;
+  io.peers = peers;
+  io.NP = NP;
   int col, tj;
   if (CONTIG) {
     col = tid / T;
@@ -208,6 +217,8 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     io.istride = inner;
     io.gout = out + o * (int64_t)N * inner + ic;
     io.ostride = inner;
+    io.line_o = o;
+    io.line_i = ic;
   }
   run_stages<LOGN, TI, CONTIG, 0>(smem, col, tj, tw, io);
 }
@@ -229,7 +240,7 @@ constexpr int tile_cols_contig() {
 template <int LOGN>
 static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
                          const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
-                         int a_lo, int a_len) {
+                         int a_lo, int a_len, cplx* const* peers, int NP) {
   constexpr int TI = tile_cols<LOGN>();
   constexpr int TC = tile_cols_contig<LOGN>();
   constexpr int n = 1 << LOGN;
@@ -242,7 +253,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
-                                                                            o_start, o_total, a_lo, a_len);
+                                                                            o_start, o_total, a_lo, a_len, nullptr, 1);
   } else {
     const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
     const int64_t blocks = outer * ((inner + TI - 1) / TI);
@@ -250,7 +261,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
-                                                     a_len);
+                                                     a_len, peers, NP);
   }
   p->launches++;
   return check_launch(p, "fft pass");
@@ -258,20 +269,20 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
 
 static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t outer, int64_t inner, int N,
                        const double* inv_c, const double* tw, bool contig, int64_t o_start, int64_t o_total,
-                       int a_lo, int a_len) {
+                       int a_lo, int a_len, cplx* const* peers = nullptr, int NP = 1) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
   cplx* co = reinterpret_cast<cplx*>(out);
   const cplx* ct = reinterpret_cast<const cplx*>(tw);
   switch (logn) {
-    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
-    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len);
+    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
     default:
       set_error("FFT length not supported");
       return HPNFFT_E_UNSUPPORTED;
@@ -279,9 +290,9 @@ static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t
 }
 
 int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
-             int64_t o_start, int64_t o_total, int a_lo, int a_len) {
+             int64_t o_start, int64_t o_total, int a_lo, int a_len, double* const* peers, int NP) {
   return launch_pass(p, p->logn[dim], in, out, outer, inner, (int)p->N[dim], p->inv_c[dim], p->twiddle[dim], contig,
-                     o_start, o_total, a_lo, a_len);
+                     o_start, o_total, a_lo, a_len, reinterpret_cast<cplx* const*>(peers), NP);
 }
 
 int fft_and_deconvolve(Plan* p, double* fhat) {

@@ -128,7 +128,7 @@ class DistPlan:
         """This rank's partial fhat_rank(k) (Eq. 8 term) from the injected local transform."""
         return self.local_fn(self._x, f)
 
-    def adjoint(self, f):
+    def adjoint(self, f, out=None):
         """fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate of Alg. 3).
 
         Library plans run the whole exchange in libhpnfft.so (NCCL); with ``local_fn`` the
@@ -137,7 +137,7 @@ class DistPlan:
         import torch.distributed as dist
 
         if self.plan is not None:
-            out = self.plan.adjoint(f)
+            out = self.plan.adjoint(f, out=out)
             return None if (self.mode == "reduce" and self.rank != 0) else out
         fh = self.partial(f)
         if self.world == 1:
