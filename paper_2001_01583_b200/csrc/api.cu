@@ -288,8 +288,12 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
                                      cudaMemcpyDeviceToHost, p->stream),
                   "flag d2h");
   HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
-  if (p->err_flag_host[0]) {
+  if (p->err_flag_host[0] == 1) {
     set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
+    return HPNFFT_E_RANGE;
+  }
+  if (p->err_flag_host[0] == 2) {
+    set_error("a point lies outside this rank's grid slab (HPNFFT_DIST_GRID_SLAB)");
     return HPNFFT_E_RANGE;
   }
   if (p->dist_err) {   // a cross-GPU barrier of an earlier grid-slab transform timed out

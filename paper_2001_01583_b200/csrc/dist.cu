@@ -527,6 +527,13 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
   p->dist_rank = rank;
   p->slab_len = n0 / nranks;
   p->slab_lo = (int64_t)rank * p->slab_len;
+  // grid-slab ranks zero and scan only their own key range per set_points (sort.cu key_range):
+  // the rest of the bin table must read as empty
+  if (cudaMemset(p->bin_count, 0, sizeof(uint32_t) * (size_t)(p->nbins + 1)) != cudaSuccess) {
+    hpnfft_destroy(h);
+    set_error("bin table initialisation failed");
+    return HPNFFT_E_CUDA;
+  }
   if (nranks > 1) {
     NcclUid u;
     memcpy(u.internal, id, 128);

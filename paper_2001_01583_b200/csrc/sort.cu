@@ -21,8 +21,8 @@ __global__ void k_range_init(int* err) {
 }
 
 __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
-                       uint32_t* __restrict__ count, uint32_t* __restrict__ key, uint32_t* __restrict__ rank,
-                       int* __restrict__ err) {
+                       uint32_t k_lo, uint32_t k_hi, uint32_t* __restrict__ count, uint32_t* __restrict__ key,
+                       uint32_t* __restrict__ rank, int* __restrict__ err) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // occupied range of the x-ordered plane index c0x = (c0 + n0/2) mod n0 (monotone in x0):
   // warp min/max, one atomic per warp
@@ -62,6 +62,10 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
   int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
   int64_t nb2 = n2 >> s2;
   uint32_t k = (uint32_t)(((((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc) | (c0 & ((1 << lc) - 1)));
+  if (k < k_lo || k >= k_hi) {   // grid-slab plan: the point is outside this rank's planes
+    *err = 2;
+    k = k_lo;
+  }
   key[j] = k;
   rank[j] = atomicAdd(&count[k], 1u);
 }
@@ -180,17 +184,35 @@ __global__ void k_gather_x(const double* __restrict__ x, int64_t M, const uint32
 
 int64_t scan_workspace_elems(int64_t nbins) { return scan_tmp_need(nbins + 1); }
 
+// Key range [k_lo, k_hi) this plan's points may use: all bins, or for a grid-slab rank only the
+// bins of its own cell planes (one contiguous key range thanks to the chunk-major order).  Only
+// that range is zeroed and scanned per set_points; the bins outside stay 0 (zeroed at plan
+// time), so every lookup outside reads an empty range.
+static void key_range(const Plan* p, int s2, uint32_t& k_lo, uint32_t& k_hi) {
+  k_lo = 0;
+  k_hi = (uint32_t)p->nbins;
+  if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
+    const int64_t n0 = p->n[0], lc = p->chunk_log, per_chunk = (p->n[1] * (p->n[2] >> s2)) << lc;
+    const int64_t c0a = ((p->slab_lo + n0 / 2) % n0);   // first memory plane of the slab
+    k_lo = (uint32_t)((c0a >> lc) * per_chunk);
+    k_hi = (uint32_t)(((c0a + p->slab_len) >> lc) * per_chunk);
+  }
+}
+
 int sort_points(Plan* p, const double* x) {
   const int64_t M = p->M;
-  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count, 0, sizeof(uint32_t) * (p->nbins + 1), p->stream), "memset bins");
-  k_range_init<<<1, 2 * kRangeSlots + 1, 0, p->stream>>>(p->err_flag);
-  p->launches++;
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
+  uint32_t k_lo, k_hi;
+  key_range(p, s2, k_lo, k_hi);
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count + k_lo, 0, sizeof(uint32_t) * ((size_t)(k_hi - k_lo) + 1), p->stream),
+                  "memset bins");
+  k_range_init<<<1, 2 * kRangeSlots + 1, 0, p->stream>>>(p->err_flag);
+  p->launches++;
   stage_begin(p, 0);
   if (M > 0) {
     k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->n[0], p->n[1], p->n[2], s2, p->chunk_log,
-                                                               p->bin_count,
+                                                               k_lo, k_hi, p->bin_count,
                                                                p->key, p->rank, p->err_flag);
     p->launches++;
     int rc = check_launch(p, "keys");
@@ -198,7 +220,7 @@ int sort_points(Plan* p, const double* x) {
   }
   stage_end(p, 0);
   stage_begin(p, 1);
-  int rc = scan_exclusive(p, p->bin_count, p->nbins + 1, reinterpret_cast<uint32_t*>(p->scan_tmp));
+  int rc = scan_exclusive(p, p->bin_count + k_lo, (int64_t)(k_hi - k_lo) + 1, reinterpret_cast<uint32_t*>(p->scan_tmp));
   if (rc) return rc;
   stage_end(p, 1);
   stage_begin(p, 2);
