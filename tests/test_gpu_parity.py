@@ -289,7 +289,8 @@ def test_stage_timing_and_launch_count():
         plan.adjoint(fd)
     t = plan.stage_times()
     assert set(t) == set(hp.STAGES)
-    assert all(v > 0 for v in t.values())
+    assert all(v > 0 for k, v in t.items() if k not in ("exchange", "alltoall"))
+    assert t["exchange"] == 0 and t["alltoall"] == 0   # single-GPU plan: no exchange step
     assert t["records"] < t["spread"]
     assert plan.launch_count() >= 8
     plan.enable_timing(False)
