@@ -3,6 +3,8 @@
 Bars (BASELINE.json north_star): E2 <= 1e-12 against the CPU NFFT oracle (O2, same conventions)
 and E2 <= 1e-9 against the direct NDFT (O1).  Inputs are the seeded generators of inputs/.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -295,3 +297,22 @@ def test_stage_timing_and_launch_count():
     assert plan.launch_count() >= 8
     plan.enable_timing(False)
     plan.close()
+
+
+@pytest.mark.gpu
+def test_multi_gpu_modes_match_single_gpu():
+    """All multi-GPU exchange modes (allreduce, reduce, reduce_scatter, grid_slab over NVLink
+    peer memory) against the single-GPU transform and sampled NDFT values (tools/dist_check.py,
+    torchrun, one process per GPU).  Needs >= 2 visible GPUs."""
+    import subprocess
+    import sys
+
+    ng = torch.cuda.device_count()
+    if ng < 2:
+        pytest.skip("needs >= 2 GPUs")
+    ng = 4 if ng >= 4 else 2
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ng}",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "tools", "dist_check.py")]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
