@@ -72,6 +72,10 @@ struct SweepCfg {
   static constexpr int kThreads = (NW + 2) * 32;           // + copy warp + list warp
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
   static constexpr int kCtasPerSm = NW <= 8 ? 2 : 1;        // small patches: 2 resident CTAs
+  // the whole register file for the resident warps (multiple of 8 per thread, <= 255)
+  // (registers are granted to warps in groups of 4)
+  static constexpr int kMaxRegs0 = (65536 / ((NW + 2 + 3) / 4 * 4 * 32 * kCtasPerSm)) / 8 * 8;
+  static constexpr int kMaxRegs = kMaxRegs0 > 248 ? 248 : kMaxRegs0;
   static_assert(kRows <= 32, "one producer lane per candidate row");
 };
 
@@ -250,7 +254,7 @@ __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
 // ------------------------------------------------------------------------------------------
 // A4: the warp-specialised persistent sweep (see the file header).
 template <int P1, int P2, int M_>
-__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads, SweepCfg<P1, P2, M_>::kCtasPerSm)
+__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((SweepCfg<P1, P2, M_>::kMaxRegs))
     k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
   using R = Rec<2 * M_>;
@@ -682,9 +686,10 @@ int sweep_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HPNFFT_SWEEP_PATCH");
-    if (e && e[0] == '1' && e[1] == '2') v = 1;
+    if (e && e[0] == '1' && e[1] == '2' && e[3] == '3') v = 1;
     else if (e && e[0] == '1' && e[1] == '6') v = 2;
     else if (e && e[0] == '8' && e[2] == '1') v = 3;
+    else if (e && e[0] == '1' && e[1] == '2' && e[3] == '1') v = 4;
     else v = 0;
   }
   return v;
@@ -787,7 +792,8 @@ int run_sweep(Plan* p, const double* f) {
       p->launches++;
     }
     const int var = sweep_variant();
-    const int rc = var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
+    const int rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
+                 : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
                             : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
