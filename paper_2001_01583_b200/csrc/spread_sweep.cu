@@ -680,8 +680,10 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
 
 namespace {
 
-// CTA patch variant: 0 = 8 x 32 (16 consumer warps), 1 = 12 x 32 (24), 2 = 16 x 16 (16);
-// HPNFFT_SWEEP_PATCH = "8x32" | "12x32" | "16x16".
+// CTA patch variant (consumer warps = patch / 4 x 4, + copy and list warps): 0 = 12 x 16 (12, the
+// default: 14 warps leave 128 registers per thread), 1 = 12 x 32 (24), 2 = 16 x 16 (16),
+// 3 = 8 x 16 (8, two CTAs per SM), 4 = 8 x 32 (16); HPNFFT_SWEEP_PATCH = "12x16" | "12x32" |
+// "16x16" | "8x16" | "8x32".
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
@@ -689,7 +691,7 @@ int sweep_variant() {
     if (e && e[0] == '1' && e[1] == '2' && e[3] == '3') v = 1;
     else if (e && e[0] == '1' && e[1] == '6') v = 2;
     else if (e && e[0] == '8' && e[2] == '1') v = 3;
-    else if (e && e[0] == '1' && e[1] == '2' && e[3] == '1') v = 4;
+    else if (e && e[0] == '8' && e[2] == '3') v = 4;
     else v = 0;
   }
   return v;
@@ -792,11 +794,11 @@ int run_sweep(Plan* p, const double* f) {
       p->launches++;
     }
     const int var = sweep_variant();
-    const int rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
+    const int rc = var == 4 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                            : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
+                            : launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
