@@ -69,12 +69,16 @@ struct SweepCfg {
   static constexpr int W = 2 * M_;                         // taps per dimension
   static constexpr int NW = (P1 / kWR) * (P2 / kWC);       // consumer warps
   static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
-  static constexpr int kThreads = (NW + 2) * 32;           // + copy warp + list warp
+  // list warps: warp i owns ring stages i, i + kListWarps, ... (so that it waits on every phase of
+  // its stages' barriers in order; a parity wait must never skip a phase)
+  static constexpr int kListWarps = 1;   // (NS = 3 list warps measured no faster)
+  static_assert(NS % kListWarps == 0, "a list warp owns whole ring stages");
+  static constexpr int kThreads = (NW + 1 + kListWarps) * 32;   // + copy warp + list warps
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
   static constexpr int kCtasPerSm = NW <= 8 ? 2 : 1;        // small patches: 2 resident CTAs
   // the whole register file for the resident warps (multiple of 8 per thread, <= 255)
   // (registers are granted to warps in groups of 4)
-  static constexpr int kMaxRegs0 = (65536 / ((NW + 2 + 3) / 4 * 4 * 32 * kCtasPerSm)) / 8 * 8;
+  static constexpr int kMaxRegs0 = (65536 / ((NW + 1 + kListWarps + 3) / 4 * 4 * 32 * kCtasPerSm)) / 8 * 8;
   static constexpr int kMaxRegs = kMaxRegs0 > 248 ? 248 : kMaxRegs0;
   static_assert(kRows <= 32, "one producer lane per candidate row");
 };
@@ -418,26 +422,33 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       }
       next_stage();
     }
-    mbar_wait(&s_empty[stage], phase ^ 1u);
-    if (lane == 0) {
-      s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
-      mbar_arrive(&s_landed[stage]);
+    // one terminal marker per list warp (the consumers stop at the first)
+    for (int i = 0; i < C::kListWarps; ++i) {
+      mbar_wait(&s_empty[stage], phase ^ 1u);
+      if (lane == 0) {
+        s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
+        mbar_arrive(&s_landed[stage]);
+      }
+      next_stage();
     }
     return;
   }
 
-  if (warp == NW + 1) {
-    // ============================ list warp ============================
+  if (warp > NW) {
+    // ============================ list warps ============================
     // Once a stage's records have landed, sort them into one list per consumer warp: the records
     // whose 2m x 2m column footprint meets the warp's 4 x 4 sub-patch, entry = record | (c0 mod
     // CH) << 9 | d1 << 18 | d2 << 23 with d1 = (warp row) - (c1 - m + 1) + 3 < 2m + 3 and
     // d2 = (warp col) - (c2 - m + 1) + 3 < 2m + 3.  (Each consumer warp scanning the whole batch
     // itself would keep the FP64 tensor pipe idle while all of them do it at the same time.)
+    // List warp i takes batches i, i + kListWarps, ... of the ring (= stages it owns).
     constexpr int NWC = P2 / kWC;   // consumer warps per sub-patch row
-    int stage = 0;
-    uint32_t phase = 0;
-    for (;;) {
+    for (uint32_t seq = (uint32_t)(warp - NW - 1);; seq += C::kListWarps) {
+      const int stage = (int)(seq % NS);
+      const uint32_t phase = (seq / NS) & 1u;
+      const unsigned long long l0c = prm.prof ? clock64() : 0ull;
       mbar_wait(&s_landed[stage], phase);
+      const unsigned long long l1c = prm.prof ? clock64() : 0ull;
       const BatchHdr hdr = s_hdr[stage];
       int cnt[NW];   // list lengths (0 for tile-end markers)
 #pragma unroll
@@ -478,11 +489,11 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         if (lane == w % 32) s_cnt[stage * NW + w] = (uint32_t)cnt[w];
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_full[stage]);
-      if (hdr.B < 0) break;
-      if (++stage == NS) {
-        stage = 0;
-        phase ^= 1u;
+      if (prm.prof && lane == 0) {
+        atomicAdd(prm.prof + 9, l1c - l0c);
+        atomicAdd(prm.prof + 10, clock64() - l1c);
       }
+      if (hdr.B < 0) break;
     }
     return;
   }
@@ -754,9 +765,10 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
     double nw = (double)h[7];
     fprintf(stderr,
             "[sweep prof] cap=%d consumer warps=%.0f  per warp Mcycles: wait_full %.2f  lists %.2f  apply %.2f  "
-            "advance %.2f | producer (lane 0 sums, Mcycles): lookups %.2f  wait_empty %.2f  issue %.2f\n",
+            "advance %.2f | producer (lane 0 sums, Mcycles): lookups %.2f  wait_empty %.2f  issue %.2f | list warp: "
+            "wait_landed %.2f  build %.2f\n",
             cap, nw, h[0] / nw / 1e6, h[1] / nw / 1e6, h[2] / nw / 1e6, h[3] / nw / 1e6, h[4] / blocks / 1e6,
-            h[5] / blocks / 1e6, h[6] / blocks / 1e6);
+            h[5] / blocks / 1e6, h[6] / blocks / 1e6, h[9] / blocks / 1e6, h[10] / blocks / 1e6);
     cudaFree(prof);
   }
   return check_launch(p, "spread_sweep");
