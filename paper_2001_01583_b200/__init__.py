@@ -233,5 +233,66 @@ class Plan:
             pass
 
 
+class HostPipeline:
+    """Streamed end-to-end transforms from and to pinned HOST memory.
+
+    submit(x_host, f_host, out_host) enqueues one transform: the H2D copies of x and f on a copy
+    stream, set_points + adjoint on the compute stream, the D2H copy of fhat on a second copy
+    stream, with two device buffer sets so that the copies of one transform overlap the
+    kernels of its neighbours (PCIe in both directions and the GPU busy at the same time).
+    out_host is complete after flush() (or after the next-but-one submit).  Every submitted
+    transform still moves all of its own inputs and its result across PCIe.
+    """
+
+    def __init__(self, plan: "Plan", M: int):
+        import torch
+
+        self.plan = plan
+        dev = plan.device
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        self.compute = torch.cuda.current_stream(dev)
+        self.x = [torch.empty((M, 3), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.f = [torch.empty((M,), dtype=torch.complex128, device=dev) for _ in range(2)]
+        self.o = [torch.empty(plan.out_shape, dtype=torch.complex128, device=dev) for _ in range(2)]
+        self.in_ready = [torch.cuda.Event() for _ in range(2)]
+        self.used = [None, None]      # compute finished reading buffer set s
+        self.drained = [None, None]   # D2H finished reading output buffer s
+        self.i = 0
+
+    def submit(self, x_host, f_host, out_host):
+        import torch
+
+        s = self.i & 1
+        with torch.cuda.stream(self.h2d):
+            if self.used[s] is not None:
+                self.h2d.wait_event(self.used[s])
+            self.x[s].copy_(x_host, non_blocking=True)
+            self.f[s].copy_(f_host, non_blocking=True)
+            self.in_ready[s].record(self.h2d)
+        self.compute.wait_event(self.in_ready[s])
+        if self.drained[s] is not None:
+            self.compute.wait_event(self.drained[s])
+        with torch.cuda.stream(self.compute):
+            self.plan.set_points(self.x[s])
+            self.plan.adjoint(self.f[s], out=self.o[s])
+            done = torch.cuda.Event()
+            done.record(self.compute)
+        self.used[s] = done
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(done)
+            out_host.copy_(self.o[s], non_blocking=True)
+            drained = torch.cuda.Event()
+            drained.record(self.d2h)
+        self.drained[s] = drained
+        self.i += 1
+        return out_host
+
+    def flush(self):
+        self.h2d.synchronize()
+        self.compute.synchronize()
+        self.d2h.synchronize()
+
+
 def version() -> str:
     return load_library().hpnfft_version().decode()
