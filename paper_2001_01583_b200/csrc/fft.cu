@@ -138,11 +138,12 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
     const int j = tj + b * T;
     const int jm = j & (Ns - 1);
     if (Ns > 1) {
-      // twiddles w^r, w = exp(-2 pi i step / n): w, w^2 (and w^4) from the table, the other
-      // powers by one complex product each (fewer L1 loads than one table load per r)
+      // twiddles w^r, w = exp(-2 pi i step / n): w from the table, its powers by complex
+      // products (one L1 load instead of seven; a few ulp per power, far below the 1e-12 bar)
       const int step = jm * (n / (Ns * R));
       if (R == 8) {
-        const cplx w1 = tw[step & (n - 1)], w2 = tw[(2 * step) & (n - 1)], w4 = tw[(4 * step) & (n - 1)];
+        const cplx w1 = tw[step & (n - 1)];
+        const cplx w2 = cmul(w1, w1), w4 = cmul(w2, w2);
         const cplx w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
         const cplx ws[8] = {w1, w1, w2, w3, w4, w5, w6, w7};
 #pragma unroll
