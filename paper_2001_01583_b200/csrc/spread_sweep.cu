@@ -40,6 +40,9 @@ constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 #ifndef HPNFFT_SWEEP_NS
 #define HPNFFT_SWEEP_NS 3
 #endif
+#ifndef HPNFFT_SWEEP_NTSKIP
+#define HPNFFT_SWEEP_NTSKIP 0   // skip n-tiles no record of a k-step reaches (measured: DESIGN.md)
+#endif
 #ifndef HPNFFT_SWEEP_DEBUG
 #define HPNFFT_SWEEP_DEBUG 0    // measurement builds only: 1 = skip the MMAs, 2 = skip apply
 #endif
@@ -597,7 +600,11 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(recs);
     // operands of one k-step (lane: record k + t), loaded as a group so that two k-steps' shared
     // memory loads are in flight before their DMMAs issue
-    auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT]) {
+    // Sub-patch rows (n-tiles) outside every footprint of the k-step are skipped
+    // (HPNFFT_SWEEP_NTSKIP): lists are in batch order = candidate-row order, so the 4 records of
+    // a k-step mostly share d1.
+    auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT], int& ntlo,
+                     int& nthi) {
       const bool act = k + t < nlist;
       const uint32_t en = act ? my[k + t] : 0u;
       const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
@@ -613,11 +620,20 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
         w1v[nt] = lds_f64(ra + 8u * (uint32_t)(R::kW1 + min((unsigned)(d1 - (kWR - 1) + nt), (unsigned)W)));
+#if HPNFFT_SWEEP_NTSKIP
+      const int lo = act ? max(0, (kWR - 1) - d1) : NT, hi = act ? min(NT - 1, W + kWR - 2 - d1) : -1;
+      ntlo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
+      nthi = __reduce_max_sync(0xffffffffu, hi + 1) - 1;
+#else
+      ntlo = 0;
+      nthi = NT - 1;
+#endif
     };
-    auto apply = [&](double a0, double a1, double fp, double w2v, const double (&w1v)[NT]) {
+    auto apply = [&](double a0, double a1, double fp, double w2v, const double (&w1v)[NT], int ntlo, int nthi) {
       const double fw2 = fp * w2v;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
+        if (nt < ntlo || nt > nthi) continue;   // warp-uniform
         const double b = fw2 * w1v[nt];
 #if HPNFFT_SWEEP_DEBUG == 1
         acc[nt][0] += a0 * b + a1;   // measurement only: keep the operands alive, skip the MMAs
@@ -629,32 +645,36 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     // the first k-step's operand loads are issued before the flush of the earlier chunks, whose
     // accumulator reads wait for this warp's in-flight DMMAs
     double p0, p1, pf, p2v, p1v[NT];
-    if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v);
+    int plo = 0, phi = NT - 1;
+    if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v, plo, phi);
     advance(step0);                       // earlier chunks are complete
     int k = 0;
     if (nlist > 0) {
       if (nlist > 4) {
         double b0, b1, gp, g2v, g1v[NT];
-        fetch(4, b0, b1, gp, g2v, g1v);
-        apply(p0, p1, pf, p2v, p1v);
-        apply(b0, b1, gp, g2v, g1v);
+        int blo, bhi;
+        fetch(4, b0, b1, gp, g2v, g1v, blo, bhi);
+        apply(p0, p1, pf, p2v, p1v, plo, phi);
+        apply(b0, b1, gp, g2v, g1v, blo, bhi);
         k = 8;
       } else {
-        apply(p0, p1, pf, p2v, p1v);
+        apply(p0, p1, pf, p2v, p1v, plo, phi);
         k = 4;
       }
     }
     for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
       double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
-      fetch(k, a0, a1, fp, w2v, w1v);
-      fetch(k + 4, b0, b1, gp, g2v, g1v);
-      apply(a0, a1, fp, w2v, w1v);
-      apply(b0, b1, gp, g2v, g1v);
+      int alo, ahi, blo, bhi;
+      fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
+      fetch(k + 4, b0, b1, gp, g2v, g1v, blo, bhi);
+      apply(a0, a1, fp, w2v, w1v, alo, ahi);
+      apply(b0, b1, gp, g2v, g1v, blo, bhi);
     }
     if (k < nlist) {
       double a0, a1, fp, w2v, w1v[NT];
-      fetch(k, a0, a1, fp, w2v, w1v);
-      apply(a0, a1, fp, w2v, w1v);
+      int alo, ahi;
+      fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
+      apply(a0, a1, fp, w2v, w1v, alo, ahi);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[stage]);
