@@ -43,6 +43,10 @@ constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 #ifndef HPNFFT_SWEEP_NTSKIP
 #define HPNFFT_SWEEP_NTSKIP 0   // skip n-tiles no record of a k-step reaches (measured: DESIGN.md)
 #endif
+#ifndef HPNFFT_SWEEP_PROFILE
+#define HPNFFT_SWEEP_PROFILE 0  // measurement builds only: clock64 phase counters (HPNFFT_SWEEP_PROF=1)
+#endif
+constexpr bool kProf = HPNFFT_SWEEP_PROFILE != 0;
 #ifndef HPNFFT_SWEEP_DEBUG
 #define HPNFFT_SWEEP_DEBUG 0    // measurement builds only: 1 = skip the MMAs, 2 = skip apply
 #endif
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           rb1 = b2hi - prm.nb2;
         }
         for (int ci = 0; ci < nch; ++ci) {
-          const unsigned long long p0 = prm.prof ? clock64() : 0ull;
+          const unsigned long long p0 = kProf ? clock64() : 0ull;
           const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
           uint32_t beg0 = 0, len0 = 0, beg1 = 0, len1 = 0;
           if (r < C::kRows) {
@@ -385,13 +389,13 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           }
           const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
           const uint32_t off0 = incl - cnt, off1 = off0 + len0;
-          if (prm.prof && lane == 0) atomicAdd(prm.prof + 4, clock64() - p0);
+          if (kProf && lane == 0) atomicAdd(prm.prof + 4, clock64() - p0);
           for (uint32_t b0 = 0; b0 < total; b0 += (uint32_t)cap) {
             const uint32_t b1 = min(total, b0 + (uint32_t)cap);
             const int B = (int)(b1 - b0);
-            const unsigned long long p1 = prm.prof ? clock64() : 0ull;
+            const unsigned long long p1 = kProf ? clock64() : 0ull;
             mbar_wait(&s_empty[stage], phase ^ 1u);
-            const unsigned long long p2 = prm.prof ? clock64() : 0ull;
+            const unsigned long long p2 = kProf ? clock64() : 0ull;
             if (lane == 0) mbar_expect_tx(&s_landed[stage], (uint32_t)B * (uint32_t)(RD * sizeof(double)));
             __syncwarp();
             double* dst = s_rec + (size_t)stage * cap * RD;
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
               s_hdr[stage] = BatchHdr{B, t, ci, 0};
               mbar_arrive(&s_landed[stage]);
             }
-            if (prm.prof && lane == 0) {
+            if (kProf && lane == 0) {
               atomicAdd(prm.prof + 5, p2 - p1);
               atomicAdd(prm.prof + 6, clock64() - p2);
             }
@@ -449,9 +453,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     for (uint32_t seq = (uint32_t)(warp - NW - 1);; seq += C::kListWarps) {
       const int stage = (int)(seq % NS);
       const uint32_t phase = (seq / NS) & 1u;
-      const unsigned long long l0c = prm.prof ? clock64() : 0ull;
+      const unsigned long long l0c = kProf ? clock64() : 0ull;
       mbar_wait(&s_landed[stage], phase);
-      const unsigned long long l1c = prm.prof ? clock64() : 0ull;
+      const unsigned long long l1c = kProf ? clock64() : 0ull;
       const BatchHdr hdr = s_hdr[stage];
       int cnt[NW];   // list lengths (0 for tile-end markers)
 #pragma unroll
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         if (lane == w % 32) s_cnt[stage * NW + w] = (uint32_t)cnt[w];
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_full[stage]);
-      if (prm.prof && lane == 0) {
+      if (kProf && lane == 0) {
         atomicAdd(prm.prof + 9, l1c - l0c);
         atomicAdd(prm.prof + 10, clock64() - l1c);
       }
@@ -568,9 +572,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   unsigned long long tw = 0, tl = 0, tf = 0, tA = 0;
   const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(s_zero);
   for (;;) {
-    const unsigned long long q0 = prm.prof ? clock64() : 0ull;
+    const unsigned long long q0 = kProf ? clock64() : 0ull;
     mbar_wait(&s_full[stage], phase);
-    const unsigned long long q1 = prm.prof ? clock64() : 0ull;
+    const unsigned long long q1 = kProf ? clock64() : 0ull;
     const BatchHdr hdr = s_hdr[stage];
     if (hdr.B < 0) break;
     if (hdr.tile != cur_tile) {
@@ -591,7 +595,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     // ---- this warp's list (built by the list warp) ----
     int nlist = (int)s_cnt[stage * NW + warp];
     const uint32_t* my = s_list + ((size_t)stage * NW + warp) * cap;
-    const unsigned long long q2 = prm.prof ? clock64() : 0ull;
+    const unsigned long long q2 = kProf ? clock64() : 0ull;
 #if HPNFFT_SWEEP_DEBUG == 2
     nlist = 0;   // measurement only: skip apply
 #endif
@@ -678,10 +682,10 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[stage]);
-    const unsigned long long q3 = prm.prof ? clock64() : 0ull;
+    const unsigned long long q3 = kProf ? clock64() : 0ull;
     if (hdr.end == 1) advance(nsteps);   // tile finished: flush the remaining nodes
     if (hdr.end == 2) cur = nsteps;      // tile skipped in a multi-group pass: nothing to write
-    if (prm.prof) {
+    if (kProf) {
       tw += q1 - q0;
       tl += q2 - q1;
       tf += q3 - q2;
@@ -700,7 +704,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     if (z == 1234.5678) prm.grid[0] = z;
   }
 #endif
-  if (prm.prof && lane == 0) {
+  if (kProf && lane == 0) {
     atomicAdd(prm.prof + 0, tw);
     atomicAdd(prm.prof + 1, tl);
     atomicAdd(prm.prof + 2, tf);
@@ -711,10 +715,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
 
 namespace {
 
-// CTA patch variant (consumer warps = patch / 4 x 4, + copy and list warps): 0 = 12 x 16 (12, the
-// default: 14 warps leave 128 registers per thread), 1 = 12 x 32 (24), 2 = 16 x 16 (16),
-// 3 = 8 x 16 (8, two CTAs per SM), 4 = 8 x 32 (16); HPNFFT_SWEEP_PATCH = "12x16" | "12x32" |
-// "16x16" | "8x16" | "8x32".
+// CTA patch variant (consumer warps = patch / 4 x 4, + copy and list warps): 0 = 8 x 32 (16, the
+// default), 1 = 12 x 32 (24), 2 = 16 x 16 (16), 3 = 8 x 16 (8, two CTAs per SM), 4 = 12 x 16 (12,
+// 128 registers); HPNFFT_SWEEP_PATCH = "8x32" | "12x32" | "16x16" | "8x16" | "12x16".
 int sweep_variant() {
   static int v = -1;
   if (v < 0) {
@@ -722,7 +725,7 @@ int sweep_variant() {
     if (e && e[0] == '1' && e[1] == '2' && e[3] == '3') v = 1;
     else if (e && e[0] == '1' && e[1] == '6') v = 2;
     else if (e && e[0] == '8' && e[2] == '1') v = 3;
-    else if (e && e[0] == '8' && e[2] == '3') v = 4;
+    else if (e && e[0] == '1' && e[1] == '2' && e[3] == '1') v = 4;
     else v = 0;
   }
   return v;
@@ -826,11 +829,11 @@ int run_sweep(Plan* p, const double* f) {
       p->launches++;
     }
     const int var = sweep_variant();
-    const int rc = var == 4 ? launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi)
+    const int rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
                  : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                            : launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi);
+                            : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for L in paper_2001_01583_b200/libhpnfft.so build_var/ntskip.so; do
-HPNFFT_LIB=$L timeout 120 python tools/profile_step.py --config 4 --timing --reps 3 2>&1 | tail -1 | cut -c1-240
-done
-HPNFFT_LIB=build_var/ntskip.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+for D in clustered uniform; do for P in 12x16 16x16 8x32; do
+HPNFFT_SWEEP_PATCH=$P timeout 120 python tools/profile_step.py --config 4 --dist $D --timing --reps 4 2>&1 | tail -1 | grep -o "'dist': '[a-z]*'\|'patch': '[0-9x]*'\|'spread': [0-9.]*" | tr '\n' ' '; echo
+done; done
