@@ -78,7 +78,10 @@ struct SweepCfg {
   static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
   // list warps: warp i owns ring stages i, i + kListWarps, ... (so that it waits on every phase of
   // its stages' barriers in order; a parity wait must never skip a phase)
-  static constexpr int kListWarps = 1;   // (NS = 3 list warps measured no faster)
+#ifndef HPNFFT_SWEEP_LISTW
+#define HPNFFT_SWEEP_LISTW 1
+#endif
+  static constexpr int kListWarps = HPNFFT_SWEEP_LISTW;
   static_assert(NS % kListWarps == 0, "a list warp owns whole ring stages");
   static constexpr int kThreads = (NW + 1 + kListWarps) * 32;   // + copy warp + list warps
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
