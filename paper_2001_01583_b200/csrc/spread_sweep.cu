@@ -74,7 +74,13 @@ struct Chunk {
 template <int P1, int P2, int M_>
 struct SweepCfg {
   static constexpr int W = 2 * M_;                         // taps per dimension
-  static constexpr int NW = (P1 / kWR) * (P2 / kWC);       // consumer warps
+  static constexpr int NL = (P1 / kWR) * (P2 / kWC);       // 4 x 4 sub-patches (= record lists)
+#ifndef HPNFFT_SWEEP_SUB
+#define HPNFFT_SWEEP_SUB 1
+#endif
+  static constexpr int SUB = HPNFFT_SWEEP_SUB;             // sub-patches per consumer warp
+  static_assert(NL % SUB == 0, "whole sub-patches per warp");
+  static constexpr int NW = NL / SUB;                      // consumer warps
   static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
   // list warps: warp i owns ring stages i, i + kListWarps, ... (so that it waits on every phase of
   // its stages' barriers in order; a parity wait must never skip a phase)
@@ -85,7 +91,7 @@ struct SweepCfg {
   static_assert(NS % kListWarps == 0, "a list warp owns whole ring stages");
   static constexpr int kThreads = (NW + 1 + kListWarps) * 32;   // + copy warp + list warps
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
-  static constexpr int kCtasPerSm = NW <= 8 ? 2 : 1;        // small patches: 2 resident CTAs
+  static constexpr int kCtasPerSm = NL <= 8 ? 2 : 1;        // small patches: 2 resident CTAs
   // the whole register file for the resident warps (multiple of 8 per thread, <= 255)
   // (registers are granted to warps in groups of 4)
   static constexpr int kMaxRegs0 = (65536 / ((NW + 1 + kListWarps + 3) / 4 * 4 * 32 * kCtasPerSm)) / 8 * 8;
@@ -262,7 +268,7 @@ template <int P1, int P2, int M_>
 __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
   using C = SweepCfg<P1, P2, M_>;
   return sizeof(double) * ((size_t)C::NS * cap * Rec<2 * M_>::kDoubles + Rec<2 * M_>::kDoubles) +
-         (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NW * (cap + 1) + 16;
+         (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NL * (cap + 1) + 16;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
   using R = Rec<2 * M_>;
-  constexpr int W = C::W, NW = C::NW, NS = C::NS;
+  constexpr int W = C::W, NW = C::NW, NS = C::NS, NL = C::NL, SUB = C::SUB;
   constexpr int RD = R::kDoubles;
   constexpr int CH = Chunk<M_>::CH;
   constexpr int LC = Chunk<M_>::LOG;
@@ -285,8 +291,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   uint64_t* s_empty = s_full + NS;                                                // [NS] stage free
   uint64_t* s_landed = s_empty + NS;                                              // [NS] records landed
   BatchHdr* s_hdr = reinterpret_cast<BatchHdr*>(s_landed + NS);                   // [NS]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_hdr + NS);                      // [NS][NW]
-  uint32_t* s_list = s_cnt + NS * NW;                                             // [NS][NW][cap]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_hdr + NS);                      // [NS][NL]
+  uint32_t* s_list = s_cnt + NS * NL;                                             // [NS][NL][cap]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
@@ -460,14 +466,14 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       mbar_wait(&s_landed[stage], phase);
       const unsigned long long l1c = kProf ? clock64() : 0ull;
       const BatchHdr hdr = s_hdr[stage];
-      int cnt[NW];   // list lengths (0 for tile-end markers)
+      int cnt[NL];   // list lengths (0 for tile-end markers)
 #pragma unroll
-      for (int w = 0; w < NW; ++w) cnt[w] = 0;
+      for (int w = 0; w < NL; ++w) cnt[w] = 0;
       if (hdr.B > 0) {
         int R0, C0, L0, S_, a_lo, nch;
         tile_geom(hdr.tile, R0, C0, L0, S_, a_lo, nch);
         const double* recs = s_rec + (size_t)stage * cap * RD;
-        uint32_t* lists = s_list + (size_t)stage * NW * cap;
+        uint32_t* lists = s_list + (size_t)stage * NL * cap;
         for (int base = 0; base < hdr.B; base += 32) {
           const int e = base + lane;
           int dr = -1000, dc = -1000;   // footprint origin relative to the patch origin
@@ -495,8 +501,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         }
       }
 #pragma unroll
-      for (int w = 0; w < NW; ++w)
-        if (lane == w % 32) s_cnt[stage * NW + w] = (uint32_t)cnt[w];
+      for (int w = 0; w < NL; ++w)
+        if (lane == w % 32) s_cnt[stage * NL + w] = (uint32_t)cnt[w];
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_full[stage]);
       if (kProf && lane == 0) {
@@ -515,17 +521,28 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   // row is stored and zeroed.  Four records per k-step:
   //   C += A (16 x 4: w0 of each record placed at its cell's cyclic offset)
   //      x B (4 x 32: f w1[i1] w2[i2] of each record for every column, 0 outside its footprint)
-  const int wr_off = (warp / (P2 / kWC)) * kWR;
-  const int wc_off = (warp % (P2 / kWC)) * kWC;
+  // consumer warp `warp` owns sub-patches warp * SUB .. warp * SUB + SUB - 1 (each 4 x 4 columns)
+  int wr_off[SUB], wc_off[SUB];
+#pragma unroll
+  for (int u = 0; u < SUB; ++u) {
+    const int spid = warp * SUB + u;
+    wr_off[u] = (spid / (P2 / kWC)) * kWR;
+    wc_off[u] = (spid % (P2 / kWC)) * kWC;
+  }
   const int g = lane >> 2, t = lane & 3;
   constexpr int NT = kWR * kWC / 4;       // n-tiles of 8 real columns (4 complex)
   const int part = g & 1;                 // B: real (0) or imaginary (1) part of the column
   const int bc0 = g >> 1;                 // B: column c of complex column q = 4 nt + g/2 (row nt)
   int cur_tile = -1;
-  int first = 0, off = 0, S = 0, wr0 = 0, wc0 = 0, nsteps = 0;
-  double acc[NT][4];                      // m16n8k4 C-fragment per n-tile: rows g (0, 1), g + 8 (2, 3)
+  int first = 0, off = 0, S = 0, nsteps = 0;
+  int wr0[SUB], wc0[SUB];
+  double acc[SUB][NT][4];                 // m16n8k4 C-fragment per n-tile: rows g (0, 1), g + 8 (2, 3)
 #pragma unroll
-  for (int a = 0; a < NT; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.0;
+  for (int u = 0; u < SUB; ++u) {
+    wr0[u] = wc0[u] = 0;
+#pragma unroll
+    for (int a = 0; a < NT; ++a) acc[u][a][0] = acc[u][a][1] = acc[u][a][2] = acc[u][a][3] = 0.0;
+  }
   int cur = 0;                            // steps (cells first + s) < cur are flushed
 
   // Flush steps [cur, upto): after step sp (cell first + sp) node first + sp - m + 1 is final
@@ -548,21 +565,25 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const int sp = cur + ds;
           const int rel = sp - M_ + 1 - off;
           const int l0 = (first + sp - M_ + 1) & (n0 - 1);
-          double2* base = reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0 * n2 + (wc0 + t);
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {   // complex column (row nt, col t) of the sub-patch
-            if (rel >= 0 && rel < S && wr0 + nt < n1) {
-              double2* dst = base + (size_t)nt * n2;
-              if (prm.accumulate) {
-                double2 o = *dst;
-                o.x += acc[nt][2 * h];
-                o.y += acc[nt][2 * h + 1];
-                *dst = o;
-              } else {
-                *dst = make_double2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+          for (int u = 0; u < SUB; ++u) {
+            double2* base =
+                reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0[u] * n2 + (wc0[u] + t);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {   // complex column (row nt, col t) of the sub-patch
+              if (rel >= 0 && rel < S && wr0[u] + nt < n1) {
+                double2* dst = base + (size_t)nt * n2;
+                if (prm.accumulate) {
+                  double2 o = *dst;
+                  o.x += acc[u][nt][2 * h];
+                  o.y += acc[u][nt][2 * h + 1];
+                  *dst = o;
+                } else {
+                  *dst = make_double2(acc[u][nt][2 * h], acc[u][nt][2 * h + 1]);
+                }
               }
+              acc[u][nt][2 * h] = acc[u][nt][2 * h + 1] = 0.0;
             }
-            acc[nt][2 * h] = acc[nt][2 * h + 1] = 0.0;
           }
         }
       }
@@ -587,20 +608,32 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       first = a_lo * CH;
       off = L0 - first;
       nsteps = nch * CH;
-      wr0 = R0 + wr_off;
-      wc0 = C0 + wc_off;
       cur = 0;
 #pragma unroll
-      for (int a = 0; a < NT; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.0;
+      for (int u = 0; u < SUB; ++u) {
+        wr0[u] = R0 + wr_off[u];
+        wc0[u] = C0 + wc_off[u];
+#pragma unroll
+        for (int a = 0; a < NT; ++a) acc[u][a][0] = acc[u][a][1] = acc[u][a][2] = acc[u][a][3] = 0.0;
+      }
     }
     const int step0 = hdr.chunk * CH;
     const double* recs = s_rec + (size_t)stage * cap * RD;
-    // ---- this warp's list (built by the list warp) ----
-    int nlist = (int)s_cnt[stage * NW + warp];
-    const uint32_t* my = s_list + ((size_t)stage * NW + warp) * cap;
+    // ---- this warp's lists (built by the list warp) ----
+    int nl[SUB];
+    const uint32_t* ml[SUB];
+#pragma unroll
+    for (int u = 0; u < SUB; ++u) {
+      nl[u] = (int)s_cnt[stage * NL + warp * SUB + u];
+      ml[u] = s_list + ((size_t)stage * NL + warp * SUB + u) * cap;
+    }
+    int nlist = nl[0];
+    const uint32_t* my = ml[0];
     const unsigned long long q2 = kProf ? clock64() : 0ull;
 #if HPNFFT_SWEEP_DEBUG == 2
     nlist = 0;   // measurement only: skip apply
+#pragma unroll
+    for (int u = 0; u < SUB; ++u) nl[u] = 0;
 #endif
     // ---- k-steps of 4 records (any order inside the chunk); lanes past the list end read the
     //      all-zero record ----
@@ -610,10 +643,10 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     // Sub-patch rows (n-tiles) outside every footprint of the k-step are skipped
     // (HPNFFT_SWEEP_NTSKIP): lists are in batch order = candidate-row order, so the 4 records of
     // a k-step mostly share d1.
-    auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT], int& ntlo,
-                     int& nthi) {
-      const bool act = k + t < nlist;
-      const uint32_t en = act ? my[k + t] : 0u;
+    auto fetch_l = [&](const uint32_t* lst, int n, int k, double& a0, double& a1, double& fp, double& w2v,
+                       double (&w1v)[NT], int& ntlo, int& nthi) {
+      const bool act = k + t < n;
+      const uint32_t en = act ? lst[k + t] : 0u;
       const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
       const int sh = step0 + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
       const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
@@ -636,52 +669,77 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       nthi = NT - 1;
 #endif
     };
-    auto apply = [&](double a0, double a1, double fp, double w2v, const double (&w1v)[NT], int ntlo, int nthi) {
+    auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT], int& ntlo,
+                     int& nthi) { fetch_l(my, nlist, k, a0, a1, fp, w2v, w1v, ntlo, nthi); };
+    auto apply_u = [&](double (&ac)[NT][4], double a0, double a1, double fp, double w2v, const double (&w1v)[NT],
+                       int ntlo, int nthi) {
       const double fw2 = fp * w2v;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         if (nt < ntlo || nt > nthi) continue;   // warp-uniform
         const double b = fw2 * w1v[nt];
 #if HPNFFT_SWEEP_DEBUG == 1
-        acc[nt][0] += a0 * b + a1;   // measurement only: keep the operands alive, skip the MMAs
+        ac[nt][0] += a0 * b + a1;   // measurement only: keep the operands alive, skip the MMAs
 #else
-        dmma16(acc[nt], a0, a1, b);
+        dmma16(ac[nt], a0, a1, b);
 #endif
       }
     };
-    // the first k-step's operand loads are issued before the flush of the earlier chunks, whose
-    // accumulator reads wait for this warp's in-flight DMMAs
-    double p0, p1, pf, p2v, p1v[NT];
-    int plo = 0, phi = NT - 1;
-    if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v, plo, phi);
-    advance(step0);                       // earlier chunks are complete
-    int k = 0;
-    if (nlist > 0) {
-      if (nlist > 4) {
-        double b0, b1, gp, g2v, g1v[NT];
-        int blo, bhi;
-        fetch(4, b0, b1, gp, g2v, g1v, blo, bhi);
-        apply(p0, p1, pf, p2v, p1v, plo, phi);
-        apply(b0, b1, gp, g2v, g1v, blo, bhi);
-        k = 8;
-      } else {
-        apply(p0, p1, pf, p2v, p1v, plo, phi);
-        k = 4;
+    auto apply = [&](double a0, double a1, double fp, double w2v, const double (&w1v)[NT], int ntlo, int nthi) {
+      apply_u(acc[0], a0, a1, fp, w2v, w1v, ntlo, nthi);
+    };
+    if constexpr (SUB == 1) {
+      // the first k-step's operand loads are issued before the flush of the earlier chunks, whose
+      // accumulator reads wait for this warp's in-flight DMMAs
+      double p0, p1, pf, p2v, p1v[NT];
+      int plo = 0, phi = NT - 1;
+      if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v, plo, phi);
+      advance(step0);                       // earlier chunks are complete
+      int k = 0;
+      if (nlist > 0) {
+        if (nlist > 4) {
+          double b0, b1, gp, g2v, g1v[NT];
+          int blo, bhi;
+          fetch(4, b0, b1, gp, g2v, g1v, blo, bhi);
+          apply(p0, p1, pf, p2v, p1v, plo, phi);
+          apply(b0, b1, gp, g2v, g1v, blo, bhi);
+          k = 8;
+        } else {
+          apply(p0, p1, pf, p2v, p1v, plo, phi);
+          k = 4;
+        }
       }
-    }
-    for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
-      double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
-      int alo, ahi, blo, bhi;
-      fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
-      fetch(k + 4, b0, b1, gp, g2v, g1v, blo, bhi);
-      apply(a0, a1, fp, w2v, w1v, alo, ahi);
-      apply(b0, b1, gp, g2v, g1v, blo, bhi);
-    }
-    if (k < nlist) {
-      double a0, a1, fp, w2v, w1v[NT];
-      int alo, ahi;
-      fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
-      apply(a0, a1, fp, w2v, w1v, alo, ahi);
+      for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
+        double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
+        int alo, ahi, blo, bhi;
+        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
+        fetch(k + 4, b0, b1, gp, g2v, g1v, blo, bhi);
+        apply(a0, a1, fp, w2v, w1v, alo, ahi);
+        apply(b0, b1, gp, g2v, g1v, blo, bhi);
+      }
+      if (k < nlist) {
+        double a0, a1, fp, w2v, w1v[NT];
+        int alo, ahi;
+        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
+        apply(a0, a1, fp, w2v, w1v, alo, ahi);
+      }
+    } else {
+      // two sub-patches: their k-steps (independent accumulators) are interleaved
+      double p0, p1, pf, p2v, p1v[NT], b0, b1, gp, g2v, g1v[NT];
+      int plo = 0, phi = NT - 1, blo = 0, bhi = NT - 1;
+      if (nl[0] > 0) fetch_l(ml[0], nl[0], 0, p0, p1, pf, p2v, p1v, plo, phi);
+      if (nl[1] > 0) fetch_l(ml[1], nl[1], 0, b0, b1, gp, g2v, g1v, blo, bhi);
+      advance(step0);                     // earlier chunks are complete
+      int ka = 0, kb = 0;
+      while (ka < nl[0] || kb < nl[1]) {
+        const bool da = ka < nl[0], db = kb < nl[1];
+        if (da) apply_u(acc[0], p0, p1, pf, p2v, p1v, plo, phi);
+        if (db) apply_u(acc[1], b0, b1, gp, g2v, g1v, blo, bhi);
+        ka += 4;
+        kb += 4;
+        if (ka < nl[0]) fetch_l(ml[0], nl[0], ka, p0, p1, pf, p2v, p1v, plo, phi);
+        if (kb < nl[1]) fetch_l(ml[1], nl[1], kb, b0, b1, gp, g2v, g1v, blo, bhi);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[stage]);
@@ -703,7 +761,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   {  // keep the accumulators alive
     double z = 0.0;
 #pragma unroll
-    for (int a = 0; a < NT; ++a) z += acc[a][0] + acc[a][1] + acc[a][2] + acc[a][3];
+    for (int u = 0; u < SUB; ++u)
+#pragma unroll
+      for (int a = 0; a < NT; ++a) z += acc[u][a][0] + acc[u][a][1] + acc[u][a][2] + acc[u][a][3];
     if (z == 1234.5678) prm.grid[0] = z;
   }
 #endif
