@@ -9,6 +9,9 @@ Parts:
   O1 ndft_direct        direct NDFT, Eq. (5), Kahan-summed (oracle.c)
   O2 nfft_adjoint       CUNFFT steps in the paper's order: spread -> FFT -> scale
                         (Fig. 1, Alg. 2)
+  O1i ndft_inverse_direct  direct inverse NDFT, Eq. (6), Kahan-summed (oracle.c)
+  O2i nfft_inverse      inverse CUNFFT in the paper's order: subdivide -> inverse FFT ->
+                        interpolate (Fig. 2, Alg. 5)
   O3 windows            window/deconvolution pair (windows.py)
   O4 ewald              Madelung constant via Eqs. 10-12 (ewald.py)
   O5 rel_l2_error       Eq. (9)
@@ -56,6 +59,10 @@ def _load():
         lib.oracle_taps.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                     dp, i64p]
         lib.oracle_taps.restype = ctypes.c_int
+        lib.oracle_ndft_inverse.argtypes = [ctypes.c_int, i64p, ctypes.c_int64, dp, dp, dp, ctypes.c_int]
+        lib.oracle_ndft_inverse.restype = ctypes.c_int
+        lib.oracle_interp.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int64, dp, dp, dp]
+        lib.oracle_interp.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -204,6 +211,70 @@ def nfft_adjoint(x, f, N, m: int = 6, sigma: float = 2.0, window: int = KAISER_B
     n = grid_size(N, sigma)
     g = spread(x, f, n, m, sigma, window)
     return deconvolve_crop(fft_grid(g), N, m, sigma, window)
+
+
+def ndft_inverse_direct(x, fhat, N, nthreads: int = 0) -> np.ndarray:
+    """O1i: f(x_j) = sum_{k in I_N} fhat(k) exp(+2 pi i k.x_j) (Eq. 6).
+
+    fhat: array of shape N (index k + N/2).  Returns [M] complex.
+    """
+    N = _check_N(N)
+    d = len(N)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, d)
+    fh = np.ascontiguousarray(np.asarray(fhat, dtype=np.complex128).reshape(N))
+    M = x.shape[0]
+    out = np.zeros(2 * max(M, 1), dtype=np.float64)
+    if M == 0:
+        return np.zeros(0, dtype=np.complex128)
+    fv = fh.reshape(-1).view(np.float64).copy()
+    rc = _load().oracle_ndft_inverse(d, _ip(np.array(N, dtype=np.int64)), M, _dp(x), _dp(fv), _dp(out), nthreads)
+    if rc:
+        raise RuntimeError("oracle_ndft_inverse failed")
+    return out.view(np.complex128)[:M].copy()
+
+
+def subdivide(fhat, N, n, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
+    """O2i step 1 (Subdividing): ghat(k mod n) = fhat(k) / prod_t c_k for k in I_N,
+    0 for the other k in I_n (the transpose of deconvolve_crop)."""
+    N = _check_N(N)
+    fh = np.asarray(fhat, dtype=np.complex128).reshape(N)
+    for t in range(3):
+        c = windows.deconv_factors(N[t], n[t], m, sigma, window)
+        shape = [1, 1, 1]
+        shape[t] = N[t]
+        fh = fh / c.reshape(shape)
+    ghat = np.zeros(tuple(n), dtype=np.complex128)
+    idx = np.ix_(*[np.arange(-N[t] // 2, N[t] // 2) % n[t] for t in range(3)])
+    ghat[idx] = fh
+    return ghat
+
+
+def ifft_grid(ghat: np.ndarray) -> np.ndarray:
+    """O2i step 2 (Inverse FFT): g(l) = sum_k ghat(k) exp(+2 pi i k.l/n),
+    unnormalised (numpy's ifftn divides by prod n_t)."""
+    return np.fft.ifftn(ghat) * float(np.prod(ghat.shape))
+
+
+def interpolate(g: np.ndarray, x, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
+    """O2i step 3 (Interpolating): f_j = sum_l g(l) prod_t Phi(n_t x_jt - l_t)."""
+    n = g.shape
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+    M = x.shape[0]
+    f = np.zeros(2 * max(M, 1), dtype=np.float64)
+    if M:
+        gv = np.ascontiguousarray(g, dtype=np.complex128).reshape(-1).view(np.float64)
+        rc = _load().oracle_interp(_ip(np.array(n, dtype=np.int64)), m, sigma, window, M, _dp(x), _dp(gv), _dp(f))
+        if rc:
+            raise RuntimeError("oracle_interp failed")
+    return f.view(np.complex128)[:M].copy()
+
+
+def nfft_inverse(x, fhat, N, m: int = 6, sigma: float = 2.0, window: int = KAISER_BESSEL) -> np.ndarray:
+    """O2i: the CPU inverse CUNFFT of Eq. (6) in Alg. 5's order: subdivide -> inverse FFT ->
+    interpolate (PAPER.md:63, :242-262)."""
+    N = _check_N(N)
+    n = grid_size(N, sigma)
+    return interpolate(ifft_grid(subdivide(fhat, N, n, m, sigma, window)), x, m, sigma, window)
 
 
 def rel_l2_error(a, b) -> float:

@@ -13,6 +13,12 @@
  *                      PAPER.md:162, §3): g(l) += f_j * prod_t Phi(u_t - l_t) over the
  *                      truncated neighbourhood J(x_j), l taken modulo n (periodic grid).
  *                      Plain serial loop over points, taps in natural order.
+ * O1i oracle_ndft_inverse : direct inverse NDFT, Eq. (6) of PAPER.md:43 (§1),
+ *                      f(x_j) = sum_{k in I_N} fhat(k) exp(+2 pi i k.x_j), Kahan-summed, one
+ *                      output point at a time (OpenMP over points only).
+ * O2i oracle_interp  : the "Interpolating" step of inverse CUNFFT (§2 Fig. 2 and
+ *                      PAPER.md:242, §3): f_j = sum_l g(l) prod_t Phi(u_t - l_t) over the same
+ *                      truncated neighbourhood as oracle_spread (its transpose).
  *
  * Conventions (readings Q1-Q10):
  *   u_t = n_t x_t (exact: n_t a power of two), c_t = floor(u_t), t_t = u_t - c_t (exact),
@@ -159,6 +165,89 @@ int oracle_taps(int64_t n, int m, double sigma, int window, double x, double* w,
     int64_t lm = (ci - m + 1 + i) % n;
     if (lm < 0) lm += n;
     idx[i] = lm;
+  }
+  return 0;
+}
+
+/* O1i: direct inverse NDFT.  x: [M][d]; fhat: all of I_N in row-major order (index k_t + N_t/2),
+ * [|I_N|][2]; out: [M][2].  exp(+2 pi i k x) = conj(phase(k, x)).  Returns 0 on success. */
+int oracle_ndft_inverse(int d, const int64_t* N, int64_t M, const double* x, const double* fhat, double* out,
+                        int nthreads) {
+  if (d < 1 || d > 3) return -1;
+  int64_t total = 1;
+  for (int t = 0; t < d; ++t) total *= N[t];
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t j = 0; j < M; ++j) {
+    double sr = 0.0, si = 0.0, cr = 0.0, ci = 0.0;
+    for (int64_t q = 0; q < total; ++q) {
+      int64_t k[3] = {0, 0, 0};
+      int64_t r = q;
+      for (int t = d - 1; t >= 0; --t) {
+        k[t] = (r % N[t]) - N[t] / 2;
+        r /= N[t];
+      }
+      double er = 1.0, ei = 0.0;
+      for (int t = 0; t < d; ++t) {
+        double pr, pi_;
+        phase(k[t], x[j * d + t], &pr, &pi_);
+        pi_ = -pi_; /* exp(+2 pi i k x) */
+        double nr = er * pr - ei * pi_;
+        double ni = er * pi_ + ei * pr;
+        er = nr;
+        ei = ni;
+      }
+      double fr = fhat[2 * q], fi = fhat[2 * q + 1];
+      double vr = fr * er - fi * ei;
+      double vi = fr * ei + fi * er;
+      double y, tt;
+      y = vr - cr; tt = sr + y; cr = (tt - sr) - y; sr = tt;
+      y = vi - ci; tt = si + y; ci = (tt - si) - y; si = tt;
+    }
+    out[2 * j] = sr;
+    out[2 * j + 1] = si;
+  }
+  return 0;
+}
+
+/* O2i: interpolate.  n: grid sizes [3]; g: [n0][n1][n2][2]; x: [M][3]; out f: [M][2].
+ * Same taps and weights as oracle_spread (the interpolation is the spread's transpose). */
+int oracle_interp(const int64_t* n, int m, double sigma, int window, int64_t M, const double* x,
+                  const double* g, double* f) {
+  if (m < 1 || m > 16) return -1;
+  const int taps = 2 * m;
+  double w[3][32];
+  int64_t idx[3][32];
+  for (int64_t j = 0; j < M; ++j) {
+    for (int t = 0; t < 3; ++t) {
+      double u = (double)n[t] * x[j * 3 + t];
+      double c = floor(u);
+      double tt = u - c;
+      int64_t ci = (int64_t)c;
+      for (int i = 0; i < taps; ++i) {
+        int64_t l = ci - m + 1 + i;
+        int inside = !(i == taps - 1 && tt == 0.0);
+        w[t][i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
+        int64_t lm = l % n[t];
+        if (lm < 0) lm += n[t];
+        idx[t][i] = lm;
+      }
+    }
+    double sr = 0.0, si = 0.0;
+    for (int i0 = 0; i0 < taps; ++i0) {
+      for (int i1 = 0; i1 < taps; ++i1) {
+        for (int i2 = 0; i2 < taps; ++i2) {
+          double wt = w[0][i0] * w[1][i1] * w[2][i2];
+          int64_t off = ((idx[0][i0] * n[1] + idx[1][i1]) * n[2] + idx[2][i2]) * 2;
+          sr += g[off] * wt;
+          si += g[off + 1] * wt;
+        }
+      }
+    }
+    f[2 * j] = sr;
+    f[2 * j + 1] = si;
   }
   return 0;
 }

@@ -305,3 +305,83 @@ def test_inputs_generator_properties():
     c = inputs.clustered_points(50000, s=0.05)
     assert c.min() >= -0.5 and c.max() < 0.5
     assert np.array_equal(inputs.clustered_points(7, start=100), c[100:107])
+
+
+# ------------------------------------------------------- O1i / O2i (Eq. 6) --
+def test_O1i_mpmath_brute_force():
+    """O1i vs 50-digit brute force of Eq. 6, M = 5, N = 4^3."""
+    x = inputs.uniform_points(5, seed=12)
+    rng = np.random.default_rng(12)
+    fh = rng.standard_normal((4, 4, 4)) + 1j * rng.standard_normal((4, 4, 4))
+    got = oracle.ndft_inverse_direct(x, fh, (4, 4, 4))
+    mpmath.mp.dps = 50
+    ks = oracle.index_set((4, 4, 4))
+    ref = np.zeros(5, dtype=np.complex128)
+    for j in range(5):
+        s = mpmath.mpc(0)
+        for q, k in enumerate(ks):
+            arg = sum(int(k[t]) * mpmath.mpf(float(x[j, t])) for t in range(3))
+            v = fh.reshape(-1)[q]
+            s += mpmath.mpc(float(v.real), float(v.imag)) * mpmath.expjpi(2 * arg)
+        ref[j] = complex(s)
+    assert oracle.rel_l2_error(got, ref) < 1e-15
+
+
+def test_O1i_equispaced_reduces_to_idft_and_origin():
+    """x_j = N^{-1} ⊙ j (j in I_N): Eq. 6 is the inverse DFT (Eq. 4) up to the index shift,
+    i.e. prod N_t * numpy.fft.ifftn; a point at the origin gives sum_k fhat(k)."""
+    N = (8, 6, 4)
+    x = inputs.equispaced_points(N)
+    rng = np.random.default_rng(7)
+    fh = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    got = oracle.ndft_inverse_direct(x, fh, N).reshape(N)
+    # fhat index k + N/2 -> numpy index k mod N; output j + N/2 <- numpy index j mod N
+    G = np.fft.ifftn(np.fft.ifftshift(fh)) * np.prod(N)
+    ref = np.fft.fftshift(G)
+    assert oracle.rel_l2_error(got, ref) < 1e-14
+    o = oracle.ndft_inverse_direct(np.zeros((1, 3)), fh, N)
+    assert abs(o[0] - fh.sum()) < 1e-12
+
+
+def test_O1i_is_the_adjoint_of_O1():
+    """Eq. 6 is A^H of Eq. 5's matrix A: <A f, g> = <f, A^H g> for any f, g."""
+    N = (8, 8, 6)
+    x = inputs.uniform_points(200, seed=21)
+    f = inputs.uniform_values(200, seed=21)
+    rng = np.random.default_rng(21)
+    g = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    lhs = np.vdot(g, oracle.ndft_direct(x, f, N))
+    rhs = np.vdot(oracle.ndft_inverse_direct(x, g, N), f)
+    assert abs(lhs - rhs) / abs(lhs) < 1e-13
+
+
+def test_O2i_is_the_transpose_of_O2():
+    """The inverse CUNFFT (subdivide, inverse FFT, interpolate) is exactly the
+    adjoint of the pinned O2 chain (spread, FFT, deconvolve/crop): <O2 f, g> = <f, O2i g> to
+    rounding, for both windows and odd/boundary points.  A dropped factor, a wrong sign or a
+    transposed index in any O2i step breaks this identity."""
+    N = (8, 16, 4)
+    x = inputs.uniform_points(300, seed=23)
+    x[0] = [0.5, -0.5, 0.0]
+    x[1] = [0.25, 0.125, -0.375]   # on grid nodes
+    f = inputs.uniform_values(300, seed=23)
+    rng = np.random.default_rng(23)
+    g = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    for win, m in ((windows.KAISER_BESSEL, 4), (windows.KAISER_BESSEL, 6), (windows.GAUSSIAN, 3)):
+        lhs = np.vdot(g, oracle.nfft_adjoint(x, f, N, m=m, window=win))
+        rhs = np.vdot(oracle.nfft_inverse(x, g, N, m=m, window=win), f)
+        assert abs(lhs - rhs) / abs(lhs) < 1e-13
+
+
+def test_O2i_accuracy_vs_O1i_paper_section4():
+    """§4 setup ("the obtained precision data of HP-NFFT and its inverse process"):
+    E2(O2i vs O1i) decays with m and meets 1e-9 at m = 6, like the forward direction."""
+    setup = json.load(open(os.path.join(GOLDEN, "paper_section4_setup.json")))
+    M, N = setup["M"], tuple(setup["N"])
+    x = inputs.uniform_points(M)
+    rng = np.random.default_rng(4)
+    fh = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    s = oracle.ndft_inverse_direct(x, fh, N)
+    errs = [oracle.rel_l2_error(oracle.nfft_inverse(x, fh, N, m=m), s) for m in (2, 4, 6)]
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] < setup["north_star_e2_bar_m6"]
