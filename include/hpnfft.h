@@ -96,6 +96,22 @@ int hpnfft_set_points(hpnfft_plan_t p, const double* x);
  */
 int hpnfft_adjoint(hpnfft_plan_t p, const double* f, double* fhat);
 
+/*
+ * Inverse direction (Eq. 6, §1): the adjoint of Eq. 5's
+ * matrix, called "inverse NDFT" in the paper (not a matrix inverse):
+ *     f(x_j) = sum_{k in I_N} fhat(k) exp(+2 pi i k.x_j),   j < M,
+ * by the inverse CUNFFT of Alg. 5: Subdividing (fhat / c_k into the
+ * oversampled spectrum), Inverse FFT, Interpolating (a gather with the same 2m taps per
+ * dimension as the spread, no atomics).  Same conventions and error level as hpnfft_adjoint
+ * (the two are exact transposes of each other up to rounding).
+ *   fhat : DEVICE [N0*N1*N2][2] float64, row-major at index k_t + N_t/2 (the FULL fhat also on
+ *          multi-GPU plans: every rank interpolates its own points, Alg. 4).
+ *   f    : DEVICE [M][2] float64 output in the ORIGINAL point order of set_points.
+ * Requires a prior successful hpnfft_set_points (else HPNFFT_E_STATE).  Uses the plan's grid
+ * workspace, so it must not overlap an hpnfft_adjoint of the same plan.  Asynchronous.
+ */
+int hpnfft_inverse(hpnfft_plan_t p, const double* fhat, double* f);
+
 /* Release the plan and its workspace (synchronises the plan's stream).  NULL is a no-op. */
 int hpnfft_destroy(hpnfft_plan_t p);
 
@@ -122,7 +138,8 @@ int64_t hpnfft_launch_count(hpnfft_plan_t p);
  * out[0] keys+histogram, out[1] scan, out[2] scatter, out[3] spread, out[4] FFT pass z,
  * out[5] FFT pass y, out[6] FFT pass x + deconvolve, out[7] point records (part of out[3]),
  * out[8] multi-GPU exchange (the collective, or the halo exchange for HPNFFT_DIST_GRID_SLAB),
- * out[9] HPNFFT_DIST_GRID_SLAB pack + all-to-all.
+ * out[9] HPNFFT_DIST_GRID_SLAB pack + all-to-all, out[10] inverse: subdivide + inverse FFT,
+ * out[11] inverse: interpolation.
  * Enabled by hpnfft_enable_timing(p, 1);
  * reading synchronises the stream.  Returns the number of values written (<= n).
  */

@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("HPNFFT_LIB", os.path.join(_HERE, "libhpnfft.so"))
 
 WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
 SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}
-STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records", "exchange", "alltoall")
+STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records", "exchange", "alltoall",
+          "inv_fft", "interp")
 DIST_MODES = {"allreduce": 0, "reduce": 1, "reduce_scatter": 2, "grid_slab": 3}
 
 HPNFFT_OK = 0
@@ -80,6 +81,8 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_stage_times.restype = ctypes.c_int
     lib.hpnfft_version.argtypes = []
     lib.hpnfft_version.restype = ctypes.c_char_p
+    lib.hpnfft_inverse.argtypes = [vp, dp, dp]
+    lib.hpnfft_inverse.restype = ctypes.c_int
     lib.hpnfft_get_unique_id.argtypes = [ctypes.c_char_p]
     lib.hpnfft_get_unique_id.restype = ctypes.c_int
     lib.hpnfft_plan_dist.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
@@ -180,6 +183,22 @@ class Plan:
             raise TypeError(f"out must be a contiguous CUDA complex128 tensor of shape {self.out_shape}")
         self._sync_stream()
         _check(load_library().hpnfft_adjoint(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def inverse(self, fhat, out=None):
+        """Eq. 6 (hpnfft_inverse): f(x_j) = sum_k fhat(k) exp(+2 pi i k.x_j) for the points of the
+        last set_points, in their original order.  fhat: CUDA complex128 of shape N."""
+        import torch
+
+        if not (fhat.is_cuda and fhat.dtype == torch.complex128 and tuple(fhat.shape) == self.N):
+            raise TypeError(f"fhat must be a CUDA complex128 tensor of shape {self.N}")
+        fhat = fhat.contiguous()
+        if out is None:
+            out = torch.empty((self.M,), dtype=torch.complex128, device=fhat.device)
+        elif not (out.is_cuda and out.dtype == torch.complex128 and out.numel() == self.M and out.is_contiguous()):
+            raise TypeError("out must be a contiguous CUDA complex128 tensor with M elements")
+        self._sync_stream()
+        _check(load_library().hpnfft_inverse(self._h, ctypes.c_void_p(fhat.data_ptr()), ctypes.c_void_p(out.data_ptr())))
         return out
 
     def __call__(self, x, f):

@@ -355,6 +355,34 @@ int hpnfft_adjoint(hpnfft_plan_t h, const double* f, double* fhat) {
   return fft_and_deconvolve(p, fhat);
 }
 
+int hpnfft_inverse(hpnfft_plan_t h, const double* fhat, double* f) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (p->failed) {
+    set_error("plan is in a failed state (an earlier CUDA error)");
+    return HPNFFT_E_STATE;
+  }
+  if (!p->points_set) {
+    set_error("hpnfft_inverse called before a successful hpnfft_set_points");
+    return HPNFFT_E_STATE;
+  }
+  if (!fhat || (!f && p->M > 0)) {
+    set_error("fhat or f is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  stage_begin(p, 10);
+  int rc = subdivide_and_ifft(p, fhat);
+  stage_end(p, 10);
+  if (rc) return rc;
+  stage_begin(p, 11);
+  rc = interpolate(p, f);
+  stage_end(p, 11);
+  return rc;
+}
+
 int hpnfft_destroy(hpnfft_plan_t h) {
   free_plan(reinterpret_cast<Plan*>(h));
   return HPNFFT_OK;

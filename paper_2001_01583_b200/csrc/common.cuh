@@ -15,7 +15,7 @@ namespace hpnfft {
 constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
 constexpr int kMinM = 2;
 constexpr int kPolyDeg = 14;      // window tap polynomial degree
-constexpr int kNumStages = 10;     // timing slots, see hpnfft_stage_times
+constexpr int kNumStages = 12;     // timing slots, see hpnfft_stage_times
 constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction
 
 struct Dims3 {
@@ -92,7 +92,7 @@ struct Plan {
   int ev_used = 0;
   std::vector<int> ev_slot;     // stage id of each recorded begin/end pair
   std::vector<int> ev_pair;     // pool index of the pair's begin event
-  int ev_open[kNumStages] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  int ev_open[kNumStages] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   double stage_ms_acc[kNumStages] = {0};
   int stage_calls[kNumStages] = {0};
 };
@@ -123,6 +123,9 @@ int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int
 int dist_adjoint(Plan* p, const double* f, double* fhat);
 void dist_free(Plan* p);
 int spread(Plan* p, const double* f);
+// inverse direction (Eq. 6): fft.cu subdivide + inverse FFT into the grid, interp.cu interpolation
+int subdivide_and_ifft(Plan* p, const double* fhat);
+int interpolate(Plan* p, double* f);
 
 }  // namespace hpnfft
 

@@ -92,6 +92,10 @@ struct LineIO {
   cplx* const* peers;
   int NP;
   int64_t line_o, line_i;
+  // inverse transform (Eq. 6 direction): the line's input is the compact N-entry line of fhat
+  // (index k + N/2 <-> grid frequency k mod n, the other n - N frequencies are 0), scaled by
+  // inv_c on input and conjugated (IFFT(v) = conj(FFT(conj(v)))); all n outputs conjugated
+  bool inv;
 };
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
@@ -126,10 +130,25 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int a = j + r * (n / R);
-      if (IN_G)
-        v[b][r] = (io.valid && ((a - io.a_lo) & (n - 1)) < io.a_len) ? io.gin[(int64_t)a * io.istride]
-                                                                      : cplx{0.0, 0.0};
-      else v[b][r] = buf[slot<LOGN, TI, CONTIG>(a, col)];
+      if (IN_G) {
+        if (io.inv) {
+          const int N = io.N;
+          const bool lo = a < N / 2, hi = a >= n - N / 2;
+          const int k = lo ? a + N / 2 : a - (n - N / 2);
+          if (io.valid && (lo || hi)) {
+            const cplx u = io.gin[(int64_t)k * io.istride];
+            const double sc = io.inv_c[k];
+            v[b][r] = {u.x * sc, -u.y * sc};
+          } else {
+            v[b][r] = {0.0, 0.0};
+          }
+        } else {
+          v[b][r] = (io.valid && ((a - io.a_lo) & (n - 1)) < io.a_len) ? io.gin[(int64_t)a * io.istride]
+                                                                        : cplx{0.0, 0.0};
+        }
+      } else {
+        v[b][r] = buf[slot<LOGN, TI, CONTIG>(a, col)];
+      }
     }
   }
   if (!IN_G) __syncthreads();   // everyone has read the tile before it is overwritten
@@ -158,7 +177,9 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = idxD + r * Ns;   // frequency index on the oversampled grid
-      if (OUT_G) {
+      if (OUT_G && io.inv) {
+        if (io.valid) io.gout[(int64_t)q * io.ostride] = {v[b][r].x, -v[b][r].y};
+      } else if (OUT_G) {
         const int N = io.N;
         const bool lo = q < N / 2, hi = q >= n - N / 2;
         if (io.valid && (lo || hi)) {
@@ -193,7 +214,7 @@ template <int LOGN, int TI, bool CONTIG>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
            const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
-           int a_len, cplx* const* peers, int NP) {
+           int a_len, cplx* const* peers, int NP, int inv) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
   extern __shared__ cplx smem[];
@@ -205,6 +226,7 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
   io.a_len = a_len;
   io.peers = peers;
   io.NP = NP;
+  io.inv = inv != 0;
   int col, tj;
   if (CONTIG) {
     col = tid / T;
@@ -212,9 +234,9 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     const int64_t o = (int64_t)blockIdx.x * TI + col;
     io.valid = o < outer;
     const int64_t oc = io.valid ? (o_start + o) % o_total : 0;
-    io.gin = in + oc * n;
+    io.gin = in + oc * (inv ? (int64_t)N : (int64_t)n);
     io.istride = 1;
-    io.gout = out + oc * (int64_t)N;
+    io.gout = out + oc * (inv ? (int64_t)n : (int64_t)N);
     io.ostride = 1;
   } else {
     col = tid % TI;
@@ -224,9 +246,9 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     const int64_t i = (blockIdx.x % tiles_per_outer) * TI + col;
     io.valid = i < inner;
     const int64_t ic = io.valid ? i : 0;
-    io.gin = in + o * (int64_t)n * inner + ic;
+    io.gin = in + o * (inv ? (int64_t)N : (int64_t)n) * inner + ic;
     io.istride = inner;
-    io.gout = out + o * (int64_t)N * inner + ic;
+    io.gout = out + o * (inv ? (int64_t)n : (int64_t)N) * inner + ic;
     io.ostride = inner;
     io.line_o = o;
     io.line_i = ic;
@@ -251,7 +273,7 @@ constexpr int tile_cols_contig() {
 template <int LOGN>
 static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
                          const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
-                         int a_lo, int a_len, cplx* const* peers, int NP) {
+                         int a_lo, int a_len, cplx* const* peers, int NP, int inv) {
   constexpr int TI = tile_cols<LOGN>();
   constexpr int TC = tile_cols_contig<LOGN>();
   constexpr int n = 1 << LOGN;
@@ -264,7 +286,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
-                                                                            o_start, o_total, a_lo, a_len, nullptr, 1);
+                                                                            o_start, o_total, a_lo, a_len, nullptr, 1, inv);
   } else {
     const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
     const int64_t blocks = outer * ((inner + TI - 1) / TI);
@@ -272,7 +294,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
-                                                     a_len, peers, NP);
+                                                     a_len, peers, NP, inv);
   }
   p->launches++;
   return check_launch(p, "fft pass");
@@ -280,20 +302,20 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
 
 static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t outer, int64_t inner, int N,
                        const double* inv_c, const double* tw, bool contig, int64_t o_start, int64_t o_total,
-                       int a_lo, int a_len, cplx* const* peers = nullptr, int NP = 1) {
+                       int a_lo, int a_len, cplx* const* peers = nullptr, int NP = 1, int inv = 0) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
   cplx* co = reinterpret_cast<cplx*>(out);
   const cplx* ct = reinterpret_cast<const cplx*>(tw);
   switch (logn) {
-    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
-    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP);
+    case 2: return launch_pass_n<2>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 3: return launch_pass_n<3>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 4: return launch_pass_n<4>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 5: return launch_pass_n<5>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 6: return launch_pass_n<6>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 7: return launch_pass_n<7>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 8: return launch_pass_n<8>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 9: return launch_pass_n<9>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
+    case 10: return launch_pass_n<10>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, peers, NP, inv);
     default:
       set_error("FFT length not supported");
       return HPNFFT_E_UNSUPPORTED;
@@ -304,6 +326,23 @@ int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int
              int64_t o_start, int64_t o_total, int a_lo, int a_len, double* const* peers, int NP) {
   return launch_pass(p, p->logn[dim], in, out, outer, inner, (int)p->N[dim], p->inv_c[dim], p->twiddle[dim], contig,
                      o_start, o_total, a_lo, a_len, reinterpret_cast<cplx* const*>(peers), NP);
+}
+
+// Inverse direction (Eq. 6; Subdividing + Inverse FFT of Alg. 5):
+// ghat(k mod n) = fhat(k) / prod c_k on I_N, 0 elsewhere, then g(l) = sum_k ghat(k) e^{+2 pi i k.l/n}.
+// Three input-pruned passes, smallest data first: z (fhat[N0][N1][N2] -> C[N0][N1][n2], grid
+// memory), y (C -> D[N0][n1][n2], bufA), x (D -> g[n0][n1][n2], grid).
+int subdivide_and_ifft(Plan* p, const double* fhat) {
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  const int64_t N0 = p->N[0], N1 = p->N[1];
+  int rc = launch_pass(p, p->logn[2], fhat, p->grid, N0 * N1, 1, (int)p->N[2], p->inv_c[2], p->twiddle[2], true, 0,
+                       N0 * N1, 0, (int)n2, nullptr, 1, 1);
+  if (rc) return rc;
+  rc = launch_pass(p, p->logn[1], p->grid, p->bufA, N0, n2, (int)N1, p->inv_c[1], p->twiddle[1], false, 0, N0, 0,
+                   (int)n1, nullptr, 1, 1);
+  if (rc) return rc;
+  return launch_pass(p, p->logn[0], p->bufA, p->grid, 1, n1 * n2, (int)N0, p->inv_c[0], p->twiddle[0], false, 0, 1,
+                     0, (int)n0, nullptr, 1, 1);
 }
 
 int fft_and_deconvolve(Plan* p, double* fhat) {

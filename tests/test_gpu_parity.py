@@ -316,3 +316,73 @@ def test_multi_gpu_modes_match_single_gpu():
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "tools", "dist_check.py")]
     r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+# ------------------------------------------------------------- inverse direction (Eq. 6) --
+def gpu_inverse(x, fh, N, m=6, sigma=2.0, window="kb"):
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, x.shape[0], m=m, sigma=sigma, window=window, device=dev)
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(x)).to(dev))
+    out = plan.inverse(torch.from_numpy(np.ascontiguousarray(fh)).to(dev)).cpu().numpy()
+    plan.close()
+    return out
+
+
+def _spectrum(N, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal(N) + 1j * rng.standard_normal(N)
+
+
+def test_inverse_config1():
+    """Eq. 6 at config 1: E2 <= 1e-12 vs the CPU inverse NFFT (O2i), <= 1e-9 vs the
+    direct inverse NDFT (O1i)."""
+    N, M = (16, 16, 16), 1000
+    x, fh = inputs.uniform_points(M), _spectrum(N, 1)
+    g = gpu_inverse(x, fh, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N)) <= 1e-12
+    assert oracle.rel_l2_error(g, oracle.ndft_inverse_direct(x, fh, N)) <= 1e-9
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
+def test_inverse_all_cutoffs_ragged(m):
+    N, M = (32, 16, 64), 1777
+    x, fh = inputs.uniform_points(M, seed=40 + m), _spectrum(N, m)
+    g = gpu_inverse(x, fh, N, m=m)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N, m=m)) <= 1e-12
+
+
+def test_inverse_gaussian_clustered_boundary():
+    N, M = (16, 32, 16), 3000
+    x = inputs.clustered_points(M, s=0.02)
+    x[:4] = [[0.5, -0.5, 0.0], [-0.5, 0.5, 0.5], [0.0, 0.0, 0.0], [0.25, -0.125, 0.375]]
+    fh = _spectrum(N, 9)
+    g = gpu_inverse(x, fh, N, window="gaussian")
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N, window=oracle.GAUSSIAN)) <= 1e-12
+
+
+def test_inverse_is_adjoint_of_gpu_adjoint():
+    """<A f, g> = <f, A^H g> with both directions on the GPU (same plan, config-3-like sizes)."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (64, 64, 64), 200000
+    x, f = inputs.uniform_points(M, seed=77), inputs.uniform_values(M, seed=77)
+    g = _spectrum(N, 77)
+    plan = hp.Plan(N, M, device=dev)
+    plan.set_points(torch.from_numpy(x).to(dev))
+    af = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+    ahg = plan.inverse(torch.from_numpy(g).to(dev)).cpu().numpy()
+    plan.close()
+    lhs, rhs = np.vdot(g, af), np.vdot(ahg, f)
+    assert abs(lhs - rhs) / abs(lhs) < 1e-12
+
+
+def test_inverse_config3_sampled():
+    """N = 128^3, M = 1e6: E2 <= 1e-12 vs O2i on all points, <= 1e-9 vs O1i on sampled points."""
+    N, M = (128, 128, 128), 10 ** 6
+    x, fh = inputs.uniform_points(M), _spectrum(N, 5)
+    g = gpu_inverse(x, fh, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N)) <= 1e-12
+    js = np.array([0, 1, 12345, 500000, 999999])
+    ref = oracle.ndft_inverse_direct(x[js], fh, N)
+    assert oracle.rel_l2_error(g[js], ref) <= 1e-9
