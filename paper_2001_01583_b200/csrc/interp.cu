@@ -16,6 +16,8 @@ namespace hpnfft {
 
 namespace {
 
+constexpr int kPointsPerCta = 1024;
+
 template <int M_>
 __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__ g, const double* __restrict__ xs,
                                                       const uint32_t* __restrict__ perm,
@@ -28,8 +30,15 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
   for (int e = threadIdx.x; e < W * PD; e += blockDim.x) poly[e] = poly_g[e];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (k >= M) return;
+  const int nwarps = blockDim.x >> 5;
+  // A CTA walks one run of kPointsPerCta consecutive sorted points (its warps interleaved), so
+  // the footprints it gathers stay close together and are partly served from the SM's L1.
+  // (Measured: persistent grid-stride runs of 64 / 256 points raise the L2 hit rate to 92 % but
+  // run slower, 38.8 / 34.5 ms vs 27.7 ms at config 4: the gather is bound by L1 wavefronts.)
+  {
+  const int64_t k_begin = (int64_t)blockIdx.x * kPointsPerCta;
+  const int64_t k_end = min(M, k_begin + (int64_t)kPointsPerCta);
+  for (int64_t k = k_begin + (threadIdx.x >> 5); k < k_end; k += nwarps) {
   const CellT a0 = cell_of(xs[3 * k], n0), a1 = cell_of(xs[3 * k + 1], n1), a2 = cell_of(xs[3 * k + 2], n2);
   // tap weights: value q = 32 * round + lane is tap q % W of dimension q / W
   auto tap = [&](int q) -> double {
@@ -46,24 +55,40 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
   const int r = lane / W, i2 = lane - r * W;     // r in {0, 1} for the 2W active lanes
   const bool act = lane < 2 * W;
   const int l2 = (a2.c - M_ + 1 + (act ? i2 : 0)) & (n2 - 1);
-  double sr = 0.0, si = 0.0;
+  // this lane's rows i1 = r, r + 2, ...: their w1 and grid row offsets, fetched once per point
+  double w1r[W / 2];
+  int row[W / 2];
+#pragma unroll
+  for (int q = 0; q < W / 2; ++q) {
+    const double wa = weight(W + 2 * q), wb = weight(W + 2 * q + 1);   // all lanes shuffle
+    w1r[q] = r == 0 ? wa : wb;
+    row[q] = ((a1.c - M_ + 1 + 2 * q + r) & (n1 - 1)) * n2 + l2;
+  }
+  double sr = 0.0, si = 0.0, tr = 0.0, ti = 0.0;   // two accumulator pairs: shorter FMA chains
 #pragma unroll 2
   for (int i0 = 0; i0 < W; ++i0) {
     const double w0 = weight(i0);
     const int l0 = (a0.c - M_ + 1 + i0) & (n0 - 1);
     const double2* plane = g + (size_t)l0 * n1 * n2;
+    if (act) {
+      double2 v[W / 2];
 #pragma unroll
-    for (int i1 = 0; i1 < W; i1 += 2) {
-      const double w1a = weight(W + i1), w1b = weight(W + i1 + 1);   // all lanes shuffle
-      const double w01 = w0 * (r == 0 ? w1a : w1b);
-      const int l1 = (a1.c - M_ + 1 + i1 + r) & (n1 - 1);
-      if (act) {
-        const double2 v = __ldg(plane + (size_t)l1 * n2 + l2);
-        sr = fma(w01, v.x, sr);
-        si = fma(w01, v.y, si);
+      for (int q = 0; q < W / 2; ++q) v[q] = __ldg(plane + row[q]);
+#pragma unroll
+      for (int q = 0; q < W / 2; q += 2) {
+        const double wa = w0 * w1r[q];
+        sr = fma(wa, v[q].x, sr);
+        si = fma(wa, v[q].y, si);
+        if (q + 1 < W / 2) {
+          const double wb = w0 * w1r[q + 1];
+          tr = fma(wb, v[q + 1].x, tr);
+          ti = fma(wb, v[q + 1].y, ti);
+        }
       }
     }
   }
+  sr += tr;
+  si += ti;
   // (weight() shuffles: every lane calls it, the idle ones with a dummy index)
   const double w2raw = weight(2 * W + (act ? i2 : 0));
   const double w2 = act ? w2raw : 0.0;
@@ -75,6 +100,8 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
     si += __shfl_xor_sync(0xffffffffu, si, o);
   }
   if (lane == 0) f[perm[k]] = make_double2(sr, si);
+  }
+  }
 }
 
 template <int M_>
@@ -82,7 +109,7 @@ int launch_interp(Plan* p, double* f) {
   const int64_t M = p->M;
   if (M == 0) return HPNFFT_OK;
   constexpr int kWarps = 8;
-  const int64_t blocks = (M + kWarps - 1) / kWarps;
+  const int64_t blocks = (M + kPointsPerCta - 1) / kPointsPerCta;
   k_interpolate<M_><<<(unsigned)blocks, 32 * kWarps, 0, p->stream>>>(
       reinterpret_cast<const double2*>(p->grid), p->xs, p->perm, p->poly, reinterpret_cast<double2*>(f), M,
       (int)p->n[0], (int)p->n[1], (int)p->n[2]);

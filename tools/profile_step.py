@@ -18,6 +18,7 @@ ap.add_argument("--dist", default="uniform")
 ap.add_argument("--method", default="auto")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--timing", action="store_true")
+ap.add_argument("--inverse", action="store_true")
 a = ap.parse_args()
 N, M = CONFIGS[a.config]
 dev = torch.device("cuda", 0)
@@ -31,6 +32,8 @@ for r in range(a.reps):
         plan.enable_timing(True)
     plan.set_points(x)
     out = plan.adjoint(f)
+    if a.inverse:
+        fl = plan.inverse(out)
 torch.cuda.synchronize()
 msg = {"config": a.config, "dist": a.dist, "patch": os.environ.get("HPNFFT_SWEEP_PATCH", "default")}
 if a.timing:
