@@ -51,6 +51,7 @@ M_WINDOW, SIGMA = 6, 2.0
 # fallback rule (bf16 measured x nominal FP64/bf16 ratio = 1653.7 / 56.25 = 29.4) would be lower,
 # so the measured number is the conservative denominator.
 FP64_TC_PEAK_TFLOPS = 36.7
+FP64_FMA_PEAK_TFLOPS = 34.2   # DFMA chains, tools/ubench_fp64.cu (profiles/ubench_fp64.txt)
 
 
 def spread_flops_per_point(m: int) -> float:
@@ -198,9 +199,19 @@ def run_ours(args):
     plan.set_spread_method(args.method)
     out = torch.empty(plan.out_shape, dtype=torch.complex128, device=dev)
 
+    inverse = args.direction == "inverse"
+    if inverse:   # Eq. 6: input the full spectrum, output this rank's points (Alg. 4)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(2006)
+        fhat_in = torch.randn(N, dtype=torch.complex128, device=dev, generator=gen)
+        f_out = torch.empty(M_local, dtype=torch.complex128, device=dev)
+
     def step():
         plan.set_points(x)
-        plan.adjoint(f, out=out)
+        if inverse:
+            plan.inverse(fhat_in, out=f_out)
+        else:
+            plan.adjoint(f, out=out)
 
     for _ in range(args.warmup):
         step()
@@ -238,6 +249,9 @@ def run_ours(args):
     value = M_total / (ms_per_step * 1e-3)
 
     # ---- e2e: the public API with HOST buffers (pinned), H2D + transform + D2H each step ----
+    if inverse:
+        return _finish_inverse(args, plan, stages, ms_per_step, value, ws, rank, launches_per_step, clocks, N,
+                               M_total, M_local)
     xh = x.cpu().pin_memory()
     fh = f.cpu().pin_memory()
     oh = [torch.empty(plan.out_shape, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
@@ -357,6 +371,41 @@ def run_ours(args):
         tdist.destroy_process_group()
 
 
+def _finish_inverse(args, plan, stages, ms_per_step, value, ws, rank, launches_per_step, clocks, N, M_total, M_local):
+    """JSON line of the inverse direction (Eq. 6; SURVEY.md §8(f) NEXT #1), a separate run."""
+    import torch.distributed as tdist
+
+    fl = M_local * 2.0 * (2 * M_WINDOW) ** 3 * 2.0          # 2 (2m)^3 FMA per point
+    t_interp = stages.get("interp", 0.0)
+    achieved = fl / (t_interp * 1e-3) / 1e12 if t_interp else None
+    if rank == 0:
+        line = {
+            "metric": "inverse NFFT (Eq. 6) nonuniform points/s at N=256³ float64",
+            "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": f"synthetic seeded {args.dist} points (inputs/), seeded random spectrum",
+            "config": {"workload": f"config {args.config} inverse direction: d=3, N={N[0]}^3, M={M_total}, "
+                                   f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}",
+                       "step": "set_points + inverse (subdivide + inverse FFT + interpolation); f left on the "
+                               "rank that owns the point"},
+            "e2e": None,
+            "gpu_launches": int(launches_per_step * args.steps),
+            "roofline": {"kernel": "k_interpolate", "bound": "alu", "achieved": achieved,
+                         "peak": FP64_FMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_FMA_PEAK_TFLOPS if achieved else None, "traffic": None,
+                         "peak_source": "measured DFMA chain 34.2 TFLOP/s (tools/ubench_fp64.cu)",
+                         "note": "first version: a per-point L1 gather, bound by L1 wavefronts (ncu)"},
+            "cpu_baseline": None,
+            "clocks": clocks,
+            "detail": {"stages_ms": {k: round(v, 4) for k, v in stages.items()}, "M_local": M_local},
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- CPU oracle --
 def _oracle_timing(cfg, dist_kind, sample_points, fft_once=True):
     """Time the CPU oracle (oracle.nfft_adjoint's steps, unmodified) on a bounded sample:
@@ -448,6 +497,8 @@ def main():
     ap.add_argument("--method", default="auto", choices=["auto", "atomic", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", default="equal_size", choices=["equal_size", "equal_count"])
+    ap.add_argument("--direction", default="adjoint", choices=["adjoint", "inverse"],
+                    help="adjoint = Eq. 5 (the BASELINE metric); inverse = Eq. 6 (NEXT #1)")
     ap.add_argument("--exchange", default="grid_slab", choices=["allreduce", "reduce", "reduce_scatter", "grid_slab"],
                     help="multi-GPU exchange (SURVEY.md §8(e)); grid_slab = option G")
     args = ap.parse_args()

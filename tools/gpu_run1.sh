@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct,lts__t_bytes.sum,l1tex__t_bytes.sum,dram__bytes_read.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,l1tex__throughput.avg.pct_of_peak_sustained_active,lts__throughput.avg.pct_of_peak_sustained_active,smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio --clock-control none -k regex:k_interpolate -c 1 python tools/profile_step.py --config 4 --reps 1 --inverse 2>&1 | grep -E "k_interpolate|duration|hit_rate|bytes|active|throughput|scoreboard" | head -20
+timeout 600 python bench.py --steps 5 --warmup 3 --direction inverse 2>&1 | tail -1 | cut -c1-900
