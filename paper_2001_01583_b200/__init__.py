@@ -257,32 +257,33 @@ class HostPipeline:
 
     submit(x_host, f_host, out_host) enqueues one transform: the H2D copies of x and f on a copy
     stream, set_points + adjoint on the compute stream, the D2H copy of fhat on a second copy
-    stream, with two device buffer sets so that the copies of one transform overlap the
-    kernels of its neighbours (PCIe in both directions and the GPU busy at the same time).
+    stream, with `depth` (default two) device buffer sets so that the copies of one transform
+    overlap the kernels of its neighbours (PCIe in both directions and the GPU busy at once).
     out_host is complete after flush() (or after the next-but-one submit).  Every submitted
     transform still moves all of its own inputs and its result across PCIe.
     """
 
-    def __init__(self, plan: "Plan", M: int):
+    def __init__(self, plan: "Plan", M: int, depth: int = 2):
         import torch
 
         self.plan = plan
         dev = plan.device
+        self.depth = depth
         self.h2d = torch.cuda.Stream(device=dev)
         self.d2h = torch.cuda.Stream(device=dev)
         self.compute = torch.cuda.current_stream(dev)
-        self.x = [torch.empty((M, 3), dtype=torch.float64, device=dev) for _ in range(2)]
-        self.f = [torch.empty((M,), dtype=torch.complex128, device=dev) for _ in range(2)]
-        self.o = [torch.empty(plan.out_shape, dtype=torch.complex128, device=dev) for _ in range(2)]
-        self.in_ready = [torch.cuda.Event() for _ in range(2)]
-        self.used = [None, None]      # compute finished reading buffer set s
-        self.drained = [None, None]   # D2H finished reading output buffer s
+        self.x = [torch.empty((M, 3), dtype=torch.float64, device=dev) for _ in range(depth)]
+        self.f = [torch.empty((M,), dtype=torch.complex128, device=dev) for _ in range(depth)]
+        self.o = [torch.empty(plan.out_shape, dtype=torch.complex128, device=dev) for _ in range(depth)]
+        self.in_ready = [torch.cuda.Event() for _ in range(depth)]
+        self.used = [None] * depth      # compute finished reading buffer set s
+        self.drained = [None] * depth   # D2H finished reading output buffer s
         self.i = 0
 
     def submit(self, x_host, f_host, out_host):
         import torch
 
-        s = self.i & 1
+        s = self.i % self.depth
         with torch.cuda.stream(self.h2d):
             if self.used[s] is not None:
                 self.h2d.wait_event(self.used[s])
