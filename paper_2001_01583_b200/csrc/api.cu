@@ -378,7 +378,11 @@ int hpnfft_inverse(hpnfft_plan_t h, const double* fhat, double* f) {
   stage_end(p, 10);
   if (rc) return rc;
   stage_begin(p, 11);
-  rc = interpolate(p, f);
+  // the tensor-core gather sweep when the grid allows it (HPNFFT_INTERP=warp forces the
+  // warp-per-point gather of interp.cu)
+  static const bool force_warp = getenv("HPNFFT_INTERP") && getenv("HPNFFT_INTERP")[0] == 'w';
+  const bool sweep = !force_warp && p->spread_method != HPNFFT_SPREAD_ATOMIC && sweep_supported(p);
+  rc = sweep ? interp_sweep(p, f) : interpolate(p, f);
   stage_end(p, 11);
   return rc;
 }

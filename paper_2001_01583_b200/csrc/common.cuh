@@ -126,6 +126,7 @@ int spread(Plan* p, const double* f);
 // inverse direction (Eq. 6): fft.cu subdivide + inverse FFT into the grid, interp.cu interpolation
 int subdivide_and_ifft(Plan* p, const double* fhat);
 int interpolate(Plan* p, double* f);
+int interp_sweep(Plan* p, double* f);   // the DMMA gather sweep (spread_sweep.cu)
 
 }  // namespace hpnfft
 

@@ -52,7 +52,7 @@ constexpr bool kProf = HPNFFT_SWEEP_PROFILE != 0;
 #endif
 
 // record layout in doubles (HBM and shared memory):
-//   [0] c1|c2 (int2)  [1] c0|0 (int2)  [2..3] f
+//   [0] c1|c2 (int2)  [1] c0|perm (int2: cell plane, original point index)  [2..3] f
 //   [4 .. 20) w0 (zero padded to 16: the DMMA A operand indexes it modulo 16)
 //   [20 .. 21+W) w1 (+ zero pad)  [21+W .. 22+2W) w2 (+ zero pad)
 template <int W>
@@ -114,6 +114,7 @@ struct SweepParams {
   int cap;                 // record capacity of one shared-memory ring stage
   int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
   unsigned long long* prof;   // optional clock64 phase counters (HPNFFT_SWEEP_PROF=1), else null
+  double* fout;            // inverse direction: f [M][2] in original point order (atomically summed)
 };
 
 }  // namespace
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
   double x0 = 0.0, x1 = 0.0, x2 = 0.0;
   if (k < count) {
     const size_t src = (size_t)g0 + k;
-    fv = __ldg(reinterpret_cast<const double2*>(f) + __ldg(perm + src));
+    if (f) fv = __ldg(reinterpret_cast<const double2*>(f) + __ldg(perm + src));   // null: inverse
     x0 = __ldg(xs + 3 * src);
     x1 = __ldg(xs + 3 * src + 1);
     x2 = __ldg(xs + 3 * src + 2);
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
   for (int i = W; i < 16; ++i) out[R::kW0 + i] = 0.0;
   out[R::kW1 + W] = 0.0;
   out[R::kW2 + W] = 0.0;
-  reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, a0.c, 0);
+  reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, a0.c, (int)(k < count ? perm[(size_t)g0 + k] : 0u));
   reinterpret_cast<double2*>(out)[1] = fv;
   __syncthreads();
   const uint32_t npts = min((uint32_t)kRecPts, count - kb);
@@ -273,7 +274,7 @@ __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
 
 // ------------------------------------------------------------------------------------------
 // A4: the warp-specialised persistent sweep (see the file header).
-template <int P1, int P2, int M_>
+template <int P1, int P2, int M_, bool INV>
 __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((SweepCfg<P1, P2, M_>::kMaxRegs))
     k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
@@ -510,6 +511,136 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         atomicAdd(prm.prof + 10, clock64() - l1c);
       }
       if (hdr.B < 0) break;
+    }
+    return;
+  }
+
+  if constexpr (INV) {
+    // ======================= consumer warps, inverse direction (gather) =======================
+    // Interpolating step of the inverse CUNFFT: f_j = sum_l g(l) w0 w1 w2.  A warp
+    // holds the grid values of its 4 x 4 column sub-patch for the 16 cyclic node rows around the
+    // current chunk as the A operand of DMMA m16n8k4 (A[node][col], rows g and g + 8, column t
+    // of slice s = sub-patch row s), loaded once per node.  Per k-step of 8 records (N = record):
+    //   H[node][record] = sum_{s, t} G[node][(s, t)] * (w1[i1(s)] w2[i2(t)])[record]   (4 DMMA, re and im)
+    //   partial_j = sum_node w0_j[node] H[node][j]   (lane products + shuffle reduction)
+    // and the partials of a point from the warps (and CTAs) its footprint spans are summed with
+    // global atomics (native f64 RED in L2).  Nodes outside the tile's segment read as 0, so
+    // every (point, node) pair is gathered exactly once, mirroring the adjoint's flush.
+    static_assert(C::SUB == 1, "inverse consumer: one sub-patch per warp");
+    constexpr int NT = kWR * kWC / 4;   // slices (sub-patch rows), 4 columns each
+    const int wr_off = (warp / (P2 / kWC)) * kWR;
+    const int wc_off = (warp % (P2 / kWC)) * kWC;
+    const int g = lane >> 2, t = lane & 3;
+    int cur_tile = -1;
+    int first = 0, off = 0, S = 0, wr0 = 0, wc0 = 0;
+    double gre[NT][2], gim[NT][2];
+    int ld = 0;                         // relative nodes < ld are loaded
+    const size_t plane = (size_t)n1 * n2;
+    auto load_nodes = [&](int upto) {   // load relative nodes [ld, upto]
+      for (; ld <= upto; ++ld) {
+        const int row = ld & 15;
+        if (g == (row & 7)) {
+          const int rel = ld - off;     // node - L0
+          const bool in = rel >= 0 && rel < S;
+          const int l0 = (first + ld) & (n0 - 1);
+          const double2* base = reinterpret_cast<const double2*>(prm.grid) + (size_t)l0 * plane +
+                                (size_t)wr0 * n2 + (wc0 + t);
+#pragma unroll
+          for (int sl = 0; sl < NT; ++sl) {
+            double2 v = make_double2(0.0, 0.0);
+            if (in && wr0 + sl < n1) v = __ldg(base + (size_t)sl * n2);
+            if (row < 8) {
+              gre[sl][0] = v.x;
+              gim[sl][0] = v.y;
+            } else {
+              gre[sl][1] = v.x;
+              gim[sl][1] = v.y;
+            }
+          }
+        }
+      }
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(s_zero);
+    for (;;) {
+      mbar_wait(&s_full[stage], phase);
+      const BatchHdr hdr = s_hdr[stage];
+      if (hdr.B < 0) break;
+      if (hdr.tile != cur_tile) {
+        cur_tile = hdr.tile;
+        int R0, C0, L0, a_lo, nch;
+        tile_geom(cur_tile, R0, C0, L0, S, a_lo, nch);
+        first = a_lo * CH;
+        off = L0 - first;
+        wr0 = R0 + wr_off;
+        wc0 = C0 + wc_off;
+        ld = -M_ + 1;
+#pragma unroll
+        for (int sl = 0; sl < NT; ++sl) gre[sl][0] = gre[sl][1] = gim[sl][0] = gim[sl][1] = 0.0;
+      }
+      const int step0 = hdr.chunk * CH;
+      if (hdr.B > 0) load_nodes(step0 + CH - 1 + M_);   // the chunk's cells reach these nodes
+      const double* recs = s_rec + (size_t)stage * cap * RD;
+      const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(recs);
+      const int nlist = (int)s_cnt[stage * NL + warp];
+      const uint32_t* my = s_list + ((size_t)stage * NL + warp) * cap;
+      for (int k = 0; k < nlist; k += 8) {
+        // B: lane (g, t) = record k + g, column t of every slice
+        const bool act = k + g < nlist;
+        const uint32_t en = act ? my[k + g] : 0u;
+        const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
+        const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
+        const double w2v = lds_f64(ra + 8u * (uint32_t)(R::kW2 + min((unsigned)(d2 - (kWC - 1) + t), (unsigned)W)));
+        double hre[4] = {0.0, 0.0, 0.0, 0.0}, him[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int sl = 0; sl < NT; ++sl) {
+          const double b =
+              w2v * lds_f64(ra + 8u * (uint32_t)(R::kW1 + min((unsigned)(d1 - (kWR - 1) + sl), (unsigned)W)));
+          dmma16(hre, gre[sl][0], gre[sl][1], b);
+          dmma16(him, gim[sl][0], gim[sl][1], b);
+        }
+        // lane holds H[g][2t], H[g][2t+1], H[g+8][2t], H[g+8][2t+1] (re and im)
+        double pr[2], pi[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = 2 * t + q;      // record of this column pair
+          const uint32_t enr = __shfl_sync(0xffffffffu, en, 4 * r);
+          const bool actr = k + r < nlist;
+          const uint32_t rar = actr ? rbase + (enr & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
+          const int sh = step0 + (int)((enr >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
+          const double wa = lds_f64(rar + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
+          const double wb = lds_f64(rar + 8u * (uint32_t)(R::kW0 + ((8 + g - sh) & 15)));
+          pr[q] = wa * hre[q] + wb * hre[2 + q];
+          pi[q] = wa * him[q] + wb * him[2 + q];
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {   // sum over g (lanes with the same t)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            pr[q] += __shfl_xor_sync(0xffffffffu, pr[q], o);
+            pi[q] += __shfl_xor_sync(0xffffffffu, pi[q], o);
+          }
+        }
+        if (g == 0) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int r = 2 * t + q;
+            if (k + r < nlist) {
+              const uint32_t enr = my[k + r];
+              const int pj = reinterpret_cast<const int*>(recs + (size_t)(enr & 0x1ffu) * RD)[3];
+              atomicAdd(prm.fout + 2 * (size_t)pj, pr[q]);
+              atomicAdd(prm.fout + 2 * (size_t)pj + 1, pi[q]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[stage]);
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1u;
+      }
     }
     return;
   }
@@ -794,8 +925,8 @@ int sweep_variant() {
   return v;
 }
 
-template <int P1, int P2, int M_>
-int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, bool accumulate) {
+template <int P1, int P2, int M_, bool INV = false>
+int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, bool accumulate, double* fout = nullptr) {
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
   const size_t smem_max = C::kCtasPerSm == 1 ? (size_t)(227 * 1024) : (size_t)(113 * 1024);
@@ -826,6 +957,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   prm.nseg = (int)((len_al + prm.seg - 1) / prm.seg);
   prm.cap = cap;
   prm.tile_counter = p->tile_counter;
+  prm.fout = fout;
   static const bool prof_on = getenv("HPNFFT_SWEEP_PROF") != nullptr;
   unsigned long long* prof = nullptr;
   if (prof_on) {
@@ -834,7 +966,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   }
   prm.prof = prof;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
-  auto kern = k_spread_sweep<P1, P2, M_>;
+  auto kern = k_spread_sweep<P1, P2, M_, INV>;
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                   "sweep smem attr");
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
@@ -903,6 +1035,40 @@ int run_sweep(Plan* p, const double* f) {
   return HPNFFT_OK;
 }
 
+// inverse direction: records (no f) + the gather sweep, f summed atomically in original order
+template <int M_>
+int run_interp_sweep(Plan* p, double* fout) {
+  const uint32_t M = (uint32_t)p->M;
+  const uint32_t G = (uint32_t)p->rec_group;
+  const bool multi = M > G;
+  HPNFFT_CUDA_TRY(p, cudaMemsetAsync(fout, 0, sizeof(double) * 2 * (size_t)M, p->stream), "zero f");
+  uint32_t g0 = 0;
+  do {
+    const uint32_t g1 = (M - g0) < G ? M : g0 + G;
+    const uint32_t cnt = g1 - g0;
+    if (cnt > 0) {
+      const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
+      HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_point_records<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)rsmem),
+                      "records smem attr");
+      k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
+          p->xs, p->perm, nullptr, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
+      p->launches++;
+      int rc = check_launch(p, "point records");
+      if (rc) return rc;
+    }
+    if (multi) {
+      const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1] * Chunk<M_>::CH;
+      k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, p->nbins, g0, g1, bins_per_chunk, p->group_rows);
+      p->launches++;
+    }
+    const int rc = launch_sweep_group<8, 32, M_, true>(p, g0, g1, p->group_rows, multi, fout);
+    if (rc) return rc;
+    g0 = g1;
+  } while (g0 < M);
+  return HPNFFT_OK;
+}
+
 }  // namespace
 
 size_t record_bytes(int m) { return sizeof(double) * (22 + 4 * m); }
@@ -917,6 +1083,21 @@ bool sweep_supported(const Plan* p) {
   if (p->n[0] < 16 || p->n[0] < 2 * W) return false;
   if (p->rec == nullptr || p->rec_group == 0) return false;
   return true;
+}
+
+int interp_sweep(Plan* p, double* f) {
+  switch (p->m) {
+    case 2: return run_interp_sweep<2>(p, f);
+    case 3: return run_interp_sweep<3>(p, f);
+    case 4: return run_interp_sweep<4>(p, f);
+    case 5: return run_interp_sweep<5>(p, f);
+    case 6: return run_interp_sweep<6>(p, f);
+    case 7: return run_interp_sweep<7>(p, f);
+    case 8: return run_interp_sweep<8>(p, f);
+    default:
+      set_error("m not supported by the sweep kernel");
+      return HPNFFT_E_UNSUPPORTED;
+  }
 }
 
 int spread_sweep(Plan* p, const double* f) {

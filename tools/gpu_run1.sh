@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c5_n1.json 2> gpurun_out/c5_n1.err; tail -c 1800 gpurun_out/c5_n1.json; tail -3 gpurun_out/c5_n1.err
-timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -c 400
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "inverse" 2>&1 | tail -3
+timeout 120 python tools/profile_step.py --config 4 --timing --reps 3 --inverse 2>&1 | tail -1 | grep -o "'inv_fft': [0-9.]*\|'interp': [0-9.]*"
