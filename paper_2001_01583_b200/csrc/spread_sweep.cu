@@ -536,28 +536,40 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     double gre[NT][2], gim[NT][2];
     int ld = 0;                         // relative nodes < ld are loaded
     const size_t plane = (size_t)n1 * n2;
-    auto load_nodes = [&](int upto) {   // load relative nodes [ld, upto]
-      for (; ld <= upto; ++ld) {
-        const int row = ld & 15;
-        if (g == (row & 7)) {
-          const int rel = ld - off;     // node - L0
-          const bool in = rel >= 0 && rel < S;
-          const int l0 = (first + ld) & (n0 - 1);
+    // load relative nodes [ld, upto] into their cyclic rows (node & 15): in blocks of <= 16
+    // nodes, each lane fetches the (at most two) nodes of its rows g and g + 8 with all their
+    // global loads in flight before any register is written
+    auto load_nodes = [&](int upto) {
+      while (ld <= upto) {
+        const int nb = min(16, upto - ld + 1);
+        const int row0 = ld & 15;
+        double2 v[2][NT];
+        bool has[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ds = (g + 8 * h - row0) & 15;   // offset of this lane's row h in the block
+          has[h] = ds < nb;
+          const int node = ld + ds;
+          const int rel = node - off;                // node - L0
+          const bool in = has[h] && rel >= 0 && rel < S;
+          const int l0 = (first + node) & (n0 - 1);
           const double2* base = reinterpret_cast<const double2*>(prm.grid) + (size_t)l0 * plane +
                                 (size_t)wr0 * n2 + (wc0 + t);
 #pragma unroll
-          for (int sl = 0; sl < NT; ++sl) {
-            double2 v = make_double2(0.0, 0.0);
-            if (in && wr0 + sl < n1) v = __ldg(base + (size_t)sl * n2);
-            if (row < 8) {
-              gre[sl][0] = v.x;
-              gim[sl][0] = v.y;
-            } else {
-              gre[sl][1] = v.x;
-              gim[sl][1] = v.y;
+          for (int sl = 0; sl < NT; ++sl)
+            v[h][sl] = (in && wr0 + sl < n1) ? __ldg(base + (size_t)sl * n2) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (has[h]) {
+#pragma unroll
+            for (int sl = 0; sl < NT; ++sl) {
+              gre[sl][h] = v[h][sl].x;
+              gim[sl][h] = v[h][sl].y;
             }
           }
         }
+        ld += nb;
       }
     };
     int stage = 0;
