@@ -395,11 +395,12 @@ def _finish_inverse(args, plan, stages, ms_per_step, value, ws, rank, launches_p
                                "rank that owns the point"},
             "e2e": None,
             "gpu_launches": int(launches_per_step * args.steps),
-            "roofline": {"kernel": "k_interpolate", "bound": "alu", "achieved": achieved,
-                         "peak": FP64_FMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_FMA_PEAK_TFLOPS if achieved else None, "traffic": None,
-                         "peak_source": "measured DFMA chain 34.2 TFLOP/s (tools/ubench_fp64.cu)",
-                         "note": "first version: a per-point L1 gather, bound by L1 wavefronts (ncu)"},
+            "roofline": {"kernel": "k_spread_sweep<INV> (DMMA gather sweep)", "bound": "tensor", "achieved": achieved,
+                         "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_TC_PEAK_TFLOPS if achieved else None, "traffic": None,
+                         "peak_source": "measured FP64 DMMA m8n8k4 (tools/ubench_dmma.cu, profiles/ubench_dmma.txt)",
+                         "algorithmic": "2 (2m)^3 FMA per point",
+                         "timed_as": "interp stage (point records + gather sweep), CUDA events on the plan stream"},
             "cpu_baseline": None,
             "clocks": clocks,
             "detail": {"stages_ms": {k: round(v, 4) for k, v in stages.items()}, "M_local": M_local},
