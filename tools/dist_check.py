@@ -65,6 +65,22 @@ def main():
                   f"E2(dist vs 1-GPU)={e:.2e} E2(vs NDFT, sampled)={e2:.2e}", flush=True)
             ok &= e <= 1e-13 and e2 <= 1e-9
             ref_plan.close()
+        # inverse direction (Eq. 6, Alg. 4): every rank takes the full fhat and
+        # interpolates its own points; compare with the single-GPU inverse on the same points
+        if mode in ("allreduce", "grid_slab"):
+            full = out if mode == "allreduce" else out   # gathered above for grid_slab
+            fl_inv = dp.plan.inverse(full.contiguous())
+            ref1 = hp.Plan(N, xl.shape[0], device=dev)
+            ref1.set_points(xl)
+            fl_ref = ref1.inverse(full.contiguous())
+            ref1.close()
+            ei = float((fl_inv - fl_ref).abs().pow(2).sum().sqrt() / fl_ref.abs().pow(2).sum().sqrt())
+            flag_i = torch.tensor([1 if ei <= 1e-13 else 0], device=dev)
+            dist.all_reduce(flag_i, op=dist.ReduceOp.MIN)
+            if rank == 0:
+                print(f"[{dist_kind}/{part}/{mode}] inverse on the rank's points: E2(dist plan vs 1-GPU plan)="
+                      f"{ei:.2e} (all ranks ok: {bool(flag_i.item())})", flush=True)
+                ok &= bool(flag_i.item())
         dp.close()
         dist.barrier()
     flag = torch.tensor([1 if ok else 0], device=dev)
