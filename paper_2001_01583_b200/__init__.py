@@ -278,7 +278,24 @@ class HostPipeline:
         self.in_ready = [torch.cuda.Event() for _ in range(depth)]
         self.used = [None] * depth      # compute finished reading buffer set s
         self.drained = [None] * depth   # D2H finished reading output buffer s
+        self.pending = None             # D2H of the previous transform, enqueued after the next H2D
         self.i = 0
+
+    def _drain_pending(self):
+        # enqueued after the next transform's H2D: a D2H that waits for its kernels must not sit
+        # in front of that H2D in a shared hardware queue
+        import torch
+
+        if self.pending is None:
+            return
+        s, out_host, done = self.pending
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(done)
+            out_host.copy_(self.o[s], non_blocking=True)
+            drained = torch.cuda.Event()
+            drained.record(self.d2h)
+        self.drained[s] = drained
+        self.pending = None
 
     def submit(self, x_host, f_host, out_host):
         import torch
@@ -288,27 +305,27 @@ class HostPipeline:
             if self.used[s] is not None:
                 self.h2d.wait_event(self.used[s])
             self.x[s].copy_(x_host, non_blocking=True)
-            self.f[s].copy_(f_host, non_blocking=True)
             self.in_ready[s].record(self.h2d)
+            self.f[s].copy_(f_host, non_blocking=True)
+            f_ready = torch.cuda.Event()
+            f_ready.record(self.h2d)
+        self._drain_pending()
         self.compute.wait_event(self.in_ready[s])
         if self.drained[s] is not None:
             self.compute.wait_event(self.drained[s])
         with torch.cuda.stream(self.compute):
-            self.plan.set_points(self.x[s])
+            self.plan.set_points(self.x[s])          # needs x only: f is still copying
+            self.compute.wait_event(f_ready)
             self.plan.adjoint(self.f[s], out=self.o[s])
             done = torch.cuda.Event()
             done.record(self.compute)
         self.used[s] = done
-        with torch.cuda.stream(self.d2h):
-            self.d2h.wait_event(done)
-            out_host.copy_(self.o[s], non_blocking=True)
-            drained = torch.cuda.Event()
-            drained.record(self.d2h)
-        self.drained[s] = drained
+        self.pending = (s, out_host, done)
         self.i += 1
         return out_host
 
     def flush(self):
+        self._drain_pending()
         self.h2d.synchronize()
         self.compute.synchronize()
         self.d2h.synchronize()

@@ -55,6 +55,15 @@ void stage_end(Plan* p, int slot) {
 
 int64_t scan_workspace_elems(int64_t nbins);
 
+// set_points read-back: device flags (+ the multi-GPU barrier error) -> mapped host memory
+__global__ void k_flags_to_host(const int* __restrict__ flags, int n, const int* __restrict__ dist_err,
+                                volatile int* host) {
+  const int t = threadIdx.x;
+  if (t < n) host[t] = flags[t];
+  if (t == n) host[t] = dist_err ? *dist_err : 0;
+  __threadfence_system();
+}
+
 // A3 + A4: the sweep when the grid allows it, else the generic atomic kernel (timing slot 3)
 int spread(Plan* p, const double* f) {
   if (p->spread_method == HPNFFT_SPREAD_SWEEP && !sweep_supported(p)) {
@@ -219,7 +228,10 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   rc = rc ? rc : alloc(p, reinterpret_cast<uint32_t**>(&p->scan_tmp), (size_t)p->scan_tmp_elems);
   rc = rc ? rc : alloc(p, &p->err_flag, 1 + 2 * kRangeSlots);
   if (!rc) {
-    cudaError_t e = cudaMallocHost(&p->err_flag_host, (1 + 2 * kRangeSlots) * sizeof(int));
+    // mapped pinned memory: a kernel writes the flags straight into it, so the read-back at the
+    // end of set_points needs no copy engine (a memcpy would queue behind a caller's large D2H)
+    cudaError_t e = cudaHostAlloc(&p->err_flag_host, (2 + 2 * kRangeSlots) * sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->err_flag_host_dev), p->err_flag_host, 0);
     if (e != cudaSuccess) {
       set_error("pinned allocation failed");
       rc = HPNFFT_E_NOMEM;
@@ -284,9 +296,11 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   p->launches = 0;
   int rc = sort_points(p, x);
   if (rc) return rc;
-  HPNFFT_CUDA_TRY(p, cudaMemcpyAsync(p->err_flag_host, p->err_flag, (1 + 2 * kRangeSlots) * sizeof(int),
-                                     cudaMemcpyDeviceToHost, p->stream),
-                  "flag d2h");
+  k_flags_to_host<<<1, 2 + 2 * kRangeSlots, 0, p->stream>>>(p->err_flag, 1 + 2 * kRangeSlots, p->dist_err,
+                                                             p->err_flag_host_dev);
+  p->launches++;
+  rc = check_launch(p, "flag read-back");
+  if (rc) return rc;
   HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
   if (p->err_flag_host[0] == 1) {
     set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
@@ -296,10 +310,8 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
     set_error("a point lies outside this rank's grid slab (HPNFFT_DIST_GRID_SLAB)");
     return HPNFFT_E_RANGE;
   }
-  if (p->dist_err) {   // a cross-GPU barrier of an earlier grid-slab transform timed out
-    int e = 0;
-    cudaMemcpy(&e, p->dist_err, sizeof(int), cudaMemcpyDeviceToHost);
-    if (e) return fail(p, HPNFFT_E_NCCL, "a cross-GPU barrier timed out (peer rank missing)");
+  if (p->err_flag_host[1 + 2 * kRangeSlots]) {   // a cross-GPU barrier of an earlier grid-slab transform timed out
+    return fail(p, HPNFFT_E_NCCL, "a cross-GPU barrier timed out (peer rank missing)");
   }
   // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
   {

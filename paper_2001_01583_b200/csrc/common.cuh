@@ -60,7 +60,8 @@ struct Plan {
   int* tile_counter = nullptr;    // sweep tile scheduler counter
   int* err_flag = nullptr;        // device [1 + 2 kRangeSlots]: range-error flag, then slot pairs of
                                   // min / max of the x-ordered cell c0
-  int* err_flag_host = nullptr;   // pinned mirror
+  int* err_flag_host = nullptr;   // mapped pinned mirror [1 + 2 kRangeSlots + 1 (dist barrier error)]
+  int* err_flag_host_dev = nullptr;   // its device alias
   // occupied l0 planes (circular interval [plane_lo, plane_lo + plane_len) mod n0): planes that
   // receive any tap of the current points.  Planes outside are zero and are skipped by the sweep
   // and the first two FFT passes (x-slab subcells of the multi-GPU layer).
