@@ -288,7 +288,8 @@ def test_stage_timing_and_launch_count():
     plan.enable_timing(True)
     for _ in range(3):
         plan.set_points(xd)
-        plan.adjoint(fd)
+        fh = plan.adjoint(fd)
+        plan.inverse(fh)
     t = plan.stage_times()
     assert set(t) == set(hp.STAGES)
     assert all(v > 0 for k, v in t.items() if k not in ("exchange", "alltoall"))
