@@ -400,3 +400,41 @@ def test_inverse_sweep_and_warp_gathers(method, dist):
     fh = _spectrum(N, 88)
     g = gpu_inverse(x, fh, N, method=method)
     assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("dist", ["uniform", "clustered"])
+def test_inverse_multi_group(dist, monkeypatch):
+    """Inverse gather sweep over several record groups: f is summed across groups."""
+    monkeypatch.setenv("HPNFFT_REC_GROUP", "4096")
+    N, M = (32, 32, 64), 30011
+    x = inputs.uniform_points(M, seed=14) if dist == "uniform" else inputs.clustered_points(M, s=0.02, seed=14)
+    fh = _spectrum(N, 14)
+    g = gpu_inverse(x, fh, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("lo,hi", [(-0.5, -0.375), (-0.1, 0.1), (0.49, 0.5)])
+def test_inverse_thin_slabs(lo, hi):
+    """Points in a thin x0 slab: the gather sweep only visits the occupied planes."""
+    N, M = (64, 32, 64), 20000
+    x = inputs.uniform_points(M, seed=16)
+    x[:, 0] = lo + (hi - lo) * (x[:, 0] + 0.5)
+    fh = _spectrum(N, 16)
+    g = gpu_inverse(x, fh, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(x, fh, N)) <= 1e-12
+
+
+def test_inverse_empty_and_tiny():
+    """M = 0 leaves f empty; M = 1 at the origin gives sum_k fhat(k) (up to the NFFT error)."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N = (16, 16, 16)
+    fh = _spectrum(N, 3)
+    plan = hp.Plan(N, 0, device=dev)
+    plan.set_points(torch.zeros((0, 3), dtype=torch.float64, device=dev))
+    out = plan.inverse(torch.from_numpy(fh).to(dev))
+    assert out.numel() == 0
+    plan.close()
+    g = gpu_inverse(np.zeros((1, 3)), fh, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_inverse(np.zeros((1, 3)), fh, N)) <= 1e-12
+    assert abs(g[0] - fh.sum()) <= 1e-9 * np.abs(fh).sum()   # Eq. 6 at x = 0, within the NFFT error

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "inverse" 2>&1 | tail -5
