@@ -156,16 +156,18 @@ def make_inputs(cfg, dist_kind, device):
 def slab_select(x, f, rank, ws, partition="equal_size", exchange="allreduce", n0=512):
     """This rank's x-slab subcell: equal-size slabs, equal-count slabs, or the
     cell-aligned equal-size slabs of the grid_slab exchange (option G)."""
-    from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_mask, slab_mask
+    from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_edges, grid_slab_mask, slab_mask
 
     if ws == 1:
-        return x, f
+        return x, f, None
+    edges = None
     if exchange == "grid_slab":
-        mask = grid_slab_mask(x, rank, ws, n0)
+        # every rank holds the same full point set here: no histogram reduction needed
+        edges = grid_slab_edges(x, ws, n0, m=M_WINDOW, reduce=False) if partition == "equal_count" else None
+        mask = grid_slab_mask(x, rank, ws, n0, edges)
     else:
-        edges = equal_count_edges(x, ws) if partition == "equal_count" else None
-        mask = slab_mask(x, rank, ws, edges)
-    return x[mask].contiguous(), f[mask].contiguous()
+        mask = slab_mask(x, rank, ws, equal_count_edges(x, ws) if partition == "equal_count" else None)
+    return x[mask].contiguous(), f[mask].contiguous(), edges
 
 
 def run_ours(args):
@@ -184,7 +186,7 @@ def run_ours(args):
     N = cfg["N"]
     M_total = cfg["M"]
     x_all, f_all = make_inputs(cfg, args.dist, dev)
-    x, f = slab_select(x_all, f_all, rank, ws, args.partition, args.exchange, int(SIGMA * N[0]))
+    x, f, slab_edges = slab_select(x_all, f_all, rank, ws, args.partition, args.exchange, int(SIGMA * N[0]))
     del x_all, f_all
     M_local = x.shape[0]
     torch.cuda.synchronize()
@@ -192,7 +194,8 @@ def run_ours(args):
     if ws > 1:   # the library's multi-GPU plan: the exchange runs inside libhpnfft.so (NCCL)
         from paper_2001_01583_b200.dist import DistPlan
 
-        dplan = DistPlan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", mode=args.exchange, device=dev)
+        dplan = DistPlan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", mode=args.exchange, device=dev,
+                         slab_edges=slab_edges)
         plan = dplan.plan
     else:
         plan = hp.Plan(N, M_local, m=M_WINDOW, sigma=SIGMA, window="kb", device=dev)
@@ -351,7 +354,8 @@ def run_ours(args):
             "config": {"workload": f"BASELINE config {args.config}: d=3, N={N[0]}^3, M={M_total}, "
                                    f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}",
                        "N": list(N), "M": M_total, "m": M_WINDOW, "sigma": SIGMA, "window": "kaiser_bessel",
-                       "points": args.dist, "partition": (f"cell-aligned equal-size x-slabs x{ws}" if args.exchange == "grid_slab"
+                       "points": args.dist, "partition": ((f"cell-aligned equal-cost x-slabs x{ws} (dist.grid_slab_edges)" if args.partition == "equal_count"
+                                      else f"cell-aligned equal-size x-slabs x{ws}") if args.exchange == "grid_slab"
                                      else f"{args.partition} x-slabs x{ws}"),
                        "exchange": (EXCHANGE_TEXT[args.exchange] if ws > 1 else "none"),
                        "fhat_layout": ("full on every rank" if ws == 1 or args.exchange == "allreduce"

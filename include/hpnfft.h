@@ -193,6 +193,20 @@ int hpnfft_get_unique_id(unsigned char id[128]);
 int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_local, int m, double sigma,
                      int window, void* stream, int nranks, int rank, const unsigned char id[128], int mode);
 
+/*
+ * HPNFFT_DIST_GRID_SLAB only: replace the equal-size slabs by arbitrary cell-plane slabs, e.g.
+ * equal-COUNT slabs for clustered points (PAPER.md:93's "subcells with same
+ * size" balance the work only for uniform points).  edges: HOST int64[nranks + 1], x-ordered cell
+ * planes c0x (as above), cyclic: rank s owns c0x in [edges[s], edges[s+1]) mod n0, with
+ * 0 <= edges[0] < n0, edges[nranks] = edges[0] + n0, every slab a multiple of 4 planes and
+ * >= 2m planes, and c0x = n0/2 (x = 0, the grid's memory plane 0) one of the edges mod n0 (each
+ * slab is then one contiguous plane range of the grid in memory).  Collective in effect: every
+ * rank must pass the same edges before its next hpnfft_set_points (which this call invalidates).
+ * The default, set by hpnfft_plan_dist, is edges[s] = s n0 / nranks.  The output layout (k1 slabs)
+ * does not change.  Errors: E_INVALID (not a grid-slab plan, bad edges), E_CUDA.
+ */
+int hpnfft_set_slabs(hpnfft_plan_t p, const int64_t* edges);
+
 /* Shape (HOST int64[3]) of the fhat block hpnfft_adjoint writes on this rank (see the modes). */
 int hpnfft_output_shape(hpnfft_plan_t p, int64_t shape[3]);
 

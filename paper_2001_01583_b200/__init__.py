@@ -88,6 +88,8 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_plan_dist.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
                                      ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
     lib.hpnfft_plan_dist.restype = ctypes.c_int
+    lib.hpnfft_set_slabs.argtypes = [vp, i64p]
+    lib.hpnfft_set_slabs.restype = ctypes.c_int
     lib.hpnfft_output_shape.argtypes = [vp, i64p]
     lib.hpnfft_output_shape.restype = ctypes.c_int
     _lib = lib
@@ -154,6 +156,12 @@ class Plan:
         shp = (ctypes.c_int64 * 3)()
         _check(lib.hpnfft_output_shape(h, shp))
         self.out_shape = tuple(int(v) for v in shp)
+
+    def set_slabs(self, edges):
+        """hpnfft_set_slabs: grid_slab plans only; `edges` = nranks + 1 cyclic x-ordered cell
+        planes (e.g. dist.grid_slab_edges); every rank passes the same edges, then set_points."""
+        arr = (ctypes.c_int64 * len(edges))(*[int(e) for e in edges])
+        _check(load_library().hpnfft_set_slabs(self._h, arr))
 
     # -- stream plumbing: every call runs on the caller's current torch stream (or the fixed one)
     def _sync_stream(self):

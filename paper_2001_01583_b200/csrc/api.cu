@@ -330,11 +330,8 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
       p->plane_len = len;
     }
     if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
-      // grid-slab plans spread exactly their own cell planes plus the halo the taps reach
-      if (p->M > 0 && hi >= lo && (lo < p->slab_lo || hi >= p->slab_lo + p->slab_len)) {
-        set_error("a point lies outside this rank's grid slab (HPNFFT_DIST_GRID_SLAB)");
-        return HPNFFT_E_RANGE;
-      }
+      // grid-slab plans spread exactly their own cell planes plus the halo the taps reach (a
+      // point outside the slab was flagged by k_keys: its key is outside the slab's key range)
       p->plane_lo = ((p->slab_lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
       p->plane_len = p->slab_len + 2 * p->m - 1;
     }

@@ -74,7 +74,8 @@ struct Plan {
   int dist_mode = -1;           // HPNFFT_DIST_* or -1 for a single-GPU plan
   int nranks = 1, dist_rank = 0;
   void* comm = nullptr;         // ncclComm_t
-  int64_t slab_lo = 0, slab_len = 0;   // GRID_SLAB: owned x-ordered cell planes c0x in [lo, lo + len)
+  int64_t slab_lo = 0, slab_len = 0;   // GRID_SLAB: owned x-ordered cell planes c0x in [lo, lo + len) mod n0
+  int64_t slab_edges[17] = {};        // GRID_SLAB: every rank's slab, c0x in [edges[s], edges[s+1]) mod n0
   double* halo = nullptr;       // GRID_SLAB: received halo planes [2m - 1][n1][n2] complex
   double* partial = nullptr;    // REDUCE_SCATTER: this rank's full partial fhat
   // GRID_SLAB over NVLink peer memory (CUDA IPC): the ranks' grids and barrier flags

@@ -216,9 +216,12 @@ int slab_fft(Plan* p, double* fhat) {
   HPNFFT_NCCL_TRY(p, a->GroupStart(), "ncclGroupStart");
   for (int s = 0; s < P; ++s) {
     if (s == r) continue;
-    const int64_t dst_plane = mem_plane((int64_t)s * L, n0);   // first memory plane of rank s's slab
+    // rank s's slab (its own length: slabs may differ, hpnfft_set_slabs) is one memory-contiguous
+    // plane run (x = 0 is a slab edge)
+    const int64_t dst_plane = mem_plane(p->slab_edges[s], n0);
+    const int64_t blk_s = (p->slab_edges[s + 1] - p->slab_edges[s]) * N1P * N2;
     HPNFFT_NCCL_TRY(p, a->Send(send + s * blk, 2 * blk, kNcclFloat64, s, p->comm, p->stream), "ncclSend a2a");
-    HPNFFT_NCCL_TRY(p, a->Recv(recv + dst_plane * N1P * N2, 2 * blk, kNcclFloat64, s, p->comm, p->stream),
+    HPNFFT_NCCL_TRY(p, a->Recv(recv + dst_plane * N1P * N2, 2 * blk_s, kNcclFloat64, s, p->comm, p->stream),
                     "ncclRecv a2a");
   }
   HPNFFT_NCCL_TRY(p, a->GroupEnd(), "ncclGroupEnd");
@@ -525,6 +528,7 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
   p->dist_mode = mode;
   p->nranks = nranks;
   p->dist_rank = rank;
+  for (int s = 0; s <= nranks; ++s) p->slab_edges[s] = (int64_t)s * (n0 / nranks);
   p->slab_len = n0 / nranks;
   p->slab_lo = (int64_t)rank * p->slab_len;
   // grid-slab ranks zero and scan only their own key range per set_points (sort.cu key_range):
@@ -561,6 +565,42 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
     p->p2p = !(env && env[0] == '0') && setup_p2p(p);
   }
   *out = h;
+  return HPNFFT_OK;
+}
+
+int hpnfft_set_slabs(hpnfft_plan_t h, const int64_t* edges) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p || !edges) {
+    set_error("NULL argument");
+    return HPNFFT_E_INVALID;
+  }
+  if (p->dist_mode != HPNFFT_DIST_GRID_SLAB || p->nranks < 2) {
+    set_error("hpnfft_set_slabs: only for HPNFFT_DIST_GRID_SLAB plans of 2 or more ranks");
+    return HPNFFT_E_INVALID;
+  }
+  const int P = p->nranks;
+  const int64_t n0 = p->n[0], min_len = (2 * p->m + 3) / 4 * 4;
+  bool ok = edges[0] >= 0 && edges[0] < n0 && edges[P] == edges[0] + n0;
+  bool x0_edge = false;   // the plane c0x = n0/2 (x = 0, memory plane 0) must start a slab
+  for (int s = 0; s < P && ok; ++s) {
+    const int64_t len = edges[s + 1] - edges[s];
+    ok = len >= min_len && len % 4 == 0;
+    x0_edge = x0_edge || edges[s] % n0 == n0 / 2;
+  }
+  if (!ok || !x0_edge) {
+    set_error("hpnfft_set_slabs: need edges[0] in [0, n0), edges[P] = edges[0] + n0, every slab a multiple "
+              "of 4 planes and >= 2m, and n0/2 (x = 0) among the edges");
+    return HPNFFT_E_INVALID;
+  }
+  if (cudaStreamSynchronize(p->stream) != cudaSuccess ||
+      cudaMemset(p->bin_count, 0, sizeof(uint32_t) * (size_t)(p->nbins + 1)) != cudaSuccess) {
+    set_error("hpnfft_set_slabs: bin table reset failed");
+    return HPNFFT_E_CUDA;
+  }
+  for (int s = 0; s <= P; ++s) p->slab_edges[s] = edges[s];
+  p->slab_lo = edges[p->dist_rank] % n0;
+  p->slab_len = edges[p->dist_rank + 1] - edges[p->dist_rank];
+  p->points_set = false;
   return HPNFFT_OK;
 }
 

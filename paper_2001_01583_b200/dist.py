@@ -10,7 +10,8 @@ PAPER.md:174-200, a binomial tree of MPI Send/Recv).  Here every rank is one GPU
   libhpnfft.so with NCCL over NVLink/NVSwitch — ``allreduce`` (every rank gets fhat),
   ``reduce`` (rank 0 gets fhat, Alg. 3's semantics), ``reduce_scatter`` (k0 slabs) or
   ``grid_slab`` (SURVEY.md §8(e) option G: grid halo exchange + distributed FFT, k1 slabs;
-  the points must be partitioned by ``grid_slab_mask``).  torch.distributed only carries the
+  the points must be partitioned by ``grid_slab_mask``; ``grid_slab_edges`` gives equal-count
+  cell-plane slabs for clustered inputs).  torch.distributed only carries the
   128-byte NCCL unique id from rank 0 to the others.
 
 The partition and the result layout are host logic exercised on CPU with the gloo backend in
@@ -55,19 +56,70 @@ def slab_mask(x, rank: int, world: int, edges=None):
     return m
 
 
-def grid_slab_rank(x, world: int, n0: int):
-    """Owner rank of each point for ``grid_slab`` plans: its x-ordered cell plane
-    c0x = (floor(n0 x0) + n0/2) mod n0 lies in [r n0/P, (r+1) n0/P) (the equal-size x-slab
-    [-1/2 + r/P, -1/2 + (r+1)/P), decided with the library's exact cell rule)."""
+def _cell_plane_x(x, n0: int):
+    """x-ordered cell plane c0x = (floor(n0 x0) + n0/2) mod n0 (the library's exact cell rule)."""
     import torch
 
     c0 = torch.floor(x[:, 0] * float(n0)).to(torch.int64) % n0
-    c0x = (c0 + n0 // 2) % n0
-    return torch.div(c0x, n0 // world, rounding_mode="floor")
+    return (c0 + n0 // 2) % n0
 
 
-def grid_slab_mask(x, rank: int, world: int, n0: int):
-    return grid_slab_rank(x, world, n0) == rank
+def grid_slab_rank(x, world: int, n0: int, edges=None):
+    """Owner rank of each point for ``grid_slab`` plans.  Default: its x-ordered cell plane c0x
+    lies in [r n0/P, (r+1) n0/P) (the equal-size x-slab [-1/2 + r/P, -1/2 + (r+1)/P),
+    PAPER.md:93).  With `edges` (hpnfft_set_slabs, cyclic): c0x in [edges[r], edges[r+1]) mod n0."""
+    import torch
+
+    c0x = _cell_plane_x(x, n0)
+    if edges is None:
+        return torch.div(c0x, n0 // world, rounding_mode="floor")
+    e0 = int(edges[0])
+    rel = (c0x - e0) % n0
+    bounds = torch.tensor([int(e) - e0 for e in edges[1:world]], dtype=torch.int64, device=x.device)
+    return torch.bucketize(rel, bounds, right=True)
+
+
+def grid_slab_mask(x, rank: int, world: int, n0: int, edges=None):
+    return grid_slab_rank(x, world, n0, edges) == rank
+
+
+def grid_slab_edges(x, world: int, n0: int, m: int = 6, group=None, reduce: bool = True,
+                    plane_weight: float = 8000.0):
+    """Equal-COUNT cell-plane slabs for ``grid_slab`` plans (hpnfft_set_slabs): the cyclic edges
+    start at x = 0 (c0x = n0/2, the grid's memory plane 0) and cut the point histogram over the
+    cell planes at the quantiles r M / P, rounded up to multiples of 4 planes, every slab >= 2m
+    planes.  `x` is this rank's points; with `reduce` and torch.distributed initialised the
+    histograms of all ranks are summed first (collective), so every rank returns the same edges
+    (reduce=False when every rank already holds the same full point set).  `plane_weight` adds
+    that many points' worth of cost to every cell plane (a rank's grid planes cost spread-flush
+    and FFT time whatever their point count): the cut is then at equal cost, not equal count.
+    The default 8000 is the fit of tools/slab_cost.py on a B200 at BASELINE config 4
+    (profiles/r1_slab_cost.txt: 9.2e-7 ms per point, 7.1e-3 ms per plane of sort + spread and
+    5.7e-4 ms per plane of the z and y FFT passes); plane_weight=0 gives equal-count slabs."""
+    import torch
+    import torch.distributed as dist
+
+    c0x = _cell_plane_x(x, n0)
+    mem = (c0x + n0 // 2) % n0          # memory plane: x = 0 first
+    hist = torch.bincount(mem, minlength=n0).to(torch.int64)
+    if reduce and dist.is_available() and dist.is_initialized():
+        dist.all_reduce(hist, group=group)
+    cost = hist.to(torch.float64) + float(plane_weight)
+    cum = torch.cumsum(cost, 0).cpu().tolist()   # cum[e] = cost of the memory planes <= e
+    total = cum[-1] if cum else 0
+    step = 4
+    min_len = -(-2 * m // step) * step
+    if world * min_len > n0:
+        raise ValueError("n0 too small for world slabs of >= 2m planes")
+    E = [0]
+    for r in range(1, world):
+        target = r * total / world
+        e = E[-1] + min_len
+        while e + step <= n0 - (world - r) * min_len and cum[e - 1] < target:
+            e += step
+        E.append(min(e, n0 - (world - r) * min_len))
+    E.append(n0)
+    return [e + n0 // 2 for e in E]
 
 
 def equal_count_edges(x, world: int):
@@ -94,7 +146,7 @@ class DistPlan:
     """
 
     def __init__(self, N, M_local: int, m: int = 6, sigma: float = 2.0, window="kb", group=None,
-                 mode: str = "allreduce", device=None, local_fn: Optional[Callable] = None):
+                 mode: str = "allreduce", device=None, local_fn: Optional[Callable] = None, slab_edges=None):
         import torch.distributed as dist
 
         if mode not in MODES:
@@ -118,6 +170,8 @@ class DistPlan:
             dist.broadcast_object_list(uid, src=src, group=group)
             self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device,
                              dist=(self.world, self.rank, uid[0], mode))
+            if slab_edges is not None and self.world > 1:
+                self.plan.set_slabs(slab_edges)
 
     def set_points(self, x):
         self._x = x

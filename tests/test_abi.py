@@ -102,3 +102,5 @@ def test_dist_plan_validation_is_host_side(lib):
     assert lib.hpnfft_plan_dist(ctypes.byref(h), 3, arr, 10, 6, 2.0, 0, None, 2, 0, None, 0) == -1
     assert h.value is None
     assert lib.hpnfft_output_shape(None, None) == -1
+    edges = (ctypes.c_int64 * 3)(0, 16, 32)
+    assert lib.hpnfft_set_slabs(None, edges) == -1

@@ -32,13 +32,17 @@ def _worker(rank, world, port, mode, equal_count, outq):
     try:
         import inputs
         import oracle
-        from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, grid_slab_mask, slab_mask
+        from paper_2001_01583_b200.dist import (DistPlan, equal_count_edges, grid_slab_edges, grid_slab_mask,
+                                                slab_mask)
 
         x = torch.from_numpy(inputs.clustered_points(M, s=0.08) if equal_count else inputs.uniform_points(M))
         f = torch.from_numpy(inputs.uniform_values(M))
         edges = equal_count_edges(x, world) if equal_count else None
         if mode == "grid_slab":
-            mask = grid_slab_mask(x, rank, world, 2 * N[0])
+            # equal-count cell-plane slabs from this rank's share of the histogram (summed over
+            # the ranks inside grid_slab_edges: a collective)
+            gedges = grid_slab_edges(x[rank::world], world, 2 * N[0], plane_weight=0) if equal_count else None
+            mask = grid_slab_mask(x, rank, world, 2 * N[0], gedges)
         else:
             mask = slab_mask(x, rank, world, edges)
         xl, fl = x[mask], f[mask]
@@ -108,6 +112,49 @@ def test_equal_count_partition_balances_clustered_points():
     assert abs(res[0][3] - res[1][3]) <= 2
     x, f = inputs.clustered_points(M, s=0.08), inputs.uniform_values(M)
     assert oracle.rel_l2_error(res[0][1], oracle.nfft_adjoint(x, f, N)) < 1e-14
+
+
+def test_grid_slab_equal_count_clustered():
+    """Equal-count grid slabs (hpnfft_set_slabs edges from the summed histogram) on clustered
+    points: still a partition, better balanced than the equal-size cell slabs, same fhat."""
+    import inputs
+    import oracle
+    from paper_2001_01583_b200.dist import grid_slab_rank
+
+    res = _run(2, "grid_slab", equal_count=True)
+    assert all(r[2] == M for r in res)
+    x, f = inputs.clustered_points(M, s=0.08), inputs.uniform_values(M)
+    full = np.concatenate([r[1] for r in res], axis=1)
+    assert oracle.rel_l2_error(full, oracle.nfft_adjoint(x, f, N)) < 1e-14
+    eq = torch.bincount(grid_slab_rank(torch.from_numpy(x), 2, 2 * N[0]), minlength=2)
+    assert abs(res[0][3] - res[1][3]) <= abs(int(eq[0]) - int(eq[1]))
+
+
+def test_grid_slab_edges_valid_and_balanced():
+    """grid_slab_edges: cyclic edges from x = 0 (c0x = n0/2), multiples of 4 planes, every slab
+    >= 2m planes; owners by bucketize agree with a plain per-point loop; uniform points give
+    near-equal counts and clustered points counts within one 4-plane band of M/P."""
+    import inputs
+    from paper_2001_01583_b200.dist import grid_slab_edges, grid_slab_rank
+
+    n0, m = 512, 6
+    for world in (2, 4, 8):
+        for pts in (inputs.uniform_points(20000), inputs.clustered_points(20000, s=0.1)):
+            x = torch.from_numpy(pts)
+            e = grid_slab_edges(x, world, n0, m=m, plane_weight=0)
+            assert len(e) == world + 1 and e[0] == n0 // 2 and e[-1] == e[0] + n0
+            lens = [e[r + 1] - e[r] for r in range(world)]
+            assert all(L % 4 == 0 and L >= 2 * m for L in lens)
+            own = grid_slab_rank(x, world, n0, e)
+            c0x = [(int(np.floor(n0 * v)) % n0 + n0 // 2) % n0 for v in pts[:500, 0]]
+            brute = [next(r for r in range(world) if (c - e[r]) % n0 < lens[r]) for c in c0x]
+            assert own[:500].tolist() == brute
+            cnt = torch.bincount(own, minlength=world).tolist()
+            assert sum(cnt) == len(pts)
+            band = torch.bincount(torch.tensor([(int(np.floor(n0 * v)) % n0) // 4 for v in pts[:, 0]]),
+                                  minlength=n0 // 4).max().item()
+            # every edge is within one 4-plane band of its quantile, unless the 2m minimum binds
+            assert max(cnt) - min(cnt) <= 2 * band + 1
 
 
 def test_slab_mask_is_partition():

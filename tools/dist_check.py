@@ -18,7 +18,8 @@ import torch.distributed as dist  # noqa: E402
 import inputs  # noqa: E402
 import inputs.device as idev  # noqa: E402
 import paper_2001_01583_b200 as hp  # noqa: E402
-from paper_2001_01583_b200.dist import DistPlan, equal_count_edges, grid_slab_mask, slab_mask  # noqa: E402
+from paper_2001_01583_b200.dist import (DistPlan, equal_count_edges, grid_slab_edges, grid_slab_mask,  # noqa: E402
+                                        slab_mask)
 
 
 def main():
@@ -32,16 +33,20 @@ def main():
     ok = True
     for dist_kind, part, mode in [("uniform", "equal_size", "allreduce"), ("clustered", "equal_count", "allreduce"),
                                   ("uniform", "equal_size", "reduce"), ("uniform", "equal_size", "reduce_scatter"),
-                                  ("uniform", "grid", "grid_slab"), ("clustered", "grid", "grid_slab")]:
+                                  ("uniform", "grid", "grid_slab"), ("clustered", "grid", "grid_slab"),
+                                  ("clustered", "grid_count", "grid_slab")]:
         x = idev.uniform_points(M, device=dev) if dist_kind == "uniform" else idev.clustered_points(M, device=dev)
         f = idev.uniform_values(M, device=dev)
         edges = equal_count_edges(x, world) if part == "equal_count" else None
-        if part == "grid":
-            mask = grid_slab_mask(x, rank, world, 2 * N[0])
+        gedges = None
+        if part == "grid_count":   # equal-count cell-plane slabs (hpnfft_set_slabs), histogram summed over ranks
+            gedges = grid_slab_edges(x[rank::world], world, 2 * N[0])
+        if part in ("grid", "grid_count"):
+            mask = grid_slab_mask(x, rank, world, 2 * N[0], gedges)
         else:
             mask = slab_mask(x, rank, world, edges)
         xl, fl = x[mask].contiguous(), f[mask].contiguous()
-        dp = DistPlan(N, xl.shape[0], mode=mode, device=dev)
+        dp = DistPlan(N, xl.shape[0], mode=mode, device=dev, slab_edges=gedges)
         dp.set_points(xl)
         out = dp.adjoint(fl)
         if mode in ("reduce_scatter", "grid_slab"):
