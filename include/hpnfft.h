@@ -89,6 +89,21 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
 int hpnfft_set_points(hpnfft_plan_t p, const double* x);
 
 /*
+ * hpnfft_set_points without the host synchronisation, for pipelines that keep the host ahead of
+ * the GPU (e.g. host -> device copies of the next batch overlapping this transform).  The flags
+ * are still copied to host memory on the stream, but checked only by the NEXT call of
+ * hpnfft_set_points / hpnfft_set_points_async / hpnfft_check_points on this plan, which returns
+ * this call's HPNFFT_E_RANGE (or a grid-slab barrier timeout) — a deferred error; the transform of
+ * such points is memory-safe but its result is undefined.  Without the read-back the plan cannot
+ * prune the unoccupied grid planes: a single-GPU plan spreads and transforms all n0 planes (the
+ * same work for points that fill [-1/2, 1/2)), a grid-slab plan its fixed slab + halo planes.
+ */
+int hpnfft_set_points_async(hpnfft_plan_t p, const double* x);
+
+/* Wait for the flags of the last hpnfft_set_points_async and return its deferred error (or OK). */
+int hpnfft_check_points(hpnfft_plan_t p);
+
+/*
  * Transform (A3 window, A4 spread, A5 FFT, A6 deconvolve + crop; Alg. 2).
  *   f    : DEVICE [M][2] float64 (re, im) values in the ORIGINAL point order of set_points.
  *   fhat : DEVICE [N0*N1*N2][2] float64 output, fully overwritten (no accumulation).

@@ -59,6 +59,10 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_plan.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
                                 ctypes.c_int, vp]
     lib.hpnfft_plan.restype = ctypes.c_int
+    lib.hpnfft_set_points_async.argtypes = [vp, dp]
+    lib.hpnfft_set_points_async.restype = ctypes.c_int
+    lib.hpnfft_check_points.argtypes = [vp]
+    lib.hpnfft_check_points.restype = ctypes.c_int
     lib.hpnfft_set_points.argtypes = [vp, dp]
     lib.hpnfft_set_points.restype = ctypes.c_int
     lib.hpnfft_adjoint.argtypes = [vp, dp, dp]
@@ -167,7 +171,9 @@ class Plan:
     def _sync_stream(self):
         _check(load_library().hpnfft_set_stream(self._h, _stream_ptr(self._stream)))
 
-    def set_points(self, x):
+    def set_points(self, x, sync: bool = True):
+        """hpnfft_set_points; sync=False: hpnfft_set_points_async (no host wait, all grid planes,
+        a range error is raised by the next set_points / check_points)."""
         import torch
 
         if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.shape[1] == 3):
@@ -176,7 +182,12 @@ class Plan:
             raise ValueError(f"x has {x.shape[0]} points, the plan was built for M = {self.M}")
         x = x.contiguous()
         self._sync_stream()
-        _check(load_library().hpnfft_set_points(self._h, ctypes.c_void_p(x.data_ptr())))
+        fn = load_library().hpnfft_set_points if sync else load_library().hpnfft_set_points_async
+        _check(fn(self._h, ctypes.c_void_p(x.data_ptr())))
+
+    def check_points(self):
+        """hpnfft_check_points: raise the deferred error of the last set_points(sync=False)."""
+        _check(load_library().hpnfft_check_points(self._h))
 
     def adjoint(self, f, out=None):
         import torch
@@ -322,7 +333,9 @@ class HostPipeline:
         if self.drained[s] is not None:
             self.compute.wait_event(self.drained[s])
         with torch.cuda.stream(self.compute):
-            self.plan.set_points(self.x[s])          # needs x only: f is still copying
+            # needs x only (f is still copying); no host wait: the host stays a transform ahead,
+            # a range error surfaces at the next submit or at flush
+            self.plan.set_points(self.x[s], sync=False)
             self.compute.wait_event(f_ready)
             self.plan.adjoint(self.f[s], out=self.o[s])
             done = torch.cuda.Event()
@@ -337,6 +350,7 @@ class HostPipeline:
         self.h2d.synchronize()
         self.compute.synchronize()
         self.d2h.synchronize()
+        self.plan.check_points()
 
 
 def version() -> str:

@@ -102,6 +102,7 @@ static void free_plan(Plan* p) {
   cudaFree(p->tile_counter);
   cudaFree(p->err_flag);
   if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
+  if (p->flags_ev) cudaEventDestroy(p->flags_ev);
   dist_free(p);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   delete p;
@@ -232,6 +233,7 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     // end of set_points needs no copy engine (a memcpy would queue behind a caller's large D2H)
     cudaError_t e = cudaHostAlloc(&p->err_flag_host, (2 + 2 * kRangeSlots) * sizeof(int), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->err_flag_host_dev), p->err_flag_host, 0);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->flags_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) {
       set_error("pinned allocation failed");
       rc = HPNFFT_E_NOMEM;
@@ -278,30 +280,11 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   return HPNFFT_OK;
 }
 
-int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
-  Plan* p = reinterpret_cast<Plan*>(h);
-  if (!p) {
-    set_error("NULL plan");
-    return HPNFFT_E_INVALID;
-  }
-  if (p->failed) {
-    set_error("plan is in a failed state (an earlier CUDA error)");
-    return HPNFFT_E_STATE;
-  }
-  if (!x && p->M > 0) {
-    set_error("x is NULL");
-    return HPNFFT_E_INVALID;
-  }
-  p->points_set = false;
-  p->launches = 0;
-  int rc = sort_points(p, x);
-  if (rc) return rc;
-  k_flags_to_host<<<1, 2 + 2 * kRangeSlots, 0, p->stream>>>(p->err_flag, 1 + 2 * kRangeSlots, p->dist_err,
-                                                             p->err_flag_host_dev);
-  p->launches++;
-  rc = check_launch(p, "flag read-back");
-  if (rc) return rc;
-  HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
+namespace {
+
+// the flags of the last set_points, in the mapped host mirror: range / slab errors, the
+// barrier timeout of an earlier grid-slab transform
+int check_flags(Plan* p) {
   if (p->err_flag_host[0] == 1) {
     set_error("a point coordinate is outside [-0.5, 0.5] (or NaN)");
     return HPNFFT_E_RANGE;
@@ -313,9 +296,49 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   if (p->err_flag_host[1 + 2 * kRangeSlots]) {   // a cross-GPU barrier of an earlier grid-slab transform timed out
     return fail(p, HPNFFT_E_NCCL, "a cross-GPU barrier timed out (peer rank missing)");
   }
-  // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
-  {
-    const int64_t n0 = p->n[0];
+  return HPNFFT_OK;
+}
+
+// wait for the read-back of the last async set_points and report its deferred error
+int check_pending(Plan* p) {
+  if (!p->flags_pending) return HPNFFT_OK;
+  p->flags_pending = false;
+  HPNFFT_CUDA_TRY(p, cudaEventSynchronize(p->flags_ev), "set_points flag event");
+  return check_flags(p);
+}
+
+int set_points(Plan* p, const double* x, bool async) {
+  if (p->failed) {
+    set_error("plan is in a failed state (an earlier CUDA error)");
+    return HPNFFT_E_STATE;
+  }
+  if (!x && p->M > 0) {
+    set_error("x is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  int rc = check_pending(p);
+  if (rc) return rc;
+  p->points_set = false;
+  p->launches = 0;
+  rc = sort_points(p, x);
+  if (rc) return rc;
+  k_flags_to_host<<<1, 2 + 2 * kRangeSlots, 0, p->stream>>>(p->err_flag, 1 + 2 * kRangeSlots, p->dist_err,
+                                                             p->err_flag_host_dev);
+  p->launches++;
+  rc = check_launch(p, "flag read-back");
+  if (rc) return rc;
+  const int64_t n0 = p->n[0];
+  const bool slab = p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1;
+  if (async) {
+    HPNFFT_CUDA_TRY(p, cudaEventRecord(p->flags_ev, p->stream), "set_points flag event");
+    p->flags_pending = true;
+    p->plane_lo = 0;   // no read-back of the occupied planes: all of them
+    p->plane_len = n0;
+  } else {
+    HPNFFT_CUDA_TRY(p, cudaStreamSynchronize(p->stream), "set_points sync");
+    rc = check_flags(p);
+    if (rc) return rc;
+    // occupied planes: taps of cells c0 reach l0 = c0 - m + 1 .. c0 + m
     int64_t lo = 0x7fffffff, hi = -1;
     for (int sl = 0; sl < kRangeSlots; ++sl) {
       lo = lo < p->err_flag_host[1 + 2 * sl] ? lo : p->err_flag_host[1 + 2 * sl];
@@ -329,15 +352,44 @@ int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
       p->plane_lo = ((lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
       p->plane_len = len;
     }
-    if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
-      // grid-slab plans spread exactly their own cell planes plus the halo the taps reach (a
-      // point outside the slab was flagged by k_keys: its key is outside the slab's key range)
-      p->plane_lo = ((p->slab_lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
-      p->plane_len = p->slab_len + 2 * p->m - 1;
-    }
+  }
+  if (slab) {
+    // grid-slab plans spread exactly their own cell planes plus the halo the taps reach (a
+    // point outside the slab was flagged by k_keys: its key is outside the slab's key range)
+    p->plane_lo = ((p->slab_lo - n0 / 2 - p->m + 1) % n0 + n0) % n0;
+    p->plane_len = p->slab_len + 2 * p->m - 1;
   }
   p->points_set = true;
   return HPNFFT_OK;
+}
+
+}  // namespace
+
+int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  return set_points(p, x, false);
+}
+
+int hpnfft_set_points_async(hpnfft_plan_t h, const double* x) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  return set_points(p, x, true);
+}
+
+int hpnfft_check_points(hpnfft_plan_t h) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  return check_pending(p);
 }
 
 int hpnfft_adjoint(hpnfft_plan_t h, const double* f, double* fhat) {

@@ -60,6 +60,8 @@ struct Plan {
   int* tile_counter = nullptr;    // sweep tile scheduler counter
   int* err_flag = nullptr;        // device [1 + 2 kRangeSlots]: range-error flag, then slot pairs of
                                   // min / max of the x-ordered cell c0
+  cudaEvent_t flags_ev = nullptr;   // recorded after the flag read-back of an async set_points
+  bool flags_pending = false;       // an async set_points' flags are not checked yet
   int* err_flag_host = nullptr;   // mapped pinned mirror [1 + 2 kRangeSlots + 1 (dist barrier error)]
   int* err_flag_host_dev = nullptr;   // its device alias
   // occupied l0 planes (circular interval [plane_lo, plane_lo + plane_len) mod n0): planes that

@@ -438,3 +438,83 @@ def test_inverse_empty_and_tiny():
     g = gpu_inverse(np.zeros((1, 3)), fh, N)
     assert oracle.rel_l2_error(g, oracle.nfft_inverse(np.zeros((1, 3)), fh, N)) <= 1e-12
     assert abs(g[0] - fh.sum()) <= 1e-9 * np.abs(fh).sum()   # Eq. 6 at x = 0, within the NFFT error
+
+
+# ---- asynchronous set_points and the host pipeline (the e2e path of bench.py) ----------------
+
+@pytest.mark.parametrize("dist", ["uniform", "clustered", "slab"])
+def test_set_points_async_matches_sync(dist):
+    """hpnfft_set_points_async spreads and transforms all n0 planes (no occupied-plane read-back):
+    the same fhat as the pruned synchronous path, also for clustered points and a thin slab."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (32, 64, 16), 20000
+    if dist == "uniform":
+        x = inputs.uniform_points(M, seed=5)
+    elif dist == "clustered":
+        x = inputs.clustered_points(M, s=0.03, seed=5)
+    else:
+        x = inputs.uniform_points(M, seed=5)
+        x[:, 0] = 0.1 + 0.05 * (x[:, 0] + 0.5)
+    f = inputs.uniform_values(M, seed=5)
+    xd, fd = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
+    plan = hp.Plan(N, M, device=dev)
+    plan.set_points(xd)
+    a = plan.adjoint(fd).cpu().numpy()
+    plan.set_points(xd, sync=False)
+    b = plan.adjoint(fd).cpu().numpy()
+    plan.check_points()
+    fl = plan.inverse(torch.from_numpy(a).to(dev)).cpu().numpy()
+    plan.close()
+    assert oracle.rel_l2_error(b, a) <= 1e-14
+    assert oracle.rel_l2_error(b, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+    assert oracle.rel_l2_error(fl, oracle.nfft_inverse(x, a, N)) <= 1e-12
+
+
+def test_set_points_async_deferred_range_error():
+    """An out-of-range point passed to set_points_async is reported by the next call
+    (check_points or set_points), not lost; the plan stays usable."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (16, 16, 16), 100
+    x = inputs.uniform_points(M, seed=3)
+    bad = x.copy()
+    bad[17, 1] = 0.7
+    plan = hp.Plan(N, M, device=dev)
+    plan.set_points(torch.from_numpy(bad).to(dev), sync=False)   # returns at once
+    with pytest.raises(ValueError):
+        plan.check_points()
+    plan.check_points()                                          # reported once
+    plan.set_points(torch.from_numpy(bad).to(dev), sync=False)
+    with pytest.raises(ValueError):
+        plan.set_points(torch.from_numpy(x).to(dev), sync=False)  # the next call reports it
+    plan.set_points(torch.from_numpy(x).to(dev))
+    f = inputs.uniform_values(M, seed=3)
+    g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+    plan.close()
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_host_pipeline_matches_plan(depth):
+    """HostPipeline (pinned host -> device copies, async set_points, deferred D2H) returns for
+    every submitted batch the fhat of the CPU NFFT on that batch."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (16, 32, 16), 3000
+    plan = hp.Plan(N, M, device=dev)
+    pipe = hp.HostPipeline(plan, M, depth=depth)
+    batches, outs = [], []
+    for b in range(5):
+        x = inputs.uniform_points(M, seed=100 + b) if b % 2 else inputs.clustered_points(M, s=0.05, seed=100 + b)
+        f = inputs.uniform_values(M, seed=100 + b)
+        xh = torch.from_numpy(x).pin_memory()
+        fh = torch.from_numpy(f).pin_memory()
+        oh = torch.empty(plan.out_shape, dtype=torch.complex128).pin_memory()
+        pipe.submit(xh, fh, oh)
+        batches.append((x, f))
+        outs.append(oh)
+    pipe.flush()
+    plan.close()
+    for (x, f), oh in zip(batches, outs):
+        assert oracle.rel_l2_error(oh.numpy(), oracle.nfft_adjoint(x, f, N)) <= 1e-12
