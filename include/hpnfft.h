@@ -164,6 +164,22 @@ int hpnfft_stage_times(hpnfft_plan_t p, float* out, int n);
 /* Library version string. */
 const char* hpnfft_version(void);
 
+/*
+ * ENUF reciprocal-space energy (Eq. 12, §5 "HP-ENUF"):
+ *   U = 1/(2 pi L) sum_{n in I_N, n != 0} exp(-pi^2 |n|^2 / (alpha L)^2) / |n|^2 |S(n)|^2
+ *       - alpha / sqrt(pi) sum_i q_i^2,        S(n) = sum_i q_i exp(-2 pi i n.r_i / L),
+ * with the points of the last hpnfft_set_points taken as x_i = r_i / L - 1/2 (so that
+ * |S(n)| = |fhat(n)| of Eq. 5 with f_i = q_i).
+ *   q     : DEVICE [M] float64 real charges (this rank's points for a multi-GPU plan).
+ *   L     : box side (> 0), alpha : Ewald parameter (> 0), in the same length unit.
+ *   U     : DEVICE 1 float64, written in stream order (the sum over all ranks for a grid-slab plan).
+ * Runs the adjoint's spread and FFT passes on f_i = q_i + 0i; the last FFT pass sums the weighted
+ * |fhat|^2 instead of storing fhat (no fhat buffer); fixed-order reductions (deterministic).
+ * Errors: E_INVALID (NULL, L or alpha <= 0), E_STATE (no set_points), E_UNSUPPORTED (a multi-GPU
+ * plan other than HPNFFT_DIST_GRID_SLAB), E_NOMEM, E_CUDA, E_NCCL.  Asynchronous.
+ */
+int hpnfft_ewald_reciprocal(hpnfft_plan_t p, const double* q, double L, double alpha, double* U);
+
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU (A7 of SURVEY.md §8(a), §8(e)): one process per GPU, NCCL over NVLink/NVSwitch.
  * By Eq. 8 (§3) fhat is linear in the point set: every rank transforms its own

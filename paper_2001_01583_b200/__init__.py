@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_plan_dist.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64, ctypes.c_int, ctypes.c_double,
                                      ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
     lib.hpnfft_plan_dist.restype = ctypes.c_int
+    lib.hpnfft_ewald_reciprocal.argtypes = [vp, dp, ctypes.c_double, ctypes.c_double, dp]
+    lib.hpnfft_ewald_reciprocal.restype = ctypes.c_int
     lib.hpnfft_set_slabs.argtypes = [vp, i64p]
     lib.hpnfft_set_slabs.restype = ctypes.c_int
     lib.hpnfft_output_shape.argtypes = [vp, i64p]
@@ -160,6 +162,22 @@ class Plan:
         shp = (ctypes.c_int64 * 3)()
         _check(lib.hpnfft_output_shape(h, shp))
         self.out_shape = tuple(int(v) for v in shp)
+
+    def ewald_reciprocal(self, q, L: float, alpha: float, out=None):
+        """hpnfft_ewald_reciprocal: Eq. 12's reciprocal-space energy of the real charges q
+        (CUDA float64 [M]) at the points of the last set_points (x = r / L - 1/2).  Returns a
+        CUDA float64 tensor of one element (stream-ordered; .item() synchronises)."""
+        import torch
+
+        if not (q.is_cuda and q.dtype == torch.float64 and q.numel() == self.M):
+            raise TypeError("q must be a CUDA float64 tensor with M elements")
+        q = q.contiguous()
+        if out is None:
+            out = torch.empty((1,), dtype=torch.float64, device=q.device)
+        self._sync_stream()
+        _check(load_library().hpnfft_ewald_reciprocal(self._h, ctypes.c_void_p(q.data_ptr()), float(L), float(alpha),
+                                                      ctypes.c_void_p(out.data_ptr())))
+        return out
 
     def set_slabs(self, edges):
         """hpnfft_set_slabs: grid_slab plans only; `edges` = nranks + 1 cyclic x-ordered cell

@@ -101,6 +101,8 @@ static void free_plan(Plan* p) {
   cudaFree(p->group_rows);
   cudaFree(p->tile_counter);
   cudaFree(p->err_flag);
+  cudaFree(p->fq);
+  cudaFree(p->e_partial);
   if (p->err_flag_host) cudaFreeHost(p->err_flag_host);
   if (p->flags_ev) cudaEventDestroy(p->flags_ev);
   dist_free(p);

@@ -34,6 +34,13 @@ struct Plan {
   int window = HPNFFT_WINDOW_KAISER_BESSEL;
   cudaStream_t stream = nullptr;
   int spread_method = HPNFFT_SPREAD_AUTO;
+  // ENUF reciprocal energy (energy.cu): while `energy` is set, the last FFT pass (x_pass) sums
+  // Eq. 12's weighted |fhat|^2 into e_partial[0 .. e_nparts) instead of storing fhat
+  bool energy = false;
+  double e_a = 0.0;
+  double* e_partial = nullptr;
+  int64_t e_nparts = 0, e_cap = 0;
+  double* fq = nullptr;   // [M] complex (q, 0) of hpnfft_ewald_reciprocal
   bool failed = false;
   bool points_set = false;
 
@@ -119,6 +126,9 @@ int spread_sweep(Plan* p, const double* f);
 bool sweep_supported(const Plan* p);
 size_t record_bytes(int m);
 int fft_and_deconvolve(Plan* p, double* fhat);
+// the last (x) pass of the adjoint: lines k1 in [k1_base, k1_base + inner / N2) of B[n0][.][N2],
+// deconvolved into fhat, or (p->energy) summed into Eq. 12's partials
+int x_pass(Plan* p, const double* in, double* fhat, int64_t inner, int64_t k1_base, int a_lo, int a_len);
 // one batched pruned FFT pass along dimension dim (fft.cu, see k_fft_pass)
 // (peers: device array of nranks output pointers for the grid-slab y pass over NVLink; NP = N/P)
 int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
@@ -126,6 +136,7 @@ int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int
 // multi-GPU exchange steps (dist.cu)
 int dist_adjoint(Plan* p, const double* f, double* fhat);
 void dist_free(Plan* p);
+int dist_allreduce_sum(Plan* p, double* buf, int64_t count);
 int spread(Plan* p, const double* f);
 // inverse direction (Eq. 6): fft.cu subdivide + inverse FFT into the grid, interp.cu interpolation
 int subdivide_and_ifft(Plan* p, const double* fhat);

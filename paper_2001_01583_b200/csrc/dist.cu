@@ -230,7 +230,7 @@ int slab_fft(Plan* p, double* fhat) {
                   "a2a self block");
   stage_end(p, 9);
   stage_begin(p, 6);
-  rc = fft_pass(p, 0, p->grid, fhat, 1, N1P * N2, false, 0, 1, 0, (int)n0);
+  rc = x_pass(p, p->grid, fhat, N1P * N2, (int64_t)r * N1P, 0, (int)n0);
   stage_end(p, 6);
   return rc;
 }
@@ -341,7 +341,7 @@ int slab_adjoint_p2p(Plan* p, double* fhat) {
   if (rc) return rc;
   // 4. x pass on the own k1 slab
   stage_begin(p, 6);
-  rc = fft_pass(p, 0, p->grid, fhat, 1, N1P * N2, false, 0, 1, 0, (int)n0);
+  rc = x_pass(p, p->grid, fhat, N1P * N2, (int64_t)r * N1P, 0, (int)n0);
   stage_end(p, 6);
   return rc;
 }
@@ -440,6 +440,14 @@ int dist_adjoint(Plan* p, const double* f, double* fhat) {
       set_error("unknown distribution mode");
       return HPNFFT_E_INVALID;
   }
+}
+
+// in-place sum over the ranks of `count` doubles (the ENUF energy scalar of grid-slab plans)
+int dist_allreduce_sum(Plan* p, double* buf, int64_t count) {
+  if (p->nranks < 2) return HPNFFT_OK;
+  const NcclApi* a = nccl();
+  HPNFFT_NCCL_TRY(p, a->AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, p->comm, p->stream), "ncclAllReduce");
+  return HPNFFT_OK;
 }
 
 void dist_free(Plan* p) {

@@ -96,6 +96,21 @@ struct LineIO {
   // (index k + N/2 <-> grid frequency k mod n, the other n - N frequencies are 0), scaled by
   // inv_c on input and conjugated (IFFT(v) = conj(FFT(conj(v)))); all n outputs conjugated
   bool inv;
+  // ENUF reciprocal energy (Eq. 12; EN kernels, pass x only): instead of storing
+  // fhat(k), accumulate exp(-e_a |n|^2) / |n|^2 |fhat(k)|^2 over n = k - N/2 != 0, where the
+  // line is (k1, k2) = (k1_base + line_i / N2e, line_i mod N2e) and the output index is k0
+  double e_a;
+  int64_t k1_base;
+  int N1e, N2e;
+  double esum;
+};
+
+// kernel argument of the energy variant of the x pass: per-CTA partial sums go to partial[]
+struct EnergyArgs {
+  double* partial;
+  double e_a;
+  int64_t k1_base;
+  int N1, N2;
 };
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
@@ -117,9 +132,9 @@ constexpr size_t tile_elems() {
   return CONTIG ? (size_t)TI * ((1 << LOGN) + (1 << LOGN) / 8) : (size_t)(1 << LOGN) * (TI + 1);
 }
 
-template <int LOGN, int R, int Ns, int TI, bool CONTIG, bool IN_G, bool OUT_G>
+template <int LOGN, int R, int Ns, int TI, bool CONTIG, bool IN_G, bool OUT_G, bool EN>
 __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const cplx* __restrict__ tw,
-                                               const LineIO& io) {
+                                               LineIO& io) {
   constexpr int n = 1 << LOGN;
   constexpr int BPT = (n >= 8 ? 8 : n) / R;   // butterflies per thread
   constexpr int T = (n >= 8 ? n / 8 : 1);     // threads per column
@@ -177,7 +192,20 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = idxD + r * Ns;   // frequency index on the oversampled grid
-      if (OUT_G && io.inv) {
+      if (OUT_G && EN) {
+        const int N = io.N;
+        const bool lo = q < N / 2, hi = q >= n - N / 2;
+        if (io.valid && (lo || hi)) {
+          const int k = lo ? q + N / 2 : q - (n - N / 2);
+          const double sc = io.inv_c[k];
+          const double re = v[b][r].x * sc, im = v[b][r].y * sc;
+          const int64_t k1 = io.k1_base + io.line_i / io.N2e;
+          const double a0 = (double)(k - N / 2), a1 = (double)(k1 - io.N1e / 2),
+                       a2 = (double)(io.line_i % io.N2e - io.N2e / 2);
+          const double nn = a0 * a0 + a1 * a1 + a2 * a2;
+          if (nn > 0.0) io.esum += exp(-io.e_a * nn) / nn * (re * re + im * im);
+        }
+      } else if (OUT_G && io.inv) {
         if (io.valid) io.gout[(int64_t)q * io.ostride] = {v[b][r].x, -v[b][r].y};
       } else if (OUT_G) {
         const int N = io.N;
@@ -197,11 +225,11 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
   if (!OUT_G) __syncthreads();   // the tile is complete before the next stage reads it
 }
 
-template <int LOGN, int TI, bool CONTIG, int K>
-__device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cplx* __restrict__ tw, const LineIO& io) {
+template <int LOGN, int TI, bool CONTIG, bool EN, int K>
+__device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cplx* __restrict__ tw, LineIO& io) {
   constexpr int NS = n_stages(LOGN);
-  stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, K == NS - 1>(buf, col, tj, tw, io);
-  if constexpr (K + 1 < NS) run_stages<LOGN, TI, CONTIG, K + 1>(buf, col, tj, tw, io);
+  stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, K == NS - 1, EN>(buf, col, tj, tw, io);
+  if constexpr (K + 1 < NS) run_stages<LOGN, TI, CONTIG, EN, K + 1>(buf, col, tj, tw, io);
 }
 
 // Batched pruned pass.  Lines are indexed by (outer o, column i); element a of a line sits at
@@ -210,11 +238,11 @@ __device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cpl
 // outers.  Output k' in [0,N) goes to out + (o * N + k') * inner + i, scaled by inv_c[k'].
 // Thread mapping: strided passes put consecutive lanes on consecutive columns (coalesced rows of
 // TI complex); the contiguous pass puts consecutive lanes on consecutive butterflies of a line.
-template <int LOGN, int TI, bool CONTIG>
+template <int LOGN, int TI, bool CONTIG, bool EN = false>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
            const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
-           int a_len, cplx* const* peers, int NP, int inv) {
+           int a_len, cplx* const* peers, int NP, int inv, EnergyArgs ea) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
   extern __shared__ cplx smem[];
@@ -253,7 +281,25 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     io.line_o = o;
     io.line_i = ic;
   }
-  run_stages<LOGN, TI, CONTIG, 0>(smem, col, tj, tw, io);
+  io.e_a = ea.e_a;
+  io.k1_base = ea.k1_base;
+  io.N1e = ea.N1;
+  io.N2e = ea.N2 > 0 ? ea.N2 : 1;
+  io.esum = 0.0;
+  run_stages<LOGN, TI, CONTIG, EN, 0>(smem, col, tj, tw, io);
+  if constexpr (EN) {   // CTA partial of Eq. 12's sum, fixed order (deterministic)
+    __shared__ double red[32];
+    double v = io.esum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      ea.partial[blockIdx.x] = t;
+    }
+  }
 }
 
 template <int LOGN>
@@ -286,7 +332,8 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
-                                                                            o_start, o_total, a_lo, a_len, nullptr, 1, inv);
+                                                                            o_start, o_total, a_lo, a_len, nullptr, 1, inv,
+                                                                            EnergyArgs{});
   } else {
     const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
     const int64_t blocks = outer * ((inner + TI - 1) / TI);
@@ -294,7 +341,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
-                                                     a_len, peers, NP, inv);
+                                                     a_len, peers, NP, inv, EnergyArgs{});
   }
   p->launches++;
   return check_launch(p, "fft pass");
@@ -362,11 +409,63 @@ int fft_and_deconvolve(Plan* p, double* fhat) {
   stage_end(p, 5);
   if (rc) return rc;
   stage_begin(p, 6);
-  rc = launch_pass(p, p->logn[0], p->bufB, fhat, 1, N1 * N2, (int)N0, p->inv_c[0], p->twiddle[0], false, 0, 1,
-                   (int)plo, (int)plen);
+  rc = x_pass(p, p->bufB, fhat, N1 * N2, 0, (int)plo, (int)plen);
   stage_end(p, 6);
   (void)N0;
   return rc;
+}
+
+// x pass of Eq. 12 (ENUF reciprocal energy): the x lines of B[n0][L1][N2] (L1 = the k1 rows
+// this plan holds, starting at k1_base) with the deconvolution applied and the weighted |fhat|^2
+// summed per CTA into partial[] (nothing is stored).  Returns the number of partials (CTAs).
+template <int LOGN>
+static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_a, int64_t k1_base, double* partial,
+                               int a_lo, int a_len) {
+  constexpr int TI = tile_cols<LOGN>();
+  constexpr int n = 1 << LOGN;
+  constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
+  const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
+  const int64_t blocks = (inner + TI - 1) / TI;
+  auto kern = k_fft_pass<LOGN, TI, false, true>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    fail(p, HPNFFT_E_CUDA, "fft smem attr");
+    return -1;
+  }
+  EnergyArgs ea{partial, e_a, k1_base, (int)p->N[1], (int)p->N[2]};
+  kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, nullptr, 1, inner, (int)p->N[0], p->inv_c[0],
+                                                   reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len,
+                                                   nullptr, 1, 0, ea);
+  p->launches++;
+  return check_launch(p, "fft energy pass") ? -1 : blocks;
+}
+
+static int64_t energy_x_pass(Plan* p, const double* in, int64_t inner, double e_a, int64_t k1_base, double* partial,
+                             int a_lo, int a_len) {
+  const cplx* ci = reinterpret_cast<const cplx*>(in);
+  switch (p->logn[0]) {
+    case 2: return launch_energy_n<2>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 3: return launch_energy_n<3>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 4: return launch_energy_n<4>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 5: return launch_energy_n<5>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 6: return launch_energy_n<6>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 7: return launch_energy_n<7>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 8: return launch_energy_n<8>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 9: return launch_energy_n<9>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 10: return launch_energy_n<10>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    default:
+      set_error("FFT length not supported");
+      return -1;
+  }
+}
+
+int x_pass(Plan* p, const double* in, double* fhat, int64_t inner, int64_t k1_base, int a_lo, int a_len) {
+  if (!p->energy)
+    return launch_pass(p, p->logn[0], in, fhat, 1, inner, (int)p->N[0], p->inv_c[0], p->twiddle[0], false, 0, 1, a_lo,
+                       a_len);
+  const int64_t nb = energy_x_pass(p, in, inner, p->e_a, k1_base, p->e_partial, a_lo, a_len);
+  if (nb < 0) return p->failed ? HPNFFT_E_CUDA : HPNFFT_E_UNSUPPORTED;
+  p->e_nparts = nb;
+  return HPNFFT_OK;
 }
 
 }  // namespace hpnfft

@@ -237,6 +237,16 @@ __device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, uint
       "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
       : "memory");
 }
+// 4-byte asynchronous global -> shared copies (the producer's bin-bound prefetch ring)
+__device__ __forceinline__ void cp_async4(uint32_t* smem, const uint32_t* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
                    (uint32_t)__cvta_generic_to_shared(bar)),
@@ -256,25 +266,39 @@ __device__ __forceinline__ void dmma16(double (&c)[4], double a0, double a1, dou
       : "d"(a0), "d"(a1), "d"(b));
 }
 
+// A batch holds the records of one chunk or, at low point density, of up to kMaxSeg chunks
+// (segments; records in chunk order), so that sparse inputs do not pay one pipeline round trip
+// per chunk of a handful of records.
+constexpr int kMaxSeg = 8;
 struct BatchHdr {
   int B;      // records in the batch; -1 terminates
   int tile;   // tile id
-  int chunk;  // chunk index within the tile (records' step = chunk * CH + (c0 mod CH))
+  int chunk;  // chunk index within the tile of the first segment (step = chunk * CH + (c0 mod CH))
   int end;    // 1: end of tile (flush the rest), 2: tile skipped in this group pass
+  int nseg;   // segments: records [seg_end[j-1], seg_end[j]) belong to chunk `chunk + seg_dch[j]`
+  int16_t seg_end[kMaxSeg];
+  uint8_t seg_dch[kMaxSeg];
 };
+// list capacity: every list of a multi-segment batch is padded to whole k-steps per segment
+__host__ __device__ constexpr int list_cap(int cap, bool merge) { return merge ? cap + 3 * kMaxSeg : cap; }
 
 __host__ __device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
+// chunks whose bin bounds the producer has in flight (cp.async ring): at low point density most
+// chunks are empty and the producer would otherwise wait one global-load latency per chunk
+constexpr int kBinPrefetch = 8;
+
 template <int P1, int P2, int M_>
-__host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap) {
+__host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap, bool merge) {
   using C = SweepCfg<P1, P2, M_>;
   return sizeof(double) * ((size_t)C::NS * cap * Rec<2 * M_>::kDoubles + Rec<2 * M_>::kDoubles) +
-         (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NL * (cap + 1) + 16;
+         (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NL * (list_cap(cap, merge) + 1) +
+         sizeof(uint32_t) * kBinPrefetch * 32 * 4 + 32;
 }
 
 // ------------------------------------------------------------------------------------------
 // A4: the warp-specialised persistent sweep (see the file header).
-template <int P1, int P2, int M_, bool INV>
+template <int P1, int P2, int M_, bool INV, bool MERGE>
 __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((SweepCfg<P1, P2, M_>::kMaxRegs))
     k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
@@ -293,7 +317,14 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   uint64_t* s_landed = s_empty + NS;                                              // [NS] records landed
   BatchHdr* s_hdr = reinterpret_cast<BatchHdr*>(s_landed + NS);                   // [NS]
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_hdr + NS);                      // [NS][NL]
-  uint32_t* s_list = s_cnt + NS * NL;                                             // [NS][NL][cap]
+  // multi-chunk batches (MERGE, chosen for sparse inputs): adjoint consumers with one sub-patch
+  // per warp only (the inverse consumer loads its grid window per chunk, two interleaved
+  // sub-patches share one flush front)
+  constexpr bool kMerge = MERGE && !INV && SUB == 1;
+  const int capL = list_cap(cap, kMerge);
+  uint32_t* s_list = s_cnt + NS * NL;                                             // [NS][NL][capL]
+  uint32_t* s_pf = reinterpret_cast<uint32_t*>(                                   // [kBinPrefetch][32][4]
+      (reinterpret_cast<uintptr_t>(s_list + (size_t)NS * NL * capL) + 15) & ~(uintptr_t)15);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = prm.n0, n1 = prm.n1, n2 = prm.n2;
@@ -368,19 +399,51 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           ra1 = 0;
           rb1 = b2hi - prm.nb2;
         }
+        // bin bounds of chunk ci (lo0, hi0, lo1, hi1 of this lane's row) -> ring slot ci mod PF
+        auto prefetch = [&](int ci) {
+          uint32_t* d = s_pf + ((ci % kBinPrefetch) * 32 + lane) * 4;
+          if (ci < nch && r < C::kRows) {
+            const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
+            const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
+            cp_async4(d + 0, prm.start + ((rowbase + ra0) << LC));
+            cp_async4(d + 1, prm.start + ((rowbase + rb0 + 1) << LC));
+            if (rb1 >= ra1) {
+              cp_async4(d + 2, prm.start + ((rowbase + ra1) << LC));
+              cp_async4(d + 3, prm.start + ((rowbase + rb1 + 1) << LC));
+            } else {
+              d[2] = d[3] = 0u;
+            }
+          } else {
+            d[0] = d[1] = d[2] = d[3] = 0u;
+          }
+          cp_async_commit();
+        };
+#pragma unroll 1
+        for (int u = 0; u < kBinPrefetch; ++u) prefetch(u);
+        // the open batch: oB records of onseg segments so far, first chunk och0
+        bool open = false;
+        int oB = 0, onseg = 0, och0 = 0;
+        auto close_batch = [&]() {
+          if (!open) return;
+          if (lane == 0) {
+            BatchHdr& h = s_hdr[stage];
+            h.B = oB;
+            h.tile = t;
+            h.chunk = och0;
+            h.end = 0;
+            h.nseg = onseg;
+            mbar_arrive(&s_landed[stage]);
+          }
+          open = false;
+          next_stage();
+        };
         for (int ci = 0; ci < nch; ++ci) {
           const unsigned long long p0 = kProf ? clock64() : 0ull;
-          const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
           uint32_t beg0 = 0, len0 = 0, beg1 = 0, len1 = 0;
-          if (r < C::kRows) {
-            const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
-            const uint32_t lo0 = __ldg(prm.start + ((rowbase + ra0) << LC));
-            const uint32_t hi0 = __ldg(prm.start + ((rowbase + rb0 + 1) << LC));
-            uint32_t lo1 = 0, hi1 = 0;
-            if (rb1 >= ra1) {
-              lo1 = __ldg(prm.start + ((rowbase + ra1) << LC));
-              hi1 = __ldg(prm.start + ((rowbase + rb1 + 1) << LC));
-            }
+          cp_async_wait<kBinPrefetch - 1>();   // chunk ci's group has landed (one group per chunk)
+          {
+            const uint4 v = *reinterpret_cast<const uint4*>(s_pf + ((ci % kBinPrefetch) * 32 + lane) * 4);
+            const uint32_t lo0 = v.x, hi0 = v.y, lo1 = v.z, hi1 = v.w;
             // clip to the group, make group-relative
             const uint32_t l0c = max(lo0, prm.g0), h0c = min(hi0, prm.g1);
             const uint32_t l1c = max(lo1, prm.g0), h1c = min(hi1, prm.g1);
@@ -389,6 +452,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
             beg1 = l1c - prm.g0;
             len1 = h1c > l1c ? h1c - l1c : 0u;
           }
+          prefetch(ci + kBinPrefetch);   // (after this slot's values are in registers)
           // chunk offsets: exclusive warp scan of the lane totals
           const uint32_t cnt = len0 + len1;
           uint32_t incl = cnt;
@@ -400,15 +464,23 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
           const uint32_t off0 = incl - cnt, off1 = off0 + len0;
           if (kProf && lane == 0) atomicAdd(prm.prof + 4, clock64() - p0);
-          for (uint32_t b0 = 0; b0 < total; b0 += (uint32_t)cap) {
-            const uint32_t b1 = min(total, b0 + (uint32_t)cap);
-            const int B = (int)(b1 - b0);
+          if (total == 0) continue;
+          if (open && (oB + (int)total > cap || onseg == kMaxSeg || ci - och0 > 127)) close_batch();
+          for (uint32_t b0 = 0; b0 < total;) {
             const unsigned long long p1 = kProf ? clock64() : 0ull;
-            mbar_wait(&s_empty[stage], phase ^ 1u);
+            if (!open) {
+              mbar_wait(&s_empty[stage], phase ^ 1u);
+              open = true;
+              oB = 0;
+              onseg = 0;
+              och0 = ci;
+            }
             const unsigned long long p2 = kProf ? clock64() : 0ull;
-            if (lane == 0) mbar_expect_tx(&s_landed[stage], (uint32_t)B * (uint32_t)(RD * sizeof(double)));
+            const uint32_t b1 = min(total, b0 + (uint32_t)(cap - oB));
+            const int take = (int)(b1 - b0);
+            if (lane == 0) mbar_expect_tx(&s_landed[stage], (uint32_t)take * (uint32_t)(RD * sizeof(double)));
             __syncwarp();
-            double* dst = s_rec + (size_t)stage * cap * RD;
+            double* dst = s_rec + ((size_t)stage * cap + oB) * RD;
             // the part of each run inside [b0, b1) -> consecutive ring slots, one bulk copy
             auto issue = [&](uint32_t off, uint32_t beg, uint32_t len) {
               if (len == 0 || off >= b1 || off + len <= b0) return;
@@ -419,22 +491,30 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
             };
             issue(off0, beg0, len0);
             issue(off1, beg1, len1);
+            oB += take;
             if (lane == 0) {
-              s_hdr[stage] = BatchHdr{B, t, ci, 0};
-              mbar_arrive(&s_landed[stage]);
+              s_hdr[stage].seg_end[onseg] = (int16_t)oB;
+              s_hdr[stage].seg_dch[onseg] = (uint8_t)(ci - och0);
             }
+            ++onseg;
+            b0 = b1;
             if (kProf && lane == 0) {
               atomicAdd(prm.prof + 5, p2 - p1);
               atomicAdd(prm.prof + 6, clock64() - p2);
             }
-            next_stage();
+            if (!kMerge || oB == cap) close_batch();
           }
         }
+        close_batch();
       }
       // end-of-tile marker (consumers flush every remaining node of the tile unless it is skipped)
       mbar_wait(&s_empty[stage], phase ^ 1u);
       if (lane == 0) {
-        s_hdr[stage] = BatchHdr{0, t, skip ? 0 : nch, skip ? 2 : 1};
+        s_hdr[stage].B = 0;
+        s_hdr[stage].tile = t;
+        s_hdr[stage].chunk = skip ? 0 : nch;
+        s_hdr[stage].end = skip ? 2 : 1;
+        s_hdr[stage].nseg = 0;
         mbar_arrive(&s_landed[stage]);
       }
       next_stage();
@@ -443,7 +523,11 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     for (int i = 0; i < C::kListWarps; ++i) {
       mbar_wait(&s_empty[stage], phase ^ 1u);
       if (lane == 0) {
-        s_hdr[stage] = BatchHdr{-1, -1, 0, 0};
+        s_hdr[stage].B = -1;
+        s_hdr[stage].tile = -1;
+        s_hdr[stage].chunk = 0;
+        s_hdr[stage].end = 0;
+        s_hdr[stage].nseg = 0;
         mbar_arrive(&s_landed[stage]);
       }
       next_stage();
@@ -474,29 +558,48 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         int R0, C0, L0, S_, a_lo, nch;
         tile_geom(hdr.tile, R0, C0, L0, S_, a_lo, nch);
         const double* recs = s_rec + (size_t)stage * cap * RD;
-        uint32_t* lists = s_list + (size_t)stage * NL * cap;
-        for (int base = 0; base < hdr.B; base += 32) {
-          const int e = base + lane;
-          int dr = -1000, dc = -1000;   // footprint origin relative to the patch origin
-          uint32_t ebase = 0;
-          if (e < hdr.B) {
-            const int4 cc = *reinterpret_cast<const int4*>(recs + (size_t)e * RD);
-            dr = ((cc.x - M_ + 1 - R0 + W) & (n1 - 1)) - W;
-            dc = ((cc.y - M_ + 1 - C0 + W) & (n2 - 1)) - W;
-            ebase = (uint32_t)e | ((uint32_t)(cc.z & (CH - 1)) << 9);
+        uint32_t* lists = s_list + (size_t)stage * NL * capL;
+        // entry = record | (c0 mod CH) << 9 | segment chunk offset << 11 | d1 << 18 | d2 << 23
+        // (single-chunk batches: one segment [0, B), offset 0)
+        const int nseg = kMerge ? hdr.nseg : 1;
+        for (int j = 0; j < nseg; ++j) {
+          const int sb = (kMerge && j) ? (int)s_hdr[stage].seg_end[j - 1] : 0;
+          const int se = kMerge ? (int)s_hdr[stage].seg_end[j] : hdr.B;
+          const uint32_t dch = kMerge ? (uint32_t)s_hdr[stage].seg_dch[j] << 11 : 0u;
+          for (int base = sb; base < se; base += 32) {
+            const int e = base + lane;
+            int dr = -1000, dc = -1000;   // footprint origin relative to the patch origin
+            uint32_t ebase = 0;
+            if (e < se) {
+              const int4 cc = *reinterpret_cast<const int4*>(recs + (size_t)e * RD);
+              dr = ((cc.x - M_ + 1 - R0 + W) & (n1 - 1)) - W;
+              dc = ((cc.y - M_ + 1 - C0 + W) & (n2 - 1)) - W;
+              ebase = (uint32_t)e | ((uint32_t)(cc.z & (CH - 1)) << 9) | dch;
+            }
+#pragma unroll
+            for (int wr = 0; wr < P1 / kWR; ++wr) {
+              const uint32_t d1 = (uint32_t)(kWR * wr - dr + (kWR - 1));
+              const bool relr = d1 < (uint32_t)(W + kWR - 1);
+#pragma unroll
+              for (int wc = 0; wc < NWC; ++wc) {
+                const uint32_t d2 = (uint32_t)(kWC * wc - dc + (kWC - 1));
+                const bool rel = relr && d2 < (uint32_t)(W + kWC - 1);
+                const unsigned bal = __ballot_sync(0xffffffffu, rel);
+                const int w = wr * NWC + wc;
+                if (rel)
+                  lists[(size_t)w * capL + cnt[w] + __popc(bal & ((1u << lane) - 1))] = ebase | (d1 << 18) | (d2 << 23);
+                cnt[w] += __popc(bal);
+              }
+            }
           }
+          if (kMerge && nseg > 1) {
+            // pad every list to whole k-steps (4 entries) with null records (index 0x1ff: the
+            // all-zero record) of this segment's chunk, so that no k-step spans two chunks
 #pragma unroll
-          for (int wr = 0; wr < P1 / kWR; ++wr) {
-            const uint32_t d1 = (uint32_t)(kWR * wr - dr + (kWR - 1));
-            const bool relr = d1 < (uint32_t)(W + kWR - 1);
-#pragma unroll
-            for (int wc = 0; wc < NWC; ++wc) {
-              const uint32_t d2 = (uint32_t)(kWC * wc - dc + (kWC - 1));
-              const bool rel = relr && d2 < (uint32_t)(W + kWC - 1);
-              const unsigned bal = __ballot_sync(0xffffffffu, rel);
-              const int w = wr * NWC + wc;
-              if (rel) lists[(size_t)w * cap + cnt[w] + __popc(bal & ((1u << lane) - 1))] = ebase | (d1 << 18) | (d2 << 23);
-              cnt[w] += __popc(bal);
+            for (int w = 0; w < NL; ++w) {
+              const int pad = (-cnt[w]) & 3;
+              if (lane < pad) lists[(size_t)w * capL + cnt[w] + lane] = 0x1ffu | dch;
+              cnt[w] += pad;
             }
           }
         }
@@ -596,7 +699,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       const double* recs = s_rec + (size_t)stage * cap * RD;
       const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(recs);
       const int nlist = (int)s_cnt[stage * NL + warp];
-      const uint32_t* my = s_list + ((size_t)stage * NL + warp) * cap;
+      const uint32_t* my = s_list + ((size_t)stage * NL + warp) * capL;
       for (int k = 0; k < nlist; k += 8) {
         // B: lane (g, t) = record k + g, column t of every slice
         const bool act = k + g < nlist;
@@ -768,7 +871,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
 #pragma unroll
     for (int u = 0; u < SUB; ++u) {
       nl[u] = (int)s_cnt[stage * NL + warp * SUB + u];
-      ml[u] = s_list + ((size_t)stage * NL + warp * SUB + u) * cap;
+      ml[u] = s_list + ((size_t)stage * NL + warp * SUB + u) * capL;
     }
     int nlist = nl[0];
     const uint32_t* my = ml[0];
@@ -786,12 +889,16 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     // Sub-patch rows (n-tiles) outside every footprint of the k-step are skipped
     // (HPNFFT_SWEEP_NTSKIP): lists are in batch order = candidate-row order, so the 4 records of
     // a k-step mostly share d1.
+    // kc: the k-step's chunk offset within a multi-chunk batch (entries of a k-step share it;
+    // lane 0 always holds a live entry); null entries (0x1ff, list padding) read the zero record
     auto fetch_l = [&](const uint32_t* lst, int n, int k, double& a0, double& a1, double& fp, double& w2v,
-                       double (&w1v)[NT], int& ntlo, int& nthi) {
+                       double (&w1v)[NT], int& ntlo, int& nthi, int& kc) {
       const bool act = k + t < n;
       const uint32_t en = act ? lst[k + t] : 0u;
-      const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
-      const int sh = step0 + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
+      const bool live = act && (!kMerge || (en & 0x1ffu) != 0x1ffu);
+      const uint32_t ra = live ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
+      kc = kMerge ? (int)__shfl_sync(0xffffffffu, (en >> 11) & 127u, 0) : 0;
+      const int sh = step0 + kc * CH + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
       const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
       // A fragments: rows 8 mt + g hold node (row - (st - m + 1)) mod 16 of this record
       a0 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
@@ -813,7 +920,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
 #endif
     };
     auto fetch = [&](int k, double& a0, double& a1, double& fp, double& w2v, double (&w1v)[NT], int& ntlo,
-                     int& nthi) { fetch_l(my, nlist, k, a0, a1, fp, w2v, w1v, ntlo, nthi); };
+                     int& nthi, int& kc) { fetch_l(my, nlist, k, a0, a1, fp, w2v, w1v, ntlo, nthi, kc); };
     auto apply_u = [&](double (&ac)[NT][4], double a0, double a1, double fp, double w2v, const double (&w1v)[NT],
                        int ntlo, int nthi) {
       const double fw2 = fp * w2v;
@@ -835,16 +942,24 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       // the first k-step's operand loads are issued before the flush of the earlier chunks, whose
       // accumulator reads wait for this warp's in-flight DMMAs
       double p0, p1, pf, p2v, p1v[NT];
-      int plo = 0, phi = NT - 1;
-      if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v, plo, phi);
-      advance(step0);                       // earlier chunks are complete
+      int plo = 0, phi = NT - 1, pkc = 0;
+      if (nlist > 0) fetch(0, p0, p1, pf, p2v, p1v, plo, phi, pkc);
+      advance(step0 + pkc * CH);            // earlier chunks are complete
+      int ckc = pkc;                        // chunk (offset) the accumulator window is at
+      auto to_chunk = [&](int kc) {         // a multi-chunk batch moves on: flush the chunks before
+        if (kMerge && kc != ckc) {
+          advance(step0 + kc * CH);
+          ckc = kc;
+        }
+      };
       int k = 0;
       if (nlist > 0) {
         if (nlist > 4) {
           double b0, b1, gp, g2v, g1v[NT];
-          int blo, bhi;
-          fetch(4, b0, b1, gp, g2v, g1v, blo, bhi);
+          int blo, bhi, bkc;
+          fetch(4, b0, b1, gp, g2v, g1v, blo, bhi, bkc);
           apply(p0, p1, pf, p2v, p1v, plo, phi);
+          to_chunk(bkc);
           apply(b0, b1, gp, g2v, g1v, blo, bhi);
           k = 8;
         } else {
@@ -854,24 +969,28 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       }
       for (; k + 4 < nlist; k += 8) {   // two k-steps per iteration
         double a0, a1, fp, w2v, w1v[NT], b0, b1, gp, g2v, g1v[NT];
-        int alo, ahi, blo, bhi;
-        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
-        fetch(k + 4, b0, b1, gp, g2v, g1v, blo, bhi);
+        int alo, ahi, blo, bhi, akc, bkc;
+        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi, akc);
+        fetch(k + 4, b0, b1, gp, g2v, g1v, blo, bhi, bkc);
+        to_chunk(akc);
         apply(a0, a1, fp, w2v, w1v, alo, ahi);
+        to_chunk(bkc);
         apply(b0, b1, gp, g2v, g1v, blo, bhi);
       }
       if (k < nlist) {
         double a0, a1, fp, w2v, w1v[NT];
-        int alo, ahi;
-        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi);
+        int alo, ahi, akc;
+        fetch(k, a0, a1, fp, w2v, w1v, alo, ahi, akc);
+        to_chunk(akc);
         apply(a0, a1, fp, w2v, w1v, alo, ahi);
       }
     } else {
       // two sub-patches: their k-steps (independent accumulators) are interleaved
       double p0, p1, pf, p2v, p1v[NT], b0, b1, gp, g2v, g1v[NT];
       int plo = 0, phi = NT - 1, blo = 0, bhi = NT - 1;
-      if (nl[0] > 0) fetch_l(ml[0], nl[0], 0, p0, p1, pf, p2v, p1v, plo, phi);
-      if (nl[1] > 0) fetch_l(ml[1], nl[1], 0, b0, b1, gp, g2v, g1v, blo, bhi);
+      int kc_unused = 0;   // single-chunk batches (no merging with two sub-patches per warp)
+      if (nl[0] > 0) fetch_l(ml[0], nl[0], 0, p0, p1, pf, p2v, p1v, plo, phi, kc_unused);
+      if (nl[1] > 0) fetch_l(ml[1], nl[1], 0, b0, b1, gp, g2v, g1v, blo, bhi, kc_unused);
       advance(step0);                     // earlier chunks are complete
       int ka = 0, kb = 0;
       while (ka < nl[0] || kb < nl[1]) {
@@ -880,8 +999,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         if (db) apply_u(acc[1], b0, b1, gp, g2v, g1v, blo, bhi);
         ka += 4;
         kb += 4;
-        if (ka < nl[0]) fetch_l(ml[0], nl[0], ka, p0, p1, pf, p2v, p1v, plo, phi);
-        if (kb < nl[1]) fetch_l(ml[1], nl[1], kb, b0, b1, gp, g2v, g1v, blo, bhi);
+        if (ka < nl[0]) fetch_l(ml[0], nl[0], ka, p0, p1, pf, p2v, p1v, plo, phi, kc_unused);
+        if (kb < nl[1]) fetch_l(ml[1], nl[1], kb, b0, b1, gp, g2v, g1v, blo, bhi, kc_unused);
       }
     }
     __syncwarp();
@@ -942,9 +1061,16 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
   const size_t smem_max = C::kCtasPerSm == 1 ? (size_t)(227 * 1024) : (size_t)(113 * 1024);
+  // multi-chunk batches when a (tile, chunk) holds few records on average (sparse points: one
+  // pipeline round trip per chunk would dominate); HPNFFT_SWEEP_MERGE=0/1 forces the choice
+  constexpr int W = 2 * M_;
+  const double dens = (double)p->M / ((double)p->n[0] * (double)p->n[1] * (double)p->n[2]);
+  const double per_chunk = dens * (P1 + W - 1) * (P2 + W - 1) * CH;
+  bool merge = !INV && C::SUB == 1 && per_chunk < 64.0;
+  if (const char* e = getenv("HPNFFT_SWEEP_MERGE")) merge = !INV && C::SUB == 1 && e[0] == '1';
   int cap = 32;
-  while (cap + 32 <= 511 && sweep_smem_bytes_of<P1, P2, M_>(cap + 32) <= smem_max) cap += 32;
-  const size_t smem = sweep_smem_bytes_of<P1, P2, M_>(cap);
+  while (cap + 32 <= 511 && sweep_smem_bytes_of<P1, P2, M_>(cap + 32, merge) <= smem_max) cap += 32;
+  const size_t smem = sweep_smem_bytes_of<P1, P2, M_>(cap, merge);
   SweepParams prm;
   prm.rec = p->rec;
   prm.start = p->bin_count;
@@ -978,7 +1104,10 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   }
   prm.prof = prof;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
-  auto kern = k_spread_sweep<P1, P2, M_, INV>;
+  auto kern = k_spread_sweep<P1, P2, M_, INV, false>;
+  if constexpr (!INV) {
+    if (merge) kern = k_spread_sweep<P1, P2, M_, false, true>;
+  }
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                   "sweep smem attr");
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;

@@ -104,3 +104,4 @@ def test_dist_plan_validation_is_host_side(lib):
     assert lib.hpnfft_output_shape(None, None) == -1
     edges = (ctypes.c_int64 * 3)(0, 16, 32)
     assert lib.hpnfft_set_slabs(None, edges) == -1
+    assert lib.hpnfft_ewald_reciprocal(None, None, 1.0, 1.0, None) == -1

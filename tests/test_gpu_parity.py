@@ -246,6 +246,31 @@ def test_sweep_multi_group_accumulate(dist, monkeypatch):
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
 
 
+@pytest.mark.parametrize("merge", ["0", "1"])
+@pytest.mark.parametrize("case", ["dense", "sparse", "crystal", "groups"])
+def test_sweep_multi_chunk_batches(merge, case, monkeypatch):
+    """Both batch modes of the sweep on dense and sparse inputs: one chunk per batch, and the
+    multi-chunk batches of sparse inputs (several chunks' records per pipeline stage, lists padded
+    to whole k-steps per chunk, flushes between chunks inside a batch), also with record groups."""
+    monkeypatch.setenv("HPNFFT_SWEEP_MERGE", merge)
+    if case == "dense":
+        N, M = (32, 32, 64), 40000
+        x = inputs.uniform_points(M, seed=21)
+    elif case == "sparse":
+        N, M = (64, 64, 64), 3001
+        x = inputs.clustered_points(M, s=0.1, seed=21)
+    elif case == "crystal":
+        x, _, _ = inputs.crystal_nfft_inputs("caf2", 4)
+        N, M = (32, 32, 32), x.shape[0]
+    else:
+        monkeypatch.setenv("HPNFFT_REC_GROUP", "1024")
+        N, M = (64, 32, 64), 7001
+        x = inputs.uniform_points(M, seed=22)
+    f = inputs.uniform_values(M, seed=21)
+    g = gpu_adjoint(x, f, N, method="sweep")
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
 @pytest.mark.parametrize("lo,hi", [(-0.5, -0.375), (-0.1, 0.1), (0.3, 0.5), (0.49, 0.5), (-0.01, 0.0),
                                    (-0.5, 0.5)])
 @pytest.mark.parametrize("method", ["auto", "atomic"])
@@ -518,3 +543,88 @@ def test_host_pipeline_matches_plan(depth):
     plan.close()
     for (x, f), oh in zip(batches, outs):
         assert oracle.rel_l2_error(oh.numpy(), oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+# ---- ENUF reciprocal energy, Eq. 12 ---------------------------------
+
+def _gpu_ewald(kind, cells, N, alpha):
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    r, q, L = inputs.crystal(kind, cells)
+    x = r / L - 0.5
+    plan = hp.Plan(N, x.shape[0], device=dev)
+    plan.set_points(torch.from_numpy(x).to(dev))
+    u = plan.ewald_reciprocal(torch.from_numpy(q).to(dev), L, alpha).item()
+    plan.close()
+    return u, r, q, L
+
+
+def test_ewald_reciprocal_config2_vs_oracle():
+    """BASELINE config 2 (fluorite 8^3 cells, N = 64^3): the fused GPU energy equals Eq. 12 on the
+    CPU NFFT's fhat (O2) to 1e-11 and on the direct NDFT (O1) to 1e-9, and with the oracle's
+    real-space Eq. 11 gives the paper's Madelung constant 2.5194."""
+    import json
+
+    from oracle import ewald
+
+    N, alpha = (64, 64, 64), 0.85
+    u, r, q, L = _gpu_ewald("caf2", 8, N, alpha)
+    x, f = r / L - 0.5, q.astype(np.complex128)
+    u_o2 = ewald.reciprocal_energy(oracle.nfft_adjoint(x, f, N), q, L, alpha)
+    assert abs(u - u_o2) <= 1e-11 * abs(u_o2)
+    u_o1 = ewald.reciprocal_energy(oracle.ndft_direct(x, f, N), q, L, alpha)
+    assert abs(u - u_o1) <= 1e-9 * abs(u_o1)
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "madelung.json")))["caf2"]
+    U = ewald.real_space_energy(r, q, L, alpha) + u
+    mad = abs(U) * 3 / (r.shape[0] * 2.0 * 1.0)
+    assert abs(mad - gold["value"]) < gold["tolerance"]
+
+
+def test_ewald_reciprocal_paper_scale_madelung():
+    """The paper's system: 32^3 fluorite cells = 393216 ions, L = 73.9 r0, alpha =
+    1.2 / r0 (Fig. 15's range), N = 256^3.  Pins: (a) extensivity — for a perfect crystal
+    S(n) = 32^3 S_cell(n / 32) on n = 0 mod 32 and 0 elsewhere, so U^K = 32^3 U^K(one cell,
+    N = 8^3), the latter by the direct NDFT of 12 ions; (b) with the oracle's real-space energy
+    (per cell, from 4^3 cells: erfc(alpha L/2) ~ 1e-14) the Madelung constant is 2.5194."""
+    import json
+
+    from oracle import ewald
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "madelung.json")))["caf2"]
+    r1, q1, L1 = inputs.crystal("caf2", 1)
+    x1 = r1 / L1 - 0.5
+    r4, q4, L4 = inputs.crystal("caf2", 4)
+    for alpha in (1.2, 1.5, 1.8):   # Fig. 15's range (PAPER.md:312)
+        u, r, q, L = _gpu_ewald("caf2", 32, (256, 256, 256), alpha)
+        assert r.shape[0] == 393216 and abs(L - 73.9) < 0.05
+        u1 = ewald.reciprocal_energy(oracle.ndft_direct(x1, q1.astype(np.complex128), (8, 8, 8)), q1, L1, alpha)
+        assert abs(u - 32 ** 3 * u1) <= 1e-9 * abs(u)
+        ur = ewald.real_space_energy(r4, q4, L4, alpha) * (32 / 4) ** 3
+        mad = abs(ur + u) * 3 / (r.shape[0] * 2.0 * 1.0)
+        print(f"alpha={alpha}: U^K={u:.10e} rel(U^K - 32^3 U^K_cell)={abs(u - 32 ** 3 * u1) / abs(u):.1e} "
+              f"Madelung={mad:.6f}")
+        assert abs(mad - gold["value"]) < gold["tolerance"]
+
+
+def test_ewald_reciprocal_random_charges_and_edges():
+    """Random neutral-ish charges at uniform points on a non-cubic grid (ragged tiles) vs Eq. 12 on
+    the CPU NFFT; M = 0 gives U = 0; energy before set_points is E_STATE."""
+    from oracle import ewald
+
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M, L, alpha = (32, 16, 64), 3001, 10.0, 0.7
+    x = inputs.uniform_points(M, seed=9)
+    q = inputs.uniform_values(M, seed=9).real.copy()
+    plan = hp.Plan(N, M, device=dev)
+    with pytest.raises(RuntimeError):
+        plan.ewald_reciprocal(torch.from_numpy(q).to(dev), L, alpha)
+    plan.set_points(torch.from_numpy(x).to(dev))
+    u = plan.ewald_reciprocal(torch.from_numpy(q).to(dev), L, alpha).item()
+    plan.close()
+    u_o2 = ewald.reciprocal_energy(oracle.nfft_adjoint(x, q.astype(np.complex128), N), q, L, alpha)
+    assert abs(u - u_o2) <= 1e-11 * abs(u_o2)
+    plan0 = hp.Plan(N, 0, device=dev)
+    plan0.set_points(torch.zeros((0, 3), dtype=torch.float64, device=dev))
+    assert plan0.ewald_reciprocal(torch.zeros(0, dtype=torch.float64, device=dev), L, alpha).item() == 0.0
+    plan0.close()

@@ -86,6 +86,21 @@ def main():
                 print(f"[{dist_kind}/{part}/{mode}] inverse on the rank's points: E2(dist plan vs 1-GPU plan)="
                       f"{ei:.2e} (all ranks ok: {bool(flag_i.item())})", flush=True)
                 ok &= bool(flag_i.item())
+        # ENUF reciprocal energy (Eq. 12) of real charges q = Re f: grid-slab plans sum their k1 slabs
+        # and all-reduce the scalar; compare with the single-GPU plan on all points
+        if mode == "grid_slab":
+            q = f.real.contiguous()
+            ql = q[mask].contiguous()
+            L, alpha = 10.0, 0.6
+            u = dp.plan.ewald_reciprocal(ql, L, alpha).item()
+            if rank == 0:
+                ref_e = hp.Plan(N, M, device=dev)
+                ref_e.set_points(x)
+                u1 = ref_e.ewald_reciprocal(q, L, alpha).item()
+                ref_e.close()
+                ee = abs(u - u1) / abs(u1)
+                print(f"[{dist_kind}/{part}/{mode}] ewald_reciprocal: U={u:.12e} rel(dist vs 1-GPU)={ee:.2e}", flush=True)
+                ok &= ee <= 1e-12
         dp.close()
         dist.barrier()
     flag = torch.tensor([1 if ok else 0], device=dev)
