@@ -1064,7 +1064,9 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   // multi-chunk batches when a (tile, chunk) holds few records on average (sparse points: one
   // pipeline round trip per chunk would dominate); HPNFFT_SWEEP_MERGE=0/1 forces the choice
   constexpr int W = 2 * M_;
-  const double dens = (double)p->M / ((double)p->n[0] * (double)p->n[1] * (double)p->n[2]);
+  // (points per cell of the planes this plan spreads: a grid-slab rank's slab, occupied planes)
+  const double planes = (double)(p->plane_len > 0 ? p->plane_len : p->n[0]);
+  const double dens = (double)p->M / (planes * (double)p->n[1] * (double)p->n[2]);
   const double per_chunk = dens * (P1 + W - 1) * (P2 + W - 1) * CH;
   bool merge = !INV && C::SUB == 1 && per_chunk < 64.0;
   if (const char* e = getenv("HPNFFT_SWEEP_MERGE")) merge = !INV && C::SUB == 1 && e[0] == '1';
