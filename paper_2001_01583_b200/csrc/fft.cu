@@ -302,6 +302,119 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// n = 1024 contiguous pass (z lines of config 5 and of the large HP-ENUF grids): four-step
+// 1024 = 32 x 32 with each 32-point DFT in one thread's registers and ONE shared-memory
+// transpose, instead of 4 Stockham stages (3 round trips, 3 CTAs per SM):
+//   x index t + 32 j, frequency k1 + 32 k2:
+//   Y[t][k1] = W1024^{t k1} sum_j x[t + 32 j] W32^{j k1}      (thread t, coalesced loads)
+//   X[k1 + 32 k2] = sum_t Y[t][k1] W32^{t k2}                  (thread k1, coalesced stores)
+// shared tile [k1][t] with row stride 33 (conflict-free in both phases).  The twiddles
+// W1024^{t k1} are powers of the table value W1024^t by complex products (31 products:
+// ~31 ulp, far below the 1e-12 bar).  Forward, output-pruned (k in I_N, scaled by 1/c_k).
+__constant__ cplx c_w32[32] = {
+    {1, -0},
+    {0.98078528040323043, -0.19509032201612825},
+    {0.92387953251128674, -0.38268343236508978},
+    {0.83146961230254524, -0.55557023301960218},
+    {0.70710678118654757, -0.70710678118654746},
+    {0.55557023301960229, -0.83146961230254524},
+    {0.38268343236508984, -0.92387953251128674},
+    {0.19509032201612833, -0.98078528040323043},
+    {6.123233995736766e-17, -1},
+    {-0.19509032201612819, -0.98078528040323043},
+    {-0.38268343236508973, -0.92387953251128674},
+    {-0.55557023301960196, -0.83146961230254546},
+    {-0.70710678118654746, -0.70710678118654757},
+    {-0.83146961230254535, -0.55557023301960218},
+    {-0.92387953251128674, -0.38268343236508989},
+    {-0.98078528040323043, -0.19509032201612861},
+    {-1, -1.2246467991473532e-16},
+    {-0.98078528040323043, 0.19509032201612836},
+    {-0.92387953251128685, 0.38268343236508967},
+    {-0.83146961230254546, 0.55557023301960196},
+    {-0.70710678118654768, 0.70710678118654746},
+    {-0.55557023301960218, 0.83146961230254524},
+    {-0.38268343236509034, 0.92387953251128652},
+    {-0.19509032201612866, 0.98078528040323032},
+    {-1.8369701987210297e-16, 1},
+    {0.1950903220161283, 0.98078528040323043},
+    {0.38268343236509, 0.92387953251128663},
+    {0.55557023301960184, 0.83146961230254546},
+    {0.70710678118654735, 0.70710678118654768},
+    {0.83146961230254524, 0.55557023301960218},
+    {0.92387953251128652, 0.38268343236509039},
+    {0.98078528040323032, 0.19509032201612872}};
+
+// in-register 32-point DFT, v[j] -> V[k]: 32 = 4 x 8, j = r + 4 i, k = k1 + 8 k2
+__device__ __forceinline__ void dft32(cplx (&v)[32]) {
+  cplx y[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[r][i] = v[r + 4 * i];
+    dft<8>(y[r]);
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1)
+      if (r > 0) y[r][k1] = cmul(y[r][k1], c_w32[(r * k1) & 31]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 8; ++k1) {
+    cplx z[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+    dft<4>(z);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 8 * k2] = z[k2];
+  }
+}
+
+constexpr int kF1024Lines = 2;   // lines per CTA (32 threads each; 33.8 KB static shared)
+
+__global__ void __launch_bounds__(32 * kF1024Lines) k_fft1024_contig(const cplx* __restrict__ in, cplx* __restrict__ out,
+                                                                   int64_t outer, int N,
+                                                                   const double* __restrict__ inv_c,
+                                                                   const cplx* __restrict__ tw, int64_t o_start,
+                                                                   int64_t o_total) {
+  constexpr int n = 1024;
+  __shared__ cplx tile[kF1024Lines][32 * 33];
+  const int t = threadIdx.x & 31, line = threadIdx.x >> 5;
+  const int64_t o = (int64_t)blockIdx.x * kF1024Lines + line;
+  const bool valid = o < outer;
+  const int64_t oc = valid ? (o_start + o) % o_total : 0;
+  const cplx* gin = in + oc * n;
+  cplx v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = valid ? gin[t + 32 * j] : cplx{0.0, 0.0};
+  dft32(v);
+  cplx* tl = tile[line];
+  {
+    const cplx w = tw[t];   // W1024^t
+    cplx p = {1.0, 0.0};
+#pragma unroll
+    for (int k1 = 0; k1 < 32; ++k1) {
+      tl[k1 * 33 + t] = k1 ? cmul(v[k1], p) : v[0];
+      p = cmul(p, w);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int tt = 0; tt < 32; ++tt) v[tt] = tl[t * 33 + tt];   // thread t now holds k1 = t
+  dft32(v);
+  if (!valid) return;
+  cplx* gout = out + oc * N;
+  const int k1 = t;
+#pragma unroll
+  for (int k2 = 0; k2 < 32; ++k2) {
+    const int q = k1 + 32 * k2;
+    const bool lo = q < N / 2, hi = q >= n - N / 2;
+    if (lo || hi) {
+      const int k = lo ? q + N / 2 : q - (n - N / 2);
+      const double sc = inv_c[k];
+      gout[k] = {v[k2].x * sc, v[k2].y * sc};
+    }
+  }
+}
+
 template <int LOGN>
 constexpr int tile_cols() {
   return (1 << LOGN) >= 1024 ? 4 : ((4096 >> LOGN) > 64 ? 64 : (4096 >> LOGN));
@@ -316,6 +429,14 @@ constexpr int tile_cols_contig() {
   return tile_cols<LOGN>() < HPNFFT_FFT_CONTIG_LINES ? tile_cols<LOGN>() : HPNFFT_FFT_CONTIG_LINES;
 }
 
+static bool fft1024_disabled() {   // HPNFFT_FFT1024=0: the generic Stockham pass (measurement)
+  static const bool off = [] {
+    const char* e = getenv("HPNFFT_FFT1024");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 template <int LOGN>
 static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
                          const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
@@ -325,6 +446,12 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
   if (outer <= 0 || inner <= 0) return HPNFFT_OK;
+  if (LOGN == 10 && contig && !inv && a_lo == 0 && a_len == n && !fft1024_disabled()) {
+    k_fft1024_contig<<<(unsigned)((outer + kF1024Lines - 1) / kF1024Lines), 32 * kF1024Lines, 0, p->stream>>>(
+        in, out, outer, N, inv_c, tw, o_start, o_total);
+    p->launches++;
+    return check_launch(p, "fft pass (n = 1024)");
+  }
   if (contig) {
     const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(cplx);
     const int64_t blocks = (outer + TC - 1) / TC;

@@ -628,3 +628,13 @@ def test_ewald_reciprocal_random_charges_and_edges():
     plan0.set_points(torch.zeros((0, 3), dtype=torch.float64, device=dev))
     assert plan0.ewald_reciprocal(torch.zeros(0, dtype=torch.float64, device=dev), L, alpha).item() == 0.0
     plan0.close()
+
+
+def test_fft_n1024_lines_four_step():
+    """n2 = 1024 (N2 = 512): the z pass runs the four-step 32 x 32 register kernel; the
+    result matches the CPU NFFT, with Gaussian-clustered points and a ragged M."""
+    N, M = (16, 8, 512), 5003
+    x = inputs.clustered_points(M, s=0.1, seed=31)
+    f = inputs.uniform_values(M, seed=31)
+    g = gpu_adjoint(x, f, N)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
