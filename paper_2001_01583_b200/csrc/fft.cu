@@ -429,6 +429,96 @@ constexpr int tile_cols_contig() {
   return tile_cols<LOGN>() < HPNFFT_FFT_CONTIG_LINES ? tile_cols<LOGN>() : HPNFFT_FFT_CONTIG_LINES;
 }
 
+
+// Strided n = 1024 lines (passes y and x): the same four-step transform, CW columns per CTA.
+// Thread (c, t) = (tid mod CW, tid / CW): lanes run along the columns, so each of the 32 loads
+// of a thread is part of a CW x 16 B row segment.  Shared tile [c][k1][t], k1 rows of 33, one
+// padding element per column (conflict-free stores and loads).  Input rows a with
+// (a - a_lo) mod n >= a_len read as 0 (pass x: unoccupied planes).
+template <int CW, bool EN>
+__global__ void __launch_bounds__(32 * CW) k_fft1024_strided(const cplx* __restrict__ in, cplx* __restrict__ out,
+                                                            int64_t inner, int N, const double* __restrict__ inv_c,
+                                                            const cplx* __restrict__ tw, int64_t o_start,
+                                                            int64_t o_total, int a_lo, int a_len, EnergyArgs ea) {
+  constexpr int n = 1024;
+  constexpr int CS = 32 * 33 + 1;   // column stride of the tile (elements)
+  extern __shared__ cplx smem[];
+  const int c = threadIdx.x % CW, t = threadIdx.x / CW;
+  const int64_t tiles_per_outer = (inner + CW - 1) / CW;
+  const int64_t o = (o_start + blockIdx.x / tiles_per_outer) % o_total;
+  const int64_t i = (blockIdx.x % tiles_per_outer) * CW + c;
+  const bool valid = i < inner;
+  const int64_t ic = valid ? i : 0;
+  const cplx* gin = in + o * (int64_t)n * inner + ic;
+  cplx v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int a = t + 32 * j;
+    v[j] = (valid && ((a - a_lo) & (n - 1)) < a_len) ? gin[(int64_t)a * inner] : cplx{0.0, 0.0};
+  }
+  dft32(v);
+  cplx* tl = smem + c * CS;
+  {
+    const cplx w = tw[t];
+    cplx p = {1.0, 0.0};
+#pragma unroll
+    for (int k1 = 0; k1 < 32; ++k1) {
+      tl[k1 * 33 + t] = k1 ? cmul(v[k1], p) : v[0];
+      p = cmul(p, w);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int tt = 0; tt < 32; ++tt) v[tt] = tl[t * 33 + tt];   // thread (c, t) now holds k1 = t
+  dft32(v);
+  const int k1 = t;
+  if constexpr (EN) {   // Eq. 12 energy variant of pass x (see LineIO): weighted |fhat|^2, CTA partial
+    double esum = 0.0;
+    if (valid) {
+      const int N2e = ea.N2 > 0 ? ea.N2 : 1;
+      const double b1 = (double)(ea.k1_base + ic / N2e - ea.N1 / 2), b2 = (double)(ic % N2e - N2e / 2);
+#pragma unroll
+      for (int k2 = 0; k2 < 32; ++k2) {
+        const int q = k1 + 32 * k2;
+        const bool lo = q < N / 2, hi = q >= n - N / 2;
+        if (lo || hi) {
+          const int k = lo ? q + N / 2 : q - (n - N / 2);
+          const double sc = inv_c[k];
+          const double re = v[k2].x * sc, im = v[k2].y * sc, b0 = (double)(k - N / 2);
+          const double nn = b0 * b0 + b1 * b1 + b2 * b2;
+          if (nn > 0.0) esum += exp(-ea.e_a * nn) / nn * (re * re + im * im);
+        }
+      }
+    }
+    __shared__ double red[32];
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, w);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = esum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      ea.partial[blockIdx.x] = tot;
+    }
+    return;
+  }
+  if (!valid) return;
+  cplx* gout = out + o * (int64_t)N * inner + ic;
+#pragma unroll
+  for (int k2 = 0; k2 < 32; ++k2) {
+    const int q = k1 + 32 * k2;
+    const bool lo = q < N / 2, hi = q >= n - N / 2;
+    if (lo || hi) {
+      const int k = lo ? q + N / 2 : q - (n - N / 2);
+      const double sc = inv_c[k];
+      gout[(int64_t)k * inner] = {v[k2].x * sc, v[k2].y * sc};
+    }
+  }
+}
+#ifndef HPNFFT_F1024_CW
+#define HPNFFT_F1024_CW 8
+#endif
+
 static bool fft1024_disabled() {   // HPNFFT_FFT1024=0: the generic Stockham pass (measurement)
   static const bool off = [] {
     const char* e = getenv("HPNFFT_FFT1024");
@@ -451,6 +541,18 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
         in, out, outer, N, inv_c, tw, o_start, o_total);
     p->launches++;
     return check_launch(p, "fft pass (n = 1024)");
+  }
+  if (LOGN == 10 && !contig && !inv && peers == nullptr && !fft1024_disabled()) {
+    constexpr int CW = HPNFFT_F1024_CW;
+    const size_t smem = sizeof(cplx) * (size_t)CW * (32 * 33 + 1);
+    HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_fft1024_strided<CW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem),
+                    "fft1024 smem attr");
+    const int64_t blocks = outer * ((inner + CW - 1) / CW);
+    k_fft1024_strided<CW, false><<<(unsigned)blocks, 32 * CW, smem, p->stream>>>(in, out, inner, N, inv_c, tw, o_start,
+                                                                                 o_total, a_lo, a_len, EnergyArgs{});
+    p->launches++;
+    return check_launch(p, "fft pass (n = 1024, strided)");
   }
   if (contig) {
     const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(cplx);
@@ -551,6 +653,22 @@ static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_
   constexpr int TI = tile_cols<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
+  if (LOGN == 10 && !fft1024_disabled()) {
+    constexpr int CW = HPNFFT_F1024_CW;
+    const size_t smem = sizeof(cplx) * (size_t)CW * (32 * 33 + 1);
+    if (cudaFuncSetAttribute(k_fft1024_strided<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      fail(p, HPNFFT_E_CUDA, "fft1024 smem attr");
+      return -1;
+    }
+    const int64_t blocks = (inner + CW - 1) / CW;
+    EnergyArgs ea{partial, e_a, k1_base, (int)p->N[1], (int)p->N[2]};
+    k_fft1024_strided<CW, true><<<(unsigned)blocks, 32 * CW, smem, p->stream>>>(
+        in, nullptr, inner, (int)p->N[0], p->inv_c[0], reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len,
+        ea);
+    p->launches++;
+    return check_launch(p, "fft energy pass (n = 1024)") ? -1 : blocks;
+  }
   const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
   const int64_t blocks = (inner + TI - 1) / TI;
   auto kern = k_fft_pass<LOGN, TI, false, true>;

@@ -630,11 +630,32 @@ def test_ewald_reciprocal_random_charges_and_edges():
     plan0.close()
 
 
-def test_fft_n1024_lines_four_step():
-    """n2 = 1024 (N2 = 512): the z pass runs the four-step 32 x 32 register kernel; the
-    result matches the CPU NFFT, with Gaussian-clustered points and a ragged M."""
-    N, M = (16, 8, 512), 5003
+@pytest.mark.parametrize("N", [(16, 8, 512), (8, 512, 16), (512, 8, 16), (512, 16, 8)])
+def test_fft_n1024_lines_four_step(N):
+    """n_t = 1024 (N_t = 512) along z, y or x: the four-step 32 x 32 register kernels (contiguous
+    and strided, with the x pass's unoccupied-plane input pruning) match the CPU NFFT, with
+    Gaussian-clustered points and a ragged M."""
+    M = 5003
     x = inputs.clustered_points(M, s=0.1, seed=31)
     f = inputs.uniform_values(M, seed=31)
     g = gpu_adjoint(x, f, N)
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("N", [(512, 8, 16), (16, 8, 32)])
+def test_ewald_reciprocal_x_pass_variants(N):
+    """The energy x pass in both kernels (Stockham tile; four-step n0 = 1024) vs Eq. 12 on the
+    CPU NFFT's fhat."""
+    from oracle import ewald
+
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    M, L, alpha = 2003, 7.0, 0.9
+    x = inputs.clustered_points(M, s=0.1, seed=41)
+    q = inputs.uniform_values(M, seed=41).real.copy()
+    plan = hp.Plan(N, M, device=dev)
+    plan.set_points(torch.from_numpy(x).to(dev))
+    u = plan.ewald_reciprocal(torch.from_numpy(q).to(dev), L, alpha).item()
+    plan.close()
+    u_o2 = ewald.reciprocal_energy(oracle.nfft_adjoint(x, q.astype(np.complex128), N), q, L, alpha)
+    assert abs(u - u_o2) <= 1e-11 * abs(u_o2)
