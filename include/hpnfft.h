@@ -5,7 +5,7 @@
  *     fhat(k) = sum_{j=0}^{M-1} f_j * exp(-2 pi i k.x_j),   k in I_N,
  *     I_N = { k in Z^3 : -N_t/2 <= k_t < N_t/2 }            (§1)
  * computed by the CUNFFT gridding scheme (§2 Fig. 1; Alg. 2):
- * bin-sort the points, spread each f_j with a Kaiser-Bessel (or Gaussian) window of 2m taps per
+ * bin-sort the points, spread each f_j with a Kaiser-Bessel (Gaussian, B-spline, sinc-power) window of 2m taps per
  * dimension onto the sigma-oversampled grid I_n (n_t = sigma N_t), FFT that grid, divide by the
  * window's Fourier weights c_k and crop to I_N ("Scaling", §3).
  * The paper's "NDFT" direction (Eq. 5, minus sign) is called "adjoint" here.
@@ -44,7 +44,14 @@ extern "C" {
 
 typedef struct hpnfft_plan_s* hpnfft_plan_t;
 
-enum { HPNFFT_WINDOW_KAISER_BESSEL = 0, HPNFFT_WINDOW_GAUSSIAN = 1 };
+/* Windows named by the paper (§4, Fig. 12); formulas in DESIGN.md reading Q21 /
+ * csrc/window.cuh (NFFT conventions, window in grid cells, support |u| < m). */
+enum {
+  HPNFFT_WINDOW_KAISER_BESSEL = 0,
+  HPNFFT_WINDOW_GAUSSIAN = 1,
+  HPNFFT_WINDOW_B_SPLINE = 2,   /* centred cardinal B-spline M_2m */
+  HPNFFT_WINDOW_SINC_POWER = 3  /* sinc(pi beta u)^2m, beta = (2 sigma - 1)/(2 m sigma) */
+};
 
 enum {
   HPNFFT_OK = 0,
@@ -73,7 +80,7 @@ enum { HPNFFT_SPREAD_AUTO = 0, HPNFFT_SPREAD_ATOMIC = 1, HPNFFT_SPREAD_SWEEP = 2
  *            2..8), else E_UNSUPPORTED.
  *   sigma  : oversampling factor > 1; n_t = sigma N_t must be an integer power of two >= 2m
  *            (PAPER.md:266 uses sigma = 2), else E_UNSUPPORTED (E_INVALID for sigma <= 1).
- *   window : HPNFFT_WINDOW_KAISER_BESSEL or HPNFFT_WINDOW_GAUSSIAN.
+ *   window : HPNFFT_WINDOW_KAISER_BESSEL, _GAUSSIAN, _B_SPLINE or _SINC_POWER.
  *   stream : cudaStream_t (as void*) all work is enqueued on; NULL = legacy default stream.
  */
 int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma,

@@ -26,7 +26,7 @@ import subprocess
 import numpy as np
 
 from . import windows  # noqa: F401
-from .windows import GAUSSIAN, KAISER_BESSEL  # noqa: F401
+from .windows import B_SPLINE, GAUSSIAN, KAISER_BESSEL, SINC_POWER  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")

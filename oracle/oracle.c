@@ -38,6 +38,8 @@
 
 #define ORACLE_KB 0
 #define ORACLE_GAUSS 1
+#define ORACLE_BSPLINE 2
+#define ORACLE_SINC_POWER 3
 
 static const double PI = 3.14159265358979323846264338327950288;
 
@@ -103,14 +105,39 @@ int oracle_ndft(int d, const int64_t* N, int64_t M, const double* x, const doubl
 }
 
 /* Window Phi(a) for a strictly inside the support (|a| < m). */
+/* centred cardinal B-spline M_p(u), Cox-de Boor: M_1 = [-1/2 <= u < 1/2],
+ * M_k(y) = ((k/2 + y) M_{k-1}(y + 1/2) + (k/2 - y) M_{k-1}(y - 1/2)) / (k - 1)  (windows.py) */
+static double bspline(double u, int p) {
+  double v[64];
+  for (int j = 0; j < p; ++j) {
+    double y = u - 0.5 * (double)(p - 1) + (double)j;
+    v[j] = (y >= -0.5 && y < 0.5) ? 1.0 : 0.0;
+  }
+  for (int k = 2; k <= p; ++k) {
+    int r = p - k;
+    for (int j = 0; j <= r; ++j) {
+      double y = u - 0.5 * (double)r + (double)j;
+      v[j] = ((0.5 * k + y) * v[j + 1] + (0.5 * k - y) * v[j]) / (double)(k - 1);
+    }
+  }
+  return v[0];
+}
+
 static inline double window_value(double a, int m, double sigma, int window) {
   if (window == ORACLE_KB) {
     double b = PI * (2.0 - 1.0 / sigma);
     double s = sqrt((double)m * (double)m - a * a);
     return sinh(b * s) / (PI * s);
-  } else {
+  } else if (window == ORACLE_GAUSS) {
     double b = 2.0 * sigma / (2.0 * sigma - 1.0) * (double)m / PI;
     return exp(-a * a / b) / sqrt(PI * b);
+  } else if (window == ORACLE_BSPLINE) {
+    return bspline(a, 2 * m);
+  } else {
+    double beta = (2.0 * sigma - 1.0) / (2.0 * m * sigma);
+    double y = PI * beta * a;
+    double sc = (y == 0.0) ? 1.0 : sin(y) / y;
+    return pow(sc, 2 * m);
   }
 }
 

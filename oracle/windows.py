@@ -18,6 +18,15 @@ conventions, with the window measured in grid cells u = n x:
       Phi(u)      = (pi b)^(-1/2) exp(-u^2 / b),                     |u| < m
       Phi_hat(xi) = exp(-b pi^2 xi^2)
 
+  B-spline (NEXT #3):        Phi(u) = M_{2m}(u), the centred cardinal B-spline of order 2m
+      (support exactly [-m, m]: no truncation), by the Cox-de Boor recursion
+      M_1(u) = [-1/2 <= u < 1/2],  M_p(u) = ((p/2 + u) M_{p-1}(u + 1/2) + (p/2 - u) M_{p-1}(u - 1/2)) / (p - 1)
+      Phi_hat(xi) = sinc(pi xi)^{2m}
+  Sinc power (NEXT #3):      beta = (2 sigma - 1) / (2 m sigma)
+      Phi(u)      = sinc(pi beta u)^{2m},                            |u| < m
+      Phi_hat(xi) = M_{2m}(xi / beta) / beta
+  (sinc(y) = sin(y)/y; both as in the NFFT library's window family, reading Q21.)
+
 Phi_hat(xi) = int Phi_untruncated(v) e^{-2 pi i xi v} dv, so the deconvolution
 factor for frequency k on an n-point grid is Phi_hat(k/n) (Q5: the closed form of
 the untruncated window; the truncation error is part of the method's error).
@@ -29,6 +38,34 @@ from scipy import special
 
 KAISER_BESSEL = 0
 GAUSSIAN = 1
+B_SPLINE = 2
+SINC_POWER = 3
+
+
+def bspline(u, p: int) -> np.ndarray:
+    """Centred cardinal B-spline M_p(u) by the Cox-de Boor recursion (stable, no cancellation)."""
+    u = np.asarray(u, dtype=np.float64)
+    # level 1 at the p points u - (p-1)/2 + j, j = 0 .. p-1; level k keeps p - k + 1 points
+    offs = np.arange(p, dtype=np.float64) - (p - 1) / 2.0
+    y = u[..., None] + offs
+    v = ((y >= -0.5) & (y < 0.5)).astype(np.float64)
+    for k in range(2, p + 1):
+        r = p - k
+        yk = u[..., None] + (np.arange(r + 1, dtype=np.float64) - r / 2.0)
+        v = ((k / 2.0 + yk) * v[..., 1:] + (k / 2.0 - yk) * v[..., :-1]) / (k - 1)
+    return v[..., 0]
+
+
+def sinc_beta(sigma: float, m: int) -> float:
+    return (2.0 * sigma - 1.0) / (2.0 * m * sigma)
+
+
+def _sinc(y):
+    y = np.asarray(y, dtype=np.float64)
+    out = np.ones_like(y)
+    nz = y != 0
+    out[nz] = np.sin(y[nz]) / y[nz]
+    return out
 
 
 def kb_b(sigma: float) -> float:
@@ -53,6 +90,10 @@ def phi(u, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
     elif window == GAUSSIAN:
         b = gauss_b(sigma, m)
         out[inside] = np.exp(-ui * ui / b) / np.sqrt(np.pi * b)
+    elif window == B_SPLINE:
+        out[inside] = bspline(ui, 2 * m)
+    elif window == SINC_POWER:
+        out[inside] = _sinc(np.pi * sinc_beta(sigma, m) * ui) ** (2 * m)
     else:
         raise ValueError("unknown window")
     return out
@@ -70,6 +111,11 @@ def phi_hat(xi, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray
     if window == GAUSSIAN:
         b = gauss_b(sigma, m)
         return np.exp(-b * np.pi ** 2 * xi * xi)
+    if window == B_SPLINE:
+        return _sinc(np.pi * xi) ** (2 * m)
+    if window == SINC_POWER:
+        beta = sinc_beta(sigma, m)
+        return bspline(xi / beta, 2 * m) / beta
     raise ValueError("unknown window")
 
 

@@ -20,7 +20,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HPNFFT_LIB", os.path.join(_HERE, "libhpnfft.so"))
 
-WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1}
+WINDOWS = {"kb": 0, "kaiser_bessel": 0, "gaussian": 1, "gauss": 1, "b_spline": 2, "bspline": 2,
+           "sinc_power": 3, "sinc": 3}
 SPREAD_METHODS = {"auto": 0, "atomic": 1, "sweep": 2}
 STAGES = ("keys", "scan", "scatter", "spread", "fft_z", "fft_y", "fft_x_deconv", "records", "exchange", "alltoall",
           "inv_fft", "interp")

@@ -167,7 +167,8 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     set_error("sigma must be > 1");
     return HPNFFT_E_INVALID;
   }
-  if (window != HPNFFT_WINDOW_KAISER_BESSEL && window != HPNFFT_WINDOW_GAUSSIAN) {
+  if (window != HPNFFT_WINDOW_KAISER_BESSEL && window != HPNFFT_WINDOW_GAUSSIAN && window != HPNFFT_WINDOW_B_SPLINE &&
+      window != HPNFFT_WINDOW_SINC_POWER) {
     set_error("unknown window");
     return HPNFFT_E_INVALID;
   }

@@ -659,3 +659,65 @@ def test_ewald_reciprocal_x_pass_variants(N):
     plan.close()
     u_o2 = ewald.reciprocal_energy(oracle.nfft_adjoint(x, q.astype(np.complex128), N), q, L, alpha)
     assert abs(u - u_o2) <= 1e-11 * abs(u_o2)
+
+
+# ---- NEXT #3: B-spline and sinc-power windows; Fig. 12 ------------------------
+
+@pytest.mark.parametrize("window", ["b_spline", "sinc_power"])
+@pytest.mark.parametrize("m", [2, 4, 6, 8])
+def test_windows_bspline_sinc_power(window, m):
+    """The GPU adjoint and inverse with the B-spline / sinc-power windows equal the CPU NFFT with
+    the same window (same approximation) to 1e-12."""
+    from oracle import windows
+
+    wid = {"b_spline": windows.B_SPLINE, "sinc_power": windows.SINC_POWER}[window]
+    N, M = (16, 32, 16), 2001
+    x = inputs.uniform_points(M, seed=51 + m)
+    f = inputs.uniform_values(M, seed=51 + m)
+    g = gpu_adjoint(x, f, N, m=m, window=window)
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= 1e-12
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, M, m=m, window=window, device=dev)
+    plan.set_points(torch.from_numpy(x).to(dev))
+    fl = plan.inverse(torch.from_numpy(g).to(dev)).cpu().numpy()
+    plan.close()
+    assert oracle.rel_l2_error(fl, oracle.nfft_inverse(x, g, N, m=m, window=wid)) <= 1e-12
+
+
+def test_fig12_precision_vs_m_all_windows():
+    """Fig. 12: E2 (Eq. 9) of the GPU transform (a) and its inverse (b)
+    against the direct sums for the four windows, m = 2 .. 8, M = 4096 points, N = 16^3,
+    sigma = 2.  The paper prints no values (shape only): E2 falls with m for every window,
+    Kaiser-Bessel is the most accurate, and every GPU value equals the CPU NFFT's."""
+    import json
+
+    from oracle import windows
+
+    setup = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_section4_setup.json")))
+    M, N = setup["M"], tuple(setup["N"])
+    x, f = inputs.uniform_points(M), inputs.uniform_values(M)
+    s = oracle.ndft_direct(x, f, N)
+    fl_ref = oracle.ndft_inverse_direct(x, s, N)
+    names = {"kb": windows.KAISER_BESSEL, "gaussian": windows.GAUSSIAN, "b_spline": windows.B_SPLINE,
+             "sinc_power": windows.SINC_POWER}
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    table = {}
+    for name, wid in names.items():
+        ea, eb = [], []
+        for m in range(2, 9):
+            plan = hp.Plan(N, M, m=m, window=name, device=dev)
+            plan.set_points(torch.from_numpy(x).to(dev))
+            g = plan.adjoint(torch.from_numpy(f).to(dev))
+            fl = plan.inverse(torch.from_numpy(s).to(dev)).cpu().numpy()
+            plan.close()
+            g = g.cpu().numpy()
+            assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= 1e-12
+            ea.append(oracle.rel_l2_error(g, s))
+            eb.append(oracle.rel_l2_error(fl, fl_ref))
+        table[name] = (ea, eb)
+        print(f"{name:10s} (a) " + " ".join(f"{e:.1e}" for e in ea) + "   (b) " + " ".join(f"{e:.1e}" for e in eb))
+        assert all(a > b for a, b in zip(ea[:4], ea[1:5])) and all(a > b for a, b in zip(eb[:4], eb[1:5]))
+    for i in range(1, 5):
+        assert table["kb"][0][i] < min(table[w][0][i] for w in names if w != "kb")

@@ -149,6 +149,70 @@ def test_O3_taps_strict_truncation():
     assert np.allclose(w2, ref, rtol=1e-13, atol=0)
 
 
+def test_O3_bspline_closed_forms_and_partition_of_unity():
+    """NEXT #3 B-spline window M_{2m} (Cox-de Boor): textbook values of M_2 (hat) and M_4 (cubic:
+    M_4(0) = 2/3, M_4(1) = 1/6, M_4(1/2) = 23/48), symmetry, unit integral, and the partition of
+    unity sum_l M_p(u - l) = 1; the C oracle's taps (a separate implementation) agree."""
+    u = np.linspace(-1, 1, 41)
+    assert np.allclose(windows.bspline(u, 2), 1 - np.abs(u), atol=1e-15, rtol=0)
+    assert windows.bspline(np.array([0.0, 1.0, -1.0, 0.5]), 4) == pytest.approx([2 / 3, 1 / 6, 1 / 6, 23 / 48], abs=1e-15)
+    for p in (4, 12, 16):
+        uu = np.random.default_rng(p).uniform(-3, 3, 25)
+        tot = sum(windows.bspline(uu - l, p) for l in range(-p, p + 1))
+        assert np.allclose(tot, 1.0, atol=1e-14, rtol=0)
+        assert np.allclose(windows.bspline(uu, p), windows.bspline(-uu, p), atol=1e-16, rtol=1e-14)
+        val, _ = integrate.quad(lambda v: windows.bspline(np.array([v]), p)[0], -p / 2, p / 2, points=list(range(-p // 2, p // 2 + 1)),
+                                epsabs=0, epsrel=1e-13, limit=200)
+        assert val == pytest.approx(1.0, abs=1e-13)
+    w, idx = oracle.taps_1d(32, 6, 2.0, windows.B_SPLINE, 0.123)
+    u0 = 32 * 0.123
+    assert np.allclose(w, windows.phi(u0 - np.arange(int(np.floor(u0)) - 5, int(np.floor(u0)) + 7), 6, 2.0,
+                                      windows.B_SPLINE), rtol=1e-13, atol=1e-16)
+
+
+@pytest.mark.parametrize("m", [2, 3, 6])
+def test_O3_bspline_fourier_pair_quadrature(m):
+    """Phi_hat(xi) = sinc(pi xi)^{2m} vs quadrature of M_{2m} (no truncation: support [-m, m])."""
+    for xi in [0.0, 0.07, 0.125, 0.25]:
+        val, _ = integrate.quad(lambda v: windows.phi(np.array([v]), m, 2.0, windows.B_SPLINE)[0] * np.cos(2 * np.pi * xi * v),
+                                -m, m, points=list(range(-m, m + 1)), epsabs=1e-15, epsrel=1e-13, limit=400)
+        ref = windows.phi_hat(xi, m, 2.0, windows.B_SPLINE)
+        assert abs(val - ref) <= 1e-13 * max(1.0, ref)
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_O3_sinc_power_fourier_pair_quadrature(m):
+    """Phi_hat(xi) = M_{2m}(xi / beta) / beta, beta = (2 sigma - 1)/(2 m sigma), vs quadrature of the
+    untruncated sinc^{2m}(pi beta u) (the transform of sinc is a box: a 2m-fold box convolution)."""
+    sigma = 2.0
+    beta = windows.sinc_beta(sigma, m)
+    f = lambda v: (np.sinc(beta * v)) ** (2 * m)   # np.sinc(y) = sin(pi y)/(pi y)
+    for xi in [0.0, 0.05, 0.1, 0.2]:
+        L = 4000.0
+        val, _ = integrate.quad(f, -L, L, weight="cos", wvar=2 * np.pi * xi, limit=4000) if xi else \
+            integrate.quad(f, -L, L, limit=4000, epsabs=0, epsrel=1e-13)
+        ref = windows.phi_hat(xi, m, sigma, windows.SINC_POWER)
+        assert abs(val - ref) <= 2e-7 * ref + 1e-12
+
+
+def test_O2_windows_accuracy_fig12_shape():
+    """Fig. 12's shape (values unpinned): on the §4 setup (M = 4096, N = 16^3,
+    sigma = 2) E2 of the CPU NFFT against the direct NDFT falls with m for all four windows, and
+    Kaiser-Bessel is the most accurate at every m >= 3."""
+    setup = json.load(open(os.path.join(GOLDEN, "paper_section4_setup.json")))
+    M, N, sigma = setup["M"], tuple(setup["N"]), setup["sigma"]
+    x, f = inputs.uniform_points(M), inputs.uniform_values(M)
+    s = oracle.ndft_direct(x, f, N)
+    E = {}
+    for win in (windows.KAISER_BESSEL, windows.GAUSSIAN, windows.B_SPLINE, windows.SINC_POWER):
+        E[win] = [oracle.rel_l2_error(oracle.nfft_adjoint(x, f, N, m=m, sigma=sigma, window=win), s) for m in range(2, 7)]
+        assert all(a > b for a, b in zip(E[win][:-1], E[win][1:])), (win, E[win])
+    for i in range(1, 5):
+        assert E[windows.KAISER_BESSEL][i] < min(E[w][i] for w in (windows.GAUSSIAN, windows.B_SPLINE, windows.SINC_POWER))
+    # B-spline: the classical (2 sigma - 1)^(-2m) decay
+    assert E[windows.B_SPLINE][4] < 4 * (2 * sigma - 1) ** (-12)
+
+
 # ------------------------------------------------------------------ O2 --
 def test_O2_spread_equals_lattice_gather():
     """oracle_spread (point-centric scatter) == per-lattice gather."""
@@ -156,7 +220,7 @@ def test_O2_spread_equals_lattice_gather():
     x[0] = [0.5, -0.5, 0.0]        # boundary and on-node coordinates
     f = inputs.uniform_values(20, seed=31)
     n = (16, 8, 16)
-    for win in (windows.KAISER_BESSEL, windows.GAUSSIAN):
+    for win in (windows.KAISER_BESSEL, windows.GAUSSIAN, windows.B_SPLINE, windows.SINC_POWER):
         a = oracle.spread(x, f, n, 3, 2.0, win)
         b = oracle.spread_naive_gather(x, f, n, 3, 2.0, win)
         assert oracle.rel_l2_error(a, b) < 1e-13
