@@ -179,7 +179,8 @@ const char* hpnfft_version(void);
  * |S(n)| = |fhat(n)| of Eq. 5 with f_i = q_i).
  *   q     : DEVICE [M] float64 real charges (this rank's points for a multi-GPU plan).
  *   L     : box side (> 0), alpha : Ewald parameter (> 0), in the same length unit.
- *   U     : DEVICE 1 float64, written in stream order (the sum over all ranks for a grid-slab plan).
+ *   U     : DEVICE 1 float64, written in stream order (the sum over all ranks for a grid-slab plan;
+ *           collective: every rank of a grid-slab plan must call it, it ends with an all-reduce).
  * Runs the adjoint's spread and FFT passes on f_i = q_i + 0i; the last FFT pass sums the weighted
  * |fhat|^2 instead of storing fhat (no fhat buffer); fixed-order reductions (deterministic).
  * Errors: E_INVALID (NULL, L or alpha <= 0), E_STATE (no set_points), E_UNSUPPORTED (a multi-GPU
