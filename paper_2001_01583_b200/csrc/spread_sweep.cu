@@ -47,6 +47,9 @@ constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
 #define HPNFFT_SWEEP_PROFILE 0  // measurement builds only: clock64 phase counters (HPNFFT_SWEEP_PROF=1)
 #endif
 constexpr bool kProf = HPNFFT_SWEEP_PROFILE != 0;
+#ifndef HPNFFT_SWEEP_LEANFLUSH
+#define HPNFFT_SWEEP_LEANFLUSH 1   // single-row-per-lane flush of short blocks (0: the generic loop)
+#endif
 #ifndef HPNFFT_SWEEP_DEBUG
 #define HPNFFT_SWEEP_DEBUG 0    // measurement builds only: 1 = skip the MMAs, 2 = skip apply
 #endif
@@ -804,6 +807,48 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     while (cur < upto) {
       const int nb = min(16, upto - cur);
       const int row0 = (cur - M_ + 1) & 15;
+#if HPNFFT_SWEEP_LEANFLUSH
+      if (nb <= 8) {
+        // a block of <= 8 steps (the per-chunk flush: CH steps) holds at most one of this lane's
+        // rows g, g + 8: one address computation, values picked by select
+        const int d0 = (g - row0) & 15, d1 = (g + 8 - row0) & 15;
+        const bool a0 = d0 < nb, a1 = d1 < nb;
+        if (a0 || a1) {
+          const int sp = cur + (a0 ? d0 : d1);
+          const int rel = sp - M_ + 1 - off;
+          const int l0 = (first + sp - M_ + 1) & (n0 - 1);
+          const bool in_seg = rel >= 0 && rel < S;
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) {
+            double2* base =
+                reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0[u] * n2 + (wc0[u] + t);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const double vx = a0 ? acc[u][nt][0] : acc[u][nt][2];
+              const double vy = a0 ? acc[u][nt][1] : acc[u][nt][3];
+              if (in_seg && wr0[u] + nt < n1) {
+                double2* dst = base + (size_t)nt * n2;
+                if (prm.accumulate) {
+                  double2 o = *dst;
+                  o.x += vx;
+                  o.y += vy;
+                  *dst = o;
+                } else {
+                  *dst = make_double2(vx, vy);
+                }
+              }
+              if (a0) {
+                acc[u][nt][0] = acc[u][nt][1] = 0.0;
+              } else {
+                acc[u][nt][2] = acc[u][nt][3] = 0.0;
+              }
+            }
+          }
+        }
+        cur += nb;
+        continue;
+      }
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int ds = (g + 8 * h - row0) & 15;     // step offset of this lane's row in the block
