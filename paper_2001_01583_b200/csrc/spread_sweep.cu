@@ -1116,7 +1116,12 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   bool merge = !INV && C::SUB == 1 && per_chunk < 64.0;
   if (const char* e = getenv("HPNFFT_SWEEP_MERGE")) merge = !INV && C::SUB == 1 && e[0] == '1';
   int cap = 32;
-  while (cap + 32 <= 511 && sweep_smem_bytes_of<P1, P2, M_>(cap + 32, merge) <= smem_max) cap += 32;
+  static const int cap_max = [] {   // HPNFFT_SWEEP_CAP: smaller ring stages (measurement)
+    const char* e = getenv("HPNFFT_SWEEP_CAP");
+    return e ? atoi(e) : 480;
+  }();
+  while (cap + 32 <= 511 && cap + 32 <= cap_max && sweep_smem_bytes_of<P1, P2, M_>(cap + 32, merge) <= smem_max)
+    cap += 32;
   const size_t smem = sweep_smem_bytes_of<P1, P2, M_>(cap, merge);
   SweepParams prm;
   prm.rec = p->rec;
