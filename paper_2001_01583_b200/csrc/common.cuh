@@ -13,7 +13,7 @@
 namespace hpnfft {
 
 constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
-constexpr int kMinM = 2;
+constexpr int kMinM = 1;
 constexpr int kPolyDeg = 14;      // window tap polynomial degree
 constexpr int kNumStages = 12;     // timing slots, see hpnfft_stage_times
 constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction

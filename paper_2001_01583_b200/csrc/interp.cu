@@ -121,6 +121,7 @@ int launch_interp(Plan* p, double* f) {
 
 int interpolate(Plan* p, double* f) {
   switch (p->m) {
+    case 1: return launch_interp<1>(p, f);
     case 2: return launch_interp<2>(p, f);
     case 3: return launch_interp<3>(p, f);
     case 4: return launch_interp<4>(p, f);

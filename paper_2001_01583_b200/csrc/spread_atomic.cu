@@ -61,6 +61,7 @@ int spread_atomic(Plan* p, const double* f) {
   size_t bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->grid, 0, bytes, p->stream), "zero grid");
   switch (p->m) {
+    case 1: return launch_atomic<1>(p, f);
     case 2: return launch_atomic<2>(p, f);
     case 3: return launch_atomic<3>(p, f);
     case 4: return launch_atomic<4>(p, f);

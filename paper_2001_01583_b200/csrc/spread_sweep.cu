@@ -1280,6 +1280,7 @@ bool sweep_supported(const Plan* p) {
 
 int interp_sweep(Plan* p, double* f) {
   switch (p->m) {
+    case 1: return run_interp_sweep<1>(p, f);
     case 2: return run_interp_sweep<2>(p, f);
     case 3: return run_interp_sweep<3>(p, f);
     case 4: return run_interp_sweep<4>(p, f);
@@ -1295,6 +1296,7 @@ int interp_sweep(Plan* p, double* f) {
 
 int spread_sweep(Plan* p, const double* f) {
   switch (p->m) {
+    case 1: return run_sweep<1>(p, f);
     case 2: return run_sweep<2>(p, f);
     case 3: return run_sweep<3>(p, f);
     case 4: return run_sweep<4>(p, f);

@@ -57,7 +57,7 @@ def test_ragged_noncubic(method, N):
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
 
 
-@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_all_cutoffs_match_cpu_nfft(m):
     N, M = (32, 32, 32), 2000
     x, f = inputs.uniform_points(M, seed=m), inputs.uniform_values(M, seed=m)
@@ -371,7 +371,7 @@ def test_inverse_config1():
     assert oracle.rel_l2_error(g, oracle.ndft_inverse_direct(x, fh, N)) <= 1e-9
 
 
-@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_inverse_all_cutoffs_ragged(m):
     N, M = (32, 16, 64), 1777
     x, fh = inputs.uniform_points(M, seed=40 + m), _spectrum(N, m)
@@ -664,7 +664,7 @@ def test_ewald_reciprocal_x_pass_variants(N):
 # ---- NEXT #3: B-spline and sinc-power windows; Fig. 12 ------------------------
 
 @pytest.mark.parametrize("window", ["b_spline", "sinc_power"])
-@pytest.mark.parametrize("m", [2, 4, 6, 8])
+@pytest.mark.parametrize("m", [1, 2, 4, 6, 8])
 def test_windows_bspline_sinc_power(window, m):
     """The GPU adjoint and inverse with the B-spline / sinc-power windows equal the CPU NFFT with
     the same window (same approximation) to 1e-12."""
@@ -687,7 +687,7 @@ def test_windows_bspline_sinc_power(window, m):
 
 def test_fig12_precision_vs_m_all_windows():
     """Fig. 12: E2 (Eq. 9) of the GPU transform (a) and its inverse (b)
-    against the direct sums for the four windows, m = 2 .. 8, M = 4096 points, N = 16^3,
+    against the direct sums for the four windows, m = 1 .. 8, M = 4096 points, N = 16^3,
     sigma = 2.  The paper prints no values (shape only): E2 falls with m for every window,
     Kaiser-Bessel is the most accurate, and every GPU value equals the CPU NFFT's."""
     import json
@@ -706,18 +706,20 @@ def test_fig12_precision_vs_m_all_windows():
     table = {}
     for name, wid in names.items():
         ea, eb = [], []
-        for m in range(2, 9):
+        for m in range(1, 9):
             plan = hp.Plan(N, M, m=m, window=name, device=dev)
             plan.set_points(torch.from_numpy(x).to(dev))
             g = plan.adjoint(torch.from_numpy(f).to(dev))
             fl = plan.inverse(torch.from_numpy(s).to(dev)).cpu().numpy()
             plan.close()
             g = g.cpu().numpy()
-            assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= 1e-12
+            # (m = 1: the Gaussian's exp(-u^2/b) with b = 0.42 is steep for the degree-14 tap
+            # polynomial, ~5e-11 relative; nine orders below that window's own E2 of ~1e-1)
+            assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= (1e-12 if m > 1 else 1e-10)
             ea.append(oracle.rel_l2_error(g, s))
             eb.append(oracle.rel_l2_error(fl, fl_ref))
         table[name] = (ea, eb)
         print(f"{name:10s} (a) " + " ".join(f"{e:.1e}" for e in ea) + "   (b) " + " ".join(f"{e:.1e}" for e in eb))
-        assert all(a > b for a, b in zip(ea[:4], ea[1:5])) and all(a > b for a, b in zip(eb[:4], eb[1:5]))
-    for i in range(1, 5):
+        assert all(a > b for a, b in zip(ea[:5], ea[1:6])) and all(a > b for a, b in zip(eb[:5], eb[1:6]))
+    for i in range(2, 6):
         assert table["kb"][0][i] < min(table[w][0][i] for w in names if w != "kb")
