@@ -100,6 +100,10 @@ static void free_plan(Plan* p) {
   cudaFree(p->rec);
   cudaFree(p->group_rows);
   cudaFree(p->tile_counter);
+  cudaFree(p->tile_sched);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->side_fork) cudaEventDestroy(p->side_fork);
+  if (p->side_join) cudaEventDestroy(p->side_join);
   cudaFree(p->err_flag);
   cudaFree(p->fq);
   cudaFree(p->e_partial);

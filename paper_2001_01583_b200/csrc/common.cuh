@@ -65,6 +65,11 @@ struct Plan {
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)
   int* group_rows = nullptr;      // [2] device scratch for the multi-group sweep (chunk range)
   int* tile_counter = nullptr;    // sweep tile scheduler counter
+  void* tile_sched = nullptr;     // sweep tile order: uint64 keys [16384] + int order [16384] (lazy)
+  cudaStream_t side = nullptr;    // side stream: the tile-order kernels overlap the records kernel
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
+  const int* sched_order = nullptr;   // tile order prepared for the next sweep launch (or null)
+  bool sched_pending = false;         // the next sweep must wait for side_join
   int* err_flag = nullptr;        // device [1 + 2 kRangeSlots]: range-error flag, then slot pairs of
                                   // min / max of the x-ordered cell c0
   cudaEvent_t flags_ev = nullptr;   // recorded after the flag read-back of an async set_points

@@ -118,6 +118,7 @@ struct SweepParams {
   int* tile_counter;       // dynamic tile scheduler (zeroed before the launch)
   unsigned long long* prof;   // optional clock64 phase counters (HPNFFT_SWEEP_PROF=1), else null
   double* fout;            // inverse direction: f [M][2] in original point order (atomically summed)
+  const int* order;        // tile processing order (largest record count first), or null
 };
 
 }  // namespace
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       if (lane == 0) t = atomicAdd(prm.tile_counter, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= ntiles) break;
+      if (prm.order) t = __ldg(prm.order + t);   // heaviest tiles first (clustered inputs)
       int R0, C0, L0, S, a_lo, nch;
       tile_geom(t, R0, C0, L0, S, a_lo, nch);
       bool skip = false;
@@ -1101,6 +1103,179 @@ int sweep_variant() {
   return v;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tile order for the persistent sweep: clustered inputs make a few tiles (the patches under a
+// cluster core) carry a large share of the records; taken in index order, one of them can start
+// late and leave every other SM idle (a tail of up to one heavy tile).  One warp per tile counts
+// the records the producer will copy (the same rows, bin runs and group clipping), then one CTA
+// sorts the tiles by count, largest first (longest-processing-time-first), unless the counts are
+// nearly uniform (max <= 2 x mean: index order, which keeps neighbouring tiles together).
+constexpr int kMaxOrderTiles = 16384;
+
+template <int P1, int P2, int M_>
+__global__ void __launch_bounds__(256) k_tile_counts(SweepParams prm, int ntiles, unsigned long long* keys) {
+  using C = SweepCfg<P1, P2, M_>;
+  constexpr int CH = Chunk<M_>::CH;
+  constexpr int LC = Chunk<M_>::LOG;
+  const int lane = threadIdx.x & 31;
+  const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (t >= ntiles) return;
+  const int n1 = prm.n1, n2 = prm.n2, nchunks0 = prm.n0 / CH;
+  const int npc = n2 / P2, npr = (n1 + P1 - 1) / P1;
+  const int pc = t % npc, rest = t / npc, pr = rest % npr, segi = rest / npr;
+  const int R0 = pr * P1, C0 = pc * P2;
+  const int L0 = prm.plane_lo + segi * prm.seg;
+  const int S = min(prm.seg, prm.plane_len - segi * prm.seg);
+  const int a_lo = floor_div(L0 - M_, CH);
+  const int nch = floor_div(L0 + S + M_ - 2, CH) - a_lo + 1;
+  // an estimate is enough to rank the tiles: the records of the patch's own rows and c2 bins
+  // (no footprint halo) in every other chunk -- ~5x fewer bin lookups than the producer makes
+  // lanes = 8 rows x 4 chunk phases (all 32 lanes busy, ~9 independent lookups each)
+  const int row = lane & 7, phase = lane >> 3;
+  const int c1 = (R0 + row) & (n1 - 1);
+  const int b2lo = C0 / kBinW, b2hi = (C0 + P2 - 1) / kBinW;
+  int ra0 = b2lo, rb0 = b2hi, ra1 = 0, rb1 = -1;
+  if (b2lo < 0) {
+    ra0 = 0;
+    ra1 = b2lo + prm.nb2;
+    rb1 = prm.nb2 - 1;
+  } else if (b2hi >= prm.nb2) {
+    rb0 = prm.nb2 - 1;
+    ra1 = 0;
+    rb1 = b2hi - prm.nb2;
+  }
+  uint32_t cnt = 0;
+  (void)sizeof(C);
+  if (row < P1) {
+#pragma unroll 4
+    for (int ci = 2 * phase; ci < nch; ci += 8) {
+      const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
+      const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
+      auto run = [&](int ra, int rb) {
+        if (rb < ra) return;
+        const uint32_t lo = max(__ldg(prm.start + ((rowbase + ra) << LC)), prm.g0);
+        const uint32_t hi = min(__ldg(prm.start + ((rowbase + rb + 1) << LC)), prm.g1);
+        cnt += hi > lo ? hi - lo : 0u;
+      };
+      run(ra0, rb0);
+      run(ra1, rb1);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) keys[t] = ((unsigned long long)cnt << 32) | (unsigned long long)(t + 1);
+}
+
+// one CTA: bitonic sort of the (count, tile + 1) keys, descending; padding keys are 0 (last)
+__global__ void __launch_bounds__(1024) k_tile_order(const unsigned long long* __restrict__ keys_in, int ntiles,
+                                                     int* __restrict__ order) {
+  extern __shared__ unsigned long long sk[];
+  __shared__ unsigned long long s_max, s_sum;
+  int P = 1;
+  while (P < ntiles) P <<= 1;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_sum = 0;
+  }
+  __syncthreads();
+  unsigned long long mx = 0, sm = 0;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const unsigned long long k = i < ntiles ? keys_in[i] : 0ull;
+    sk[i] = k;
+    mx = max(mx, k >> 32);
+    sm += k >> 32;
+  }
+  atomicMax(&s_max, mx);
+  atomicAdd(&s_sum, sm);
+  __syncthreads();
+  if (s_max * (unsigned long long)ntiles <= 2ull * s_sum) {   // nearly uniform: index order
+    for (int i = threadIdx.x; i < ntiles; i += blockDim.x) order[i] = i;
+    return;
+  }
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = sk[i], b = sk[l];
+          const bool desc = (i & k) == 0;   // descending overall
+          if (desc ? (a < b) : (a > b)) {
+            sk[i] = b;
+            sk[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < ntiles; i += blockDim.x) order[i] = (int)(sk[i] & 0xffffffffull) - 1;
+}
+
+// Tile order for the next sweep of group [g0, g1), computed on the plan's side stream so that
+// it overlaps the records kernel (it only needs the bin table of set_points).  HPNFFT_SWEEP_LPT=0
+// keeps index order.  Same plane range / segment geometry as launch_sweep_group.
+template <int P1, int P2, int M_>
+int prepare_tile_order(Plan* p, uint32_t g0, uint32_t g1) {
+  constexpr int CH = Chunk<M_>::CH;
+  p->sched_pending = false;
+  static const bool lpt_off = [] {
+    const char* e = getenv("HPNFFT_SWEEP_LPT");
+    return e && e[0] == '0';
+  }();
+  if (lpt_off) return HPNFFT_OK;
+  SweepParams prm{};
+  prm.start = p->bin_count;
+  prm.g0 = g0;
+  prm.g1 = g1;
+  prm.n0 = (int)p->n[0];
+  prm.n1 = (int)p->n[1];
+  prm.n2 = (int)p->n[2];
+  prm.nb2 = (int)(p->n[2] / kBinW);
+  const int64_t n0 = p->n[0];
+  const int64_t lo_al = p->plane_lo & ~(int64_t)(CH - 1);
+  int64_t len_al = p->plane_len + (p->plane_lo - lo_al);
+  len_al = (len_al + CH - 1) & ~(int64_t)(CH - 1);
+  if (len_al > n0) len_al = n0;
+  prm.plane_lo = (int)lo_al;
+  prm.plane_len = (int)len_al;
+  prm.seg = (int)(len_al < 256 ? len_al : 256);
+  prm.nseg = (int)((len_al + prm.seg - 1) / prm.seg);
+  const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
+  if (tiles <= 1 || tiles > kMaxOrderTiles) return HPNFFT_OK;
+  if (!p->tile_sched &&
+      cudaMalloc(&p->tile_sched, (sizeof(unsigned long long) + sizeof(int)) * kMaxOrderTiles) != cudaSuccess) {
+    cudaGetLastError();
+    p->tile_sched = nullptr;
+    return HPNFFT_OK;   // index order
+  }
+  if (!p->side) {
+    if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->side_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return HPNFFT_OK;
+    }
+  }
+  unsigned long long* keys = static_cast<unsigned long long*>(p->tile_sched);
+  int* order = reinterpret_cast<int*>(keys + kMaxOrderTiles);
+  HPNFFT_CUDA_TRY(p, cudaEventRecord(p->side_fork, p->stream), "fork tile order");
+  HPNFFT_CUDA_TRY(p, cudaStreamWaitEvent(p->side, p->side_fork, 0), "fork tile order");
+  k_tile_counts<P1, P2, M_><<<(unsigned)((tiles * 32 + 255) / 256), 256, 0, p->side>>>(prm, (int)tiles, keys);
+  int pad = 1;
+  while (pad < tiles) pad <<= 1;
+  const size_t osmem = sizeof(unsigned long long) * (size_t)pad;
+  HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_tile_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem),
+                  "tile order smem attr");
+  k_tile_order<<<1, 1024, osmem, p->side>>>(keys, (int)tiles, order);
+  p->launches += 2;
+  const int rc = check_launch(p, "tile order");
+  if (rc) return rc;
+  HPNFFT_CUDA_TRY(p, cudaEventRecord(p->side_join, p->side), "join tile order");
+  p->sched_order = order;
+  p->sched_pending = true;
+  return HPNFFT_OK;
+}
+
 template <int P1, int P2, int M_, bool INV = false>
 int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, bool accumulate, double* fout = nullptr) {
   using C = SweepCfg<P1, P2, M_>;
@@ -1163,6 +1338,16 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                   "sweep smem attr");
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
+  prm.order = nullptr;
+  if (p->sched_pending) {   // the tile order was computed on the side stream (prepare_tile_order)
+    HPNFFT_CUDA_TRY(p, cudaStreamWaitEvent(p->stream, p->side_join, 0), "join tile order");
+    static const bool dbg_unused = [] {   // HPNFFT_SWEEP_LPT_DEBUG=1: compute the order, do not use it
+      const char* e = getenv("HPNFFT_SWEEP_LPT_DEBUG");
+      return e && e[0] == '1';
+    }();
+    prm.order = dbg_unused ? nullptr : p->sched_order;
+    p->sched_pending = false;
+  }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t slots = (int64_t)sms * C::kCtasPerSm;
@@ -1198,6 +1383,15 @@ int run_sweep(Plan* p, const double* f) {
   do {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
+    {
+      const int v = sweep_variant();
+      const int rco = v == 4 ? prepare_tile_order<12, 16, M_>(p, g0, g1)
+                    : v == 3 ? prepare_tile_order<8, 16, M_>(p, g0, g1)
+                    : v == 1 ? prepare_tile_order<12, 32, M_>(p, g0, g1)
+                    : v == 2 ? prepare_tile_order<16, 16, M_>(p, g0, g1)
+                             : prepare_tile_order<8, 32, M_>(p, g0, g1);
+      if (rco) return rco;
+    }
     if (cnt > 0) {
       stage_begin(p, 7);
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
@@ -1239,6 +1433,10 @@ int run_interp_sweep(Plan* p, double* fout) {
   do {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
+    {
+      const int rco = prepare_tile_order<8, 32, M_>(p, g0, g1);
+      if (rco) return rco;
+    }
     if (cnt > 0) {
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
       HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_point_records<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
