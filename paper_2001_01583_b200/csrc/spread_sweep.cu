@@ -1341,11 +1341,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   prm.order = nullptr;
   if (p->sched_pending) {   // the tile order was computed on the side stream (prepare_tile_order)
     HPNFFT_CUDA_TRY(p, cudaStreamWaitEvent(p->stream, p->side_join, 0), "join tile order");
-    static const bool dbg_unused = [] {   // HPNFFT_SWEEP_LPT_DEBUG=1: compute the order, do not use it
-      const char* e = getenv("HPNFFT_SWEEP_LPT_DEBUG");
-      return e && e[0] == '1';
-    }();
-    prm.order = dbg_unused ? nullptr : p->sched_order;
+    prm.order = p->sched_order;
     p->sched_pending = false;
   }
   int sms = 148;
