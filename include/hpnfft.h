@@ -246,6 +246,35 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
  */
 int hpnfft_set_slabs(hpnfft_plan_t p, const int64_t* edges);
 
+/*
+ * One-GPU rank group: the ranks of a multi-GPU plan emulated as `nranks` plans on the caller's
+ * CURRENT device, for validating the exchange code where fewer GPUs than ranks exist (SURVEY.md
+ * §8(e); the driver's test box has one GPU).  Member r behaves exactly like rank r of
+ * hpnfft_plan_dist in `mode` (same partition rules, hpnfft_set_slabs, hpnfft_set_points,
+ * hpnfft_output_shape), except that
+ *   - HPNFFT_DIST_GRID_SLAB: the "peer grids" are the group's own plans' grids (no CUDA IPC) and
+ *     hpnfft_adjoint_group runs every exchange phase of the peer-memory path (spread, halo pull,
+ *     z pass, y pass with stores into the destination members' grids, x pass) for ALL members
+ *     before the next phase starts, in stream order on the one stream: the cross-GPU flag
+ *     barriers of the real path are replaced by that order, so no kernel ever waits for another;
+ *   - option A (ALLREDUCE, REDUCE_ROOT0, REDUCE_SCATTER): every member's partial fhat (Eq. 8 term)
+ *     is summed by a device kernel into the same result layout as the NCCL collective.
+ *   out : HOST array of nranks handles (filled in rank order; all NULL on failure).
+ *   M   : HOST int64[nranks], member r's point count.  Other arguments as hpnfft_plan.
+ * All members must stay on one stream and be destroyed together (hpnfft_destroy each).
+ * Errors: those of hpnfft_plan / hpnfft_plan_dist (no NCCL is needed).
+ */
+int hpnfft_plan_group(hpnfft_plan_t* out, int d, const int64_t* N, const int64_t* M, int m, double sigma, int window,
+                      void* stream, int nranks, int mode);
+
+/*
+ * The adjoint of a one-GPU rank group: f[r] (DEVICE, member r's values in its set_points order)
+ * -> fhat[r] (DEVICE, member r's output block, shape hpnfft_output_shape).  plans/f/fhat are HOST
+ * arrays of nranks pointers in rank order.  Errors: E_INVALID (not one group in rank order, or
+ * members on different streams), E_STATE (a member without set_points), E_CUDA.  Asynchronous.
+ */
+int hpnfft_adjoint_group(hpnfft_plan_t* plans, int nranks, const double* const* f, double* const* fhat);
+
 /* Shape (HOST int64[3]) of the fhat block hpnfft_adjoint writes on this rank (see the modes). */
 int hpnfft_output_shape(hpnfft_plan_t p, int64_t shape[3]);
 

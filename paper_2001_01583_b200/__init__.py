@@ -97,6 +97,11 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_ewald_reciprocal.restype = ctypes.c_int
     lib.hpnfft_set_slabs.argtypes = [vp, i64p]
     lib.hpnfft_set_slabs.restype = ctypes.c_int
+    lib.hpnfft_plan_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, i64p, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_int, vp, ctypes.c_int, ctypes.c_int]
+    lib.hpnfft_plan_group.restype = ctypes.c_int
+    lib.hpnfft_adjoint_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    lib.hpnfft_adjoint_group.restype = ctypes.c_int
     lib.hpnfft_output_shape.argtypes = [vp, i64p]
     lib.hpnfft_output_shape.restype = ctypes.c_int
     _lib = lib
@@ -133,7 +138,8 @@ class Plan:
     and adjoint() returns this rank's block of fhat (out_shape).
     """
 
-    def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None, dist=None):
+    def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None, dist=None,
+                 _handle=None):
         import torch
 
         lib = load_library()
@@ -149,7 +155,9 @@ class Plan:
         arr = (ctypes.c_int64 * len(self.N))(*self.N)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            if dist is None:
+            if _handle is not None:   # a member of a PlanGroup (created by hpnfft_plan_group)
+                h = ctypes.c_void_p(_handle)
+            elif dist is None:
                 _check(lib.hpnfft_plan(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window,
                                        _stream_ptr(stream)))
             else:
@@ -288,6 +296,64 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+class PlanGroup:
+    """hpnfft_plan_group: the `nranks` ranks of a multi-GPU plan (mode as DIST_MODES) emulated as
+    plans on ONE GPU, for validating the exchange code with fewer GPUs than ranks.  members[r]
+    is a Plan (set_slabs, set_points, out_shape as rank r); adjoint(fs) runs every exchange phase
+    for all members before the next (hpnfft_adjoint_group) and returns the members' output
+    blocks.  Ms: the members' point counts."""
+
+    def __init__(self, N, Ms, m: int = 6, sigma: float = 2.0, window="kb", mode="grid_slab", device=None):
+        import torch
+
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("hpnfft needs a CUDA device (there is no CPU path)")
+        self.N = tuple(int(v) for v in N)
+        self.P = len(Ms)
+        self.mode = DIST_MODES[mode] if isinstance(mode, str) else int(mode)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        win = WINDOWS[window] if isinstance(window, str) else int(window)
+        arr = (ctypes.c_int64 * len(self.N))(*self.N)
+        marr = (ctypes.c_int64 * self.P)(*[int(v) for v in Ms])
+        hs = (ctypes.c_void_p * self.P)()
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.current_stream(self.device)
+            _check(lib.hpnfft_plan_group(hs, len(self.N), arr, marr, int(m), float(sigma), win,
+                                         ctypes.c_void_p(self.stream.cuda_stream), self.P, self.mode))
+        self.members = [Plan(self.N, int(Ms[r]), m=m, sigma=sigma, window=window, stream=self.stream,
+                             device=self.device, _handle=hs[r]) for r in range(self.P)]
+
+    def set_slabs(self, edges):
+        for p in self.members:
+            p.set_slabs(edges)
+
+    def set_points(self, xs):
+        for p, x in zip(self.members, xs):
+            p.set_points(x)
+
+    def adjoint(self, fs):
+        import torch
+
+        outs, fp, op, hs = [], (ctypes.c_void_p * self.P)(), (ctypes.c_void_p * self.P)(), (ctypes.c_void_p * self.P)()
+        keep = []
+        for r, (p, f) in enumerate(zip(self.members, fs)):
+            if not (f.is_cuda and f.dtype == torch.complex128 and f.numel() == p.M):
+                raise TypeError("f must be a CUDA complex128 tensor with M elements")
+            f = f.contiguous()
+            keep.append(f)
+            o = torch.empty(p.out_shape, dtype=torch.complex128, device=self.device)
+            outs.append(o)
+            fp[r], op[r], hs[r] = f.data_ptr(), o.data_ptr(), p._h.value
+        with torch.cuda.stream(self.stream):
+            _check(load_library().hpnfft_adjoint_group(hs, self.P, fp, op))
+        return outs
+
+    def close(self):
+        for p in self.members:
+            p.close()
 
 
 class HostPipeline:

@@ -9,7 +9,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
 #include <string>
 
 #include "common.cuh"
@@ -24,6 +27,37 @@ int fail(Plan* p, int code, const std::string& msg) {
   set_error(msg);
   if (p && (code == HPNFFT_E_CUDA || code == HPNFFT_E_NCCL)) p->failed = true;
   return code;
+}
+
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;
+  }
+  if (cache[dev] == 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+      cudaGetLastError();
+      sms = 148;
+    }
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
+
+cudaError_t set_max_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[std::make_pair(func, dev)];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 int check_launch(Plan* p, const char* what) {
@@ -177,7 +211,7 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     return HPNFFT_E_INVALID;
   }
   if (m < kMinM || m > kMaxM) {
-    set_error("m must be in [2, 8] for the GPU kernels");
+    set_error("m must be in [" + std::to_string(kMinM) + ", " + std::to_string(kMaxM) + "] for the GPU kernels");
     return HPNFFT_E_UNSUPPORTED;
   }
   int64_t n[3];

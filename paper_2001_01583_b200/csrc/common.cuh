@@ -12,9 +12,10 @@
 
 namespace hpnfft {
 
-constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = 2..kMaxM
+constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = kMinM..kMaxM
 constexpr int kMinM = 1;
-constexpr int kPolyDeg = 14;      // window tap polynomial degree
+constexpr int kPolyDeg = 18;      // window tap polynomial degree (<= 2e-14
+                                  // of Phi(0) for every window and m = 1..15, incl. the steep m = 1 Gaussian)
 constexpr int kNumStages = 12;     // timing slots, see hpnfft_stage_times
 constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction
 
@@ -94,6 +95,8 @@ struct Plan {
   double* partial = nullptr;    // REDUCE_SCATTER: this rank's full partial fhat
   // GRID_SLAB over NVLink peer memory (CUDA IPC): the ranks' grids and barrier flags
   bool p2p = false;
+  bool virt = false;                  // member of a one-GPU rank group (hpnfft_plan_group): peers are
+                                      // the group's own plans, stream order replaces the barriers
   double** peer_grid = nullptr;       // device array [nranks] (own grid at dist_rank)
   double* peer_grid_host[16] = {};    // host copies (opened IPC pointers, closed at destroy)
   uint32_t* flags = nullptr;          // device [64]: barrier epochs written by the peers
@@ -116,6 +119,12 @@ struct Plan {
 void set_error(const std::string& msg);
 int fail(Plan* p, int code, const std::string& msg);
 
+// SM count of the calling thread's current device (cached per device)
+int device_sm_count();
+// raise a kernel's dynamic shared-memory limit to `bytes` on the current device (the attribute is
+// set only when it grows: no driver call per launch)
+cudaError_t set_max_smem(const void* func, size_t bytes);
+
 // Launch-error check helper: returns HPNFFT_OK or records the CUDA error on the plan.
 int check_launch(Plan* p, const char* what);
 
@@ -126,6 +135,9 @@ void stage_end(Plan* p, int slot);
 // kernels' host launchers (each returns HPNFFT_OK or an error code)
 int build_tables(Plan* p);
 int sort_points(Plan* p, const double* x);
+// bin keys [k_lo, k_hi) this plan's points may use (a grid-slab rank: its own planes' keys only;
+// the bin table is zeroed and scanned over that range only, sort.cu)
+void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi);
 int spread_atomic(Plan* p, const double* f);
 int spread_sweep(Plan* p, const double* f);
 bool sweep_supported(const Plan* p);
@@ -140,6 +152,11 @@ int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int
              int64_t o_start, int64_t o_total, int a_lo, int a_len, double* const* peers = nullptr, int NP = 1);
 // multi-GPU exchange steps (dist.cu)
 int dist_adjoint(Plan* p, const double* f, double* fhat);
+// grid-slab exchange phases over peer memory (dist.cu; one rank each)
+int slab_phase_halo(Plan* p);
+int slab_phase_z(Plan* p);
+int slab_phase_y(Plan* p);
+int slab_phase_x(Plan* p, double* fhat);
 void dist_free(Plan* p);
 int dist_allreduce_sum(Plan* p, double* buf, int64_t count);
 int spread(Plan* p, const double* f);

@@ -276,9 +276,11 @@ __global__ void k_xbarrier(uint32_t* const* peer_flags, int P, int r, uint32_t e
 
 // my owned planes += the same memory planes of the neighbours' grids (their halo regions)
 __global__ void k_halo_pull(double2* __restrict__ grid, const double2* __restrict__ from_upper,
-                            const double2* __restrict__ from_lower, int64_t plane_elems, PlaneMap map, int n_upper) {
+                            const double2* __restrict__ from_lower, int64_t plane_elems, PlaneMap map, int n_upper,
+                            const int* __restrict__ abort_flag) {
   const int j = blockIdx.y;
   if (j >= map.count) return;
+  if (abort_flag && *abort_flag) return;   // a cross-GPU barrier timed out: touch no peer memory
   const size_t off = (size_t)map.plane[j] * plane_elems;
   double2* dst = grid + off;
   const double2* src = (j < n_upper ? from_upper : from_lower) + off;
@@ -292,107 +294,179 @@ __global__ void k_halo_pull(double2* __restrict__ grid, const double2* __restric
 }
 
 int xbarrier(Plan* p) {
+  if (p->virt) return HPNFFT_OK;   // one-GPU rank group: stream order is the barrier
   ++p->epoch;
   k_xbarrier<<<1, 32, 0, p->stream>>>(p->peer_flags, p->nranks, p->dist_rank, p->epoch, p->dist_err);
   p->launches++;
   return check_launch(p, "cross-GPU barrier");
 }
 
-int slab_adjoint_p2p(Plan* p, double* fhat) {
+}  // namespace
+
+// The grid-slab adjoint over peer memory in four phases.  A real rank runs them back to back
+// (slab_adjoint_p2p) with cross-GPU flag barriers where a phase reads or writes a peer's grid; a
+// one-GPU rank group (hpnfft_plan_group) runs each phase for every rank before the next phase.
+// 1. halo: after every rank's sweep, pull the neighbours' halo planes into my own planes
+int slab_phase_halo(Plan* p) {
   const int P = p->nranks, r = p->dist_rank, m = p->m;
-  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2], pe = n1 * n2;
-  const int64_t N1 = p->N[1], N2 = p->N[2], N1P = N1 / P;
-  const int64_t lo = p->slab_lo, L = p->slab_len, l0 = mem_plane(lo, n0);
-  int rc;
-  // 1. halo: after every rank's sweep, pull the neighbours' halo planes into my own planes
+  const int64_t n0 = p->n[0], pe = p->n[1] * p->n[2];
+  const int64_t lo = p->slab_lo, L = p->slab_len;
   stage_begin(p, 8);
-  rc = xbarrier(p);
+  int rc = xbarrier(p);
   if (rc) return rc;
-  {
-    PlaneMap map;
-    map.count = 2 * m - 1;
-    for (int j = 0; j < m - 1; ++j) map.plane[j] = (int)mem_plane(lo + L - (m - 1) + j, n0);   // from rank r+1
-    for (int j = 0; j < m; ++j) map.plane[m - 1 + j] = (int)mem_plane(lo + j, n0);           // from rank r-1
-    dim3 g((unsigned)((pe + 255) / 256 < 512 ? (pe + 255) / 256 : 512), (unsigned)map.count);
-    k_halo_pull<<<g, 256, 0, p->stream>>>(reinterpret_cast<double2*>(p->grid),
-                                         reinterpret_cast<const double2*>(p->peer_grid_host[(r + 1) % P]),
-                                         reinterpret_cast<const double2*>(p->peer_grid_host[(r - 1 + P) % P]), pe, map,
-                                         m - 1);
-    p->launches++;
-    rc = check_launch(p, "halo pull");
-    if (rc) return rc;
-  }
+  PlaneMap map;
+  map.count = 2 * m - 1;
+  for (int j = 0; j < m - 1; ++j) map.plane[j] = (int)mem_plane(lo + L - (m - 1) + j, n0);   // from rank r+1
+  for (int j = 0; j < m; ++j) map.plane[m - 1 + j] = (int)mem_plane(lo + j, n0);           // from rank r-1
+  dim3 g((unsigned)((pe + 255) / 256 < 512 ? (pe + 255) / 256 : 512), (unsigned)map.count);
+  k_halo_pull<<<g, 256, 0, p->stream>>>(reinterpret_cast<double2*>(p->grid),
+                                       reinterpret_cast<const double2*>(p->peer_grid_host[(r + 1) % P]),
+                                       reinterpret_cast<const double2*>(p->peer_grid_host[(r - 1 + P) % P]), pe, map,
+                                       m - 1, p->virt ? nullptr : p->dist_err);
+  p->launches++;
+  rc = check_launch(p, "halo pull");
   stage_end(p, 8);
-  // 2. z pass on the own planes (the grid is read for the last time)
+  return rc;
+}
+
+// 2. z pass on the own planes (the grid is read for the last time)
+int slab_phase_z(Plan* p) {
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  const int64_t L = p->slab_len, l0 = mem_plane(p->slab_lo, n0);
   stage_begin(p, 4);
-  rc = fft_pass(p, 2, p->grid, p->bufA, L * n1, 1, true, l0 * n1, n0 * n1, 0, (int)n2);
+  const int rc = fft_pass(p, 2, p->grid, p->bufA, L * n1, 1, true, l0 * n1, n0 * n1, 0, (int)n2);
   stage_end(p, 4);
-  if (rc) return rc;
-  // 3. every rank has finished reading its grid: the y pass stores into the destination ranks'
-  //    grids ([n0][N1/P][N2] receive layout) over NVLink, then everyone waits for everyone
+  return rc;
+}
+
+// 3. every rank has finished reading its grid: the y pass stores into the destination ranks'
+//    grids ([n0][N1/P][N2] receive layout) over NVLink, then everyone waits for everyone
+int slab_phase_y(Plan* p) {
+  const int P = p->nranks;
+  const int64_t n0 = p->n[0], n1 = p->n[1];
+  const int64_t N2 = p->N[2], N1P = p->N[1] / P;
+  const int64_t L = p->slab_len, l0 = mem_plane(p->slab_lo, n0);
   stage_begin(p, 9);
-  rc = xbarrier(p);
+  int rc = xbarrier(p);
   stage_end(p, 9);
   if (rc) return rc;
   stage_begin(p, 5);
   rc = fft_pass(p, 1, p->bufA, p->grid, L, N2, false, l0, n0, 0, (int)n1, p->peer_grid, (int)N1P);
   if (!rc) rc = xbarrier(p);
   stage_end(p, 5);
-  if (rc) return rc;
-  // 4. x pass on the own k1 slab
+  return rc;
+}
+
+// 4. x pass (+ deconvolve, or the Eq. 12 energy sum) on the own k1 slab
+int slab_phase_x(Plan* p, double* fhat) {
+  const int64_t n0 = p->n[0], N2 = p->N[2], N1P = p->N[1] / p->nranks;
   stage_begin(p, 6);
-  rc = x_pass(p, p->grid, fhat, N1P * N2, (int64_t)r * N1P, 0, (int)n0);
+  const int rc = x_pass(p, p->grid, fhat, N1P * N2, (int64_t)p->dist_rank * N1P, 0, (int)n0);
   stage_end(p, 6);
   return rc;
 }
 
-// map the peers' grids and barrier flags (CUDA IPC, handles exchanged with ncclAllGather);
-// returns false (and leaves p->p2p unset) when peer memory is not available
-bool setup_p2p(Plan* p) {
+namespace {
+
+int slab_adjoint_p2p(Plan* p, double* fhat) {
+  int rc = slab_phase_halo(p);
+  if (!rc) rc = slab_phase_z(p);
+  if (!rc) rc = slab_phase_y(p);
+  if (!rc) rc = slab_phase_x(p, fhat);
+  return rc;
+}
+
+// map the peers' grids and barrier flags (CUDA IPC, handles exchanged with ncclAllGather).
+// Collective and consistent: every rank reaches both collectives whatever happens locally (an
+// allocation, a handle export or an open that fails), and the ranks agree on the outcome (the
+// minimum over the ranks of a local ok flag), so that all of them take the same exchange protocol
+// (peer memory or NCCL send/recv).  `want` = this rank's HPNFFT_DIST_P2P choice (also agreed).
+bool setup_p2p(Plan* p, bool want) {
   const NcclApi* a = nccl();
   const int P = p->nranks, r = p->dist_rank;
-  if (P > 16) return false;
-  if (cudaMalloc(&p->flags, 64 * sizeof(uint32_t)) != cudaSuccess) return false;
-  cudaMemset(p->flags, 0, 64 * sizeof(uint32_t));
-  cudaMalloc(&p->dist_err, sizeof(int));
-  cudaMemset(p->dist_err, 0, sizeof(int));
-  cudaIpcMemHandle_t h[2];
-  if (cudaIpcGetMemHandle(&h[0], p->grid) != cudaSuccess || cudaIpcGetMemHandle(&h[1], p->flags) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+  struct Msg {
+    cudaIpcMemHandle_t h[2];
+    int ok;
+    int pad;
+  };
+  Msg mine;
+  memset(&mine, 0, sizeof(mine));
+  bool ok = want && P <= 16;
+  ok = ok && cudaMalloc(&p->flags, 64 * sizeof(uint32_t)) == cudaSuccess;
+  ok = ok && cudaMemset(p->flags, 0, 64 * sizeof(uint32_t)) == cudaSuccess;
+  ok = ok && cudaMalloc(&p->dist_err, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMemset(p->dist_err, 0, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaIpcGetMemHandle(&mine.h[0], p->grid) == cudaSuccess &&
+       cudaIpcGetMemHandle(&mine.h[1], p->flags) == cudaSuccess;
+  cudaGetLastError();
+  mine.ok = ok ? 1 : 0;
+  // device scratch for the two collectives: the (not yet used) grid when it is large enough
+  const size_t hb = sizeof(Msg), need = hb * (size_t)(P + 1) + 2 * sizeof(int);
+  const size_t grid_bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
+  unsigned char* dbuf = reinterpret_cast<unsigned char*>(p->grid);
+  bool own = false;
+  if (grid_bytes < need) {
+    own = true;
+    if (cudaMalloc(&dbuf, need) != cudaSuccess) dbuf = nullptr;   // tiny grids only
   }
-  unsigned char* dbuf = nullptr;
-  const size_t hb = sizeof(h);
-  if (cudaMalloc(&dbuf, hb * (P + 1)) != cudaSuccess) return false;
-  cudaMemcpy(dbuf + hb * P, h, hb, cudaMemcpyHostToDevice);
-  bool ok = a->AllGather(dbuf + hb * P, dbuf, hb, 0 /* ncclInt8 */, p->comm, p->stream) == 0;
   std::vector<unsigned char> all(hb * P);
-  ok = ok && cudaStreamSynchronize(p->stream) == cudaSuccess &&
-       cudaMemcpy(all.data(), dbuf, hb * P, cudaMemcpyDeviceToHost) == cudaSuccess;
-  cudaFree(dbuf);
-  for (int s = 0; s < P && ok; ++s) {
+  bool coll = dbuf != nullptr && cudaMemcpy(dbuf + hb * P, &mine, hb, cudaMemcpyHostToDevice) == cudaSuccess;
+  coll = a->AllGather(dbuf + hb * P, dbuf, hb, 0 /* ncclInt8 */, p->comm, p->stream) == 0 && coll;
+  coll = coll && cudaStreamSynchronize(p->stream) == cudaSuccess &&
+         cudaMemcpy(all.data(), dbuf, hb * P, cudaMemcpyDeviceToHost) == cudaSuccess;
+  bool all_ok = coll;
+  for (int s = 0; s < P && all_ok; ++s) all_ok = reinterpret_cast<const Msg*>(all.data() + hb * s)->ok == 1;
+  bool opened = all_ok;
+  for (int s = 0; s < P && opened; ++s) {
     if (s == r) {
       p->peer_grid_host[s] = p->grid;
       p->peer_flags_host[s] = p->flags;
       continue;
     }
-    cudaIpcMemHandle_t hs[2];
-    memcpy(hs, all.data() + hb * s, hb);
+    const Msg* ms = reinterpret_cast<const Msg*>(all.data() + hb * s);
     void* g = nullptr;
     void* fl = nullptr;
-    ok = cudaIpcOpenMemHandle(&g, hs[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
-         cudaIpcOpenMemHandle(&fl, hs[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
-    p->peer_grid_host[s] = static_cast<double*>(g);
-    p->peer_flags_host[s] = static_cast<uint32_t*>(fl);
+    opened = cudaIpcOpenMemHandle(&g, ms->h[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    if (opened) p->peer_grid_host[s] = static_cast<double*>(g);
+    opened = opened && cudaIpcOpenMemHandle(&fl, ms->h[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    if (opened) p->peer_flags_host[s] = static_cast<uint32_t*>(fl);
   }
-  if (ok) {
-    ok = cudaMalloc(&p->peer_grid, sizeof(double*) * P) == cudaSuccess &&
-         cudaMalloc(&p->peer_flags, sizeof(uint32_t*) * P) == cudaSuccess &&
-         cudaMemcpy(p->peer_grid, p->peer_grid_host, sizeof(double*) * P, cudaMemcpyHostToDevice) == cudaSuccess &&
-         cudaMemcpy(p->peer_flags, p->peer_flags_host, sizeof(uint32_t*) * P, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (opened) {
+    opened = cudaMalloc(&p->peer_grid, sizeof(double*) * P) == cudaSuccess &&
+             cudaMalloc(&p->peer_flags, sizeof(uint32_t*) * P) == cudaSuccess &&
+             cudaMemcpy(p->peer_grid, p->peer_grid_host, sizeof(double*) * P, cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(p->peer_flags, p->peer_flags_host, sizeof(uint32_t*) * P, cudaMemcpyHostToDevice) == cudaSuccess;
   }
   cudaGetLastError();
-  return ok;
+  // agreement on the outcome: min over the ranks (every rank reaches this all-reduce)
+  int agreed = opened ? 1 : 0;
+  if (dbuf) {
+    int* d = reinterpret_cast<int*>(dbuf + hb * (size_t)(P + 1));
+    bool c2 = cudaMemcpy(d, &agreed, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+    c2 = a->AllReduce(d, d + 1, 1, 2 /* ncclInt32 */, 3 /* ncclMin */, p->comm, p->stream) == 0 && c2;
+    c2 = c2 && cudaStreamSynchronize(p->stream) == cudaSuccess &&
+         cudaMemcpy(&agreed, d + 1, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (!c2) agreed = 0;
+  } else {
+    agreed = 0;
+  }
+  if (own && dbuf) cudaFree(dbuf);
+  cudaGetLastError();
+  if (!agreed) {   // everyone falls back to NCCL send/recv: release what this rank mapped
+    for (int s = 0; s < 16; ++s) {
+      if (s != r && p->peer_grid_host[s]) cudaIpcCloseMemHandle(p->peer_grid_host[s]);
+      if (s != r && p->peer_flags_host[s]) cudaIpcCloseMemHandle(p->peer_flags_host[s]);
+      p->peer_grid_host[s] = nullptr;
+      p->peer_flags_host[s] = nullptr;
+    }
+    cudaFree(p->peer_grid);
+    cudaFree(p->peer_flags);
+    p->peer_grid = nullptr;
+    p->peer_flags = nullptr;
+    cudaGetLastError();
+    return false;
+  }
+  return true;
 }
 
 }  // namespace
@@ -452,9 +526,11 @@ int dist_allreduce_sum(Plan* p, double* buf, int64_t count) {
 
 void dist_free(Plan* p) {
   for (int s = 0; s < 16; ++s) {
-    if (s == p->dist_rank) continue;
+    if (s == p->dist_rank || p->virt) continue;   // a rank group's peers are its own plans' grids
     if (p->peer_grid_host[s]) cudaIpcCloseMemHandle(p->peer_grid_host[s]);
     if (p->peer_flags_host[s]) cudaIpcCloseMemHandle(p->peer_flags_host[s]);
+  }
+  for (int s = 0; s < 16; ++s) {
     p->peer_grid_host[s] = nullptr;
     p->peer_flags_host[s] = nullptr;
   }
@@ -496,42 +572,37 @@ int hpnfft_get_unique_id(unsigned char id[128]) {
   return HPNFFT_OK;
 }
 
-int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_local, int m, double sigma, int window,
-                     void* stream, int nranks, int rank, const unsigned char id[128], int mode) {
-  if (!out) {
-    set_error("hpnfft_plan_dist: out is NULL");
-    return HPNFFT_E_INVALID;
-  }
-  *out = nullptr;
-  if (nranks < 1 || rank < 0 || rank >= nranks || !id) {
-    set_error("hpnfft_plan_dist: need 0 <= rank < nranks and a unique id");
+}  // extern "C"
+
+namespace hpnfft {
+namespace {
+
+// validation shared by hpnfft_plan_dist and hpnfft_plan_group (before anything is created)
+int check_dist_args(const char* fn, int nranks, int mode) {
+  if (nranks < 1 || nranks > 16) {
+    set_error(std::string(fn) + ": need 1 <= nranks <= 16");
     return HPNFFT_E_INVALID;
   }
   if (mode < HPNFFT_DIST_ALLREDUCE || mode > HPNFFT_DIST_GRID_SLAB) {
-    set_error("hpnfft_plan_dist: unknown mode");
+    set_error(std::string(fn) + ": unknown mode");
     return HPNFFT_E_INVALID;
   }
-  hpnfft_plan_t h = nullptr;
-  int rc = hpnfft_plan(&h, d, N, M_local, m, sigma, window, stream);
-  if (rc) return rc;
-  Plan* p = reinterpret_cast<Plan*>(h);
+  return HPNFFT_OK;
+}
+
+// rank `rank` of `nranks` in `mode` on a freshly created plan: mode constraints, the equal-size
+// slabs, the bin table reset, the exchange buffers (no communication)
+int init_dist_fields(Plan* p, int nranks, int rank, int mode) {
   const int64_t n0 = p->n[0];
+  const int m = p->m;
   if (mode == HPNFFT_DIST_REDUCE_SCATTER && p->N[0] % nranks) {
-    hpnfft_destroy(h);
     set_error("HPNFFT_DIST_REDUCE_SCATTER needs N0 % nranks == 0");
     return HPNFFT_E_UNSUPPORTED;
   }
   if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1 &&
       (!is_pow2(nranks) || p->N[1] % nranks || n0 / nranks < 2 * m || n0 % nranks)) {
-    hpnfft_destroy(h);
     set_error("HPNFFT_DIST_GRID_SLAB needs nranks a power of two, N1 % nranks == 0 and n0 / nranks >= 2m");
     return HPNFFT_E_UNSUPPORTED;
-  }
-  const NcclApi* a = nccl();
-  if (!a->ok) {
-    hpnfft_destroy(h);
-    set_error("NCCL (libnccl.so.2) could not be loaded");
-    return HPNFFT_E_NCCL;
   }
   p->dist_mode = mode;
   p->nranks = nranks;
@@ -542,9 +613,71 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
   // grid-slab ranks zero and scan only their own key range per set_points (sort.cu key_range):
   // the rest of the bin table must read as empty
   if (cudaMemset(p->bin_count, 0, sizeof(uint32_t) * (size_t)(p->nbins + 1)) != cudaSuccess) {
-    hpnfft_destroy(h);
+    cudaGetLastError();
     set_error("bin table initialisation failed");
     return HPNFFT_E_CUDA;
+  }
+  cudaError_t e = cudaSuccess;
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1)
+    e = cudaMalloc(&p->halo, sizeof(double) * 2 * (size_t)(2 * m - 1) * (size_t)(p->n[1] * p->n[2]));
+  if (mode == HPNFFT_DIST_REDUCE_SCATTER && nranks > 1)
+    e = cudaMalloc(&p->partial, sizeof(double) * 2 * (size_t)(p->N[0] * p->N[1] * p->N[2]));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation of the exchange buffers failed");
+    return HPNFFT_E_NOMEM;
+  }
+  return HPNFFT_OK;
+}
+
+// dst[i] += src[i] (the option-A sum of a one-GPU rank group)
+__global__ void k_add_into(double* __restrict__ dst, const double* __restrict__ src, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+int add_into(Plan* p, double* dst, const double* src, int64_t count) {
+  const int64_t blocks = (count + 255) / 256 < 4096 ? (count + 255) / 256 : 4096;
+  if (count <= 0) return HPNFFT_OK;
+  k_add_into<<<(unsigned)blocks, 256, 0, p->stream>>>(dst, src, count);
+  p->launches++;
+  return check_launch(p, "group sum");
+}
+
+}  // namespace
+}  // namespace hpnfft
+
+extern "C" {
+
+int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_local, int m, double sigma, int window,
+                     void* stream, int nranks, int rank, const unsigned char id[128], int mode) {
+  if (!out) {
+    set_error("hpnfft_plan_dist: out is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  *out = nullptr;
+  int rc = check_dist_args("hpnfft_plan_dist", nranks, mode);
+  if (rc) return rc;
+  if (rank < 0 || rank >= nranks || !id) {
+    set_error("hpnfft_plan_dist: need 0 <= rank < nranks and a unique id");
+    return HPNFFT_E_INVALID;
+  }
+  hpnfft_plan_t h = nullptr;
+  rc = hpnfft_plan(&h, d, N, M_local, m, sigma, window, stream);
+  if (rc) return rc;
+  Plan* p = reinterpret_cast<Plan*>(h);
+  const NcclApi* a = nccl();
+  if (!a->ok) {
+    hpnfft_destroy(h);
+    set_error("NCCL (libnccl.so.2) could not be loaded");
+    return HPNFFT_E_NCCL;
+  }
+  rc = init_dist_fields(p, nranks, rank, mode);
+  if (rc) {
+    const std::string msg = hpnfft_last_error();
+    hpnfft_destroy(h);
+    set_error(msg);
+    return rc;
   }
   if (nranks > 1) {
     NcclUid u;
@@ -558,22 +691,128 @@ int hpnfft_plan_dist(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M_loca
     }
     p->comm = comm;
   }
-  cudaError_t e = cudaSuccess;
-  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1)
-    e = cudaMalloc(&p->halo, sizeof(double) * 2 * (size_t)(2 * m - 1) * (size_t)(p->n[1] * p->n[2]));
-  if (mode == HPNFFT_DIST_REDUCE_SCATTER && nranks > 1)
-    e = cudaMalloc(&p->partial, sizeof(double) * 2 * (size_t)(p->N[0] * p->N[1] * p->N[2]));
-  if (e != cudaSuccess) {
-    hpnfft_destroy(h);
-    set_error("device allocation of the exchange buffers failed");
-    return HPNFFT_E_NOMEM;
-  }
   if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1) {
     const char* env = getenv("HPNFFT_DIST_P2P");
-    p->p2p = !(env && env[0] == '0') && setup_p2p(p);
+    p->p2p = setup_p2p(p, !(env && env[0] == '0'));
   }
   *out = h;
   return HPNFFT_OK;
+}
+
+int hpnfft_plan_group(hpnfft_plan_t* out, int d, const int64_t* N, const int64_t* M, int m, double sigma, int window,
+                      void* stream, int nranks, int mode) {
+  if (!out || !M) {
+    set_error("hpnfft_plan_group: out or M is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  int rc = check_dist_args("hpnfft_plan_group", nranks, mode);
+  if (rc) return rc;
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  Plan* ps[16] = {};
+  auto undo = [&](int code) {
+    const std::string msg = hpnfft_last_error();
+    for (int r = 0; r < nranks; ++r) {
+      if (ps[r]) hpnfft_destroy(reinterpret_cast<hpnfft_plan_t>(ps[r]));
+      out[r] = nullptr;
+    }
+    set_error(msg);
+    return code;
+  };
+  for (int r = 0; r < nranks; ++r) {
+    hpnfft_plan_t h = nullptr;
+    rc = hpnfft_plan(&h, d, N, M[r], m, sigma, window, stream);
+    if (rc) return undo(rc);
+    ps[r] = reinterpret_cast<Plan*>(h);
+    ps[r]->virt = true;
+    rc = init_dist_fields(ps[r], nranks, r, mode);
+    if (rc) return undo(rc);
+  }
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1) {
+    double* grids[16] = {};
+    for (int s = 0; s < nranks; ++s) grids[s] = ps[s]->grid;
+    for (int r = 0; r < nranks; ++r) {
+      Plan* p = ps[r];
+      for (int s = 0; s < nranks; ++s) p->peer_grid_host[s] = grids[s];
+      if (cudaMalloc(&p->peer_grid, sizeof(double*) * nranks) != cudaSuccess ||
+          cudaMemcpy(p->peer_grid, grids, sizeof(double*) * nranks, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("device allocation of the group's peer table failed");
+        return undo(HPNFFT_E_NOMEM);
+      }
+      p->p2p = true;
+    }
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = reinterpret_cast<hpnfft_plan_t>(ps[r]);
+  return HPNFFT_OK;
+}
+
+int hpnfft_adjoint_group(hpnfft_plan_t* plans, int nranks, const double* const* f, double* const* fhat) {
+  if (!plans || !f || !fhat || nranks < 1 || nranks > 16) {
+    set_error("hpnfft_adjoint_group: NULL argument or bad nranks");
+    return HPNFFT_E_INVALID;
+  }
+  Plan* ps[16];
+  for (int r = 0; r < nranks; ++r) {
+    ps[r] = reinterpret_cast<Plan*>(plans[r]);
+    Plan* p = ps[r];
+    if (!p || !p->virt || p->nranks != nranks || p->dist_rank != r || p->dist_mode != ps[0]->dist_mode ||
+        p->stream != ps[0]->stream) {
+      set_error("hpnfft_adjoint_group: plans must be the members of one hpnfft_plan_group, in rank order, on one "
+                "stream");
+      return HPNFFT_E_INVALID;
+    }
+    if (p->failed) {
+      set_error("plan is in a failed state (an earlier CUDA error)");
+      return HPNFFT_E_STATE;
+    }
+    if (!p->points_set) {
+      set_error("hpnfft_adjoint_group called before a successful hpnfft_set_points of every member");
+      return HPNFFT_E_STATE;
+    }
+    if (!fhat[r] || (!f[r] && p->M > 0)) {
+      set_error("f or fhat is NULL");
+      return HPNFFT_E_INVALID;
+    }
+  }
+  const int mode = ps[0]->dist_mode;
+  int rc = HPNFFT_OK;
+  if (mode == HPNFFT_DIST_GRID_SLAB && nranks > 1) {
+    // the exchange phases of slab_adjoint_p2p, each for all ranks before the next (stream order)
+    for (int r = 0; r < nranks && !rc; ++r) rc = spread(ps[r], f[r]);
+    for (int r = 0; r < nranks && !rc; ++r) rc = slab_phase_halo(ps[r]);
+    for (int r = 0; r < nranks && !rc; ++r) rc = slab_phase_z(ps[r]);
+    for (int r = 0; r < nranks && !rc; ++r) rc = slab_phase_y(ps[r]);
+    for (int r = 0; r < nranks && !rc; ++r) rc = slab_phase_x(ps[r], fhat[r]);
+    return rc;
+  }
+  // option A: every rank's partial transform, then the collective's result layout
+  const int64_t nk = ps[0]->N[0] * ps[0]->N[1] * ps[0]->N[2];
+  const bool rs = mode == HPNFFT_DIST_REDUCE_SCATTER && nranks > 1;
+  for (int r = 0; r < nranks && !rc; ++r) {
+    rc = spread(ps[r], f[r]);
+    if (!rc) rc = fft_and_deconvolve(ps[r], rs ? ps[r]->partial : fhat[r]);
+  }
+  if (rc || nranks == 1) return rc;
+  Plan* p0 = ps[0];
+  stage_begin(p0, 8);
+  if (rs) {   // fhat[r] = sum_s partial_s[k0 slab r]
+    const int64_t blk = 2 * nk / nranks;
+    for (int r = 0; r < nranks && !rc; ++r) {
+      if (cudaMemcpyAsync(fhat[r], ps[0]->partial + r * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice,
+                          p0->stream) != cudaSuccess)
+        return fail(p0, HPNFFT_E_CUDA, "group copy");
+      for (int s = 1; s < nranks && !rc; ++s) rc = add_into(p0, fhat[r], ps[s]->partial + r * blk, blk);
+    }
+  } else {   // ALLREDUCE: every rank the sum; REDUCE_ROOT0: rank 0 the sum, the others their partial
+    for (int s = 1; s < nranks && !rc; ++s) rc = add_into(p0, fhat[0], fhat[s], 2 * nk);
+    if (mode == HPNFFT_DIST_ALLREDUCE)
+      for (int r = 1; r < nranks && !rc; ++r)
+        if (cudaMemcpyAsync(fhat[r], fhat[0], sizeof(double) * 2 * nk, cudaMemcpyDeviceToDevice, p0->stream) !=
+            cudaSuccess)
+          return fail(p0, HPNFFT_E_CUDA, "group copy");
+  }
+  stage_end(p0, 8);
+  return rc;
 }
 
 int hpnfft_set_slabs(hpnfft_plan_t h, const int64_t* edges) {

@@ -242,7 +242,7 @@ template <int LOGN, int TI, bool CONTIG, bool EN = false>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
 k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
            const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
-           int a_len, cplx* const* peers, int NP, int inv, EnergyArgs ea) {
+           int a_len, cplx* const* peers, int NP, int inv, EnergyArgs ea, const int* __restrict__ abort_flag) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
   extern __shared__ cplx smem[];
@@ -281,6 +281,9 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
     io.line_o = o;
     io.line_i = ic;
   }
+  // peer stores after a timed-out cross-GPU barrier: write nothing (the error is reported by the
+  // plan's next call)
+  if (peers && abort_flag && *abort_flag) io.valid = false;
   io.e_a = ea.e_a;
   io.k1_base = ea.k1_base;
   io.N1e = ea.N1;
@@ -545,7 +548,7 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
   if (LOGN == 10 && !contig && !inv && peers == nullptr && !fft1024_disabled()) {
     constexpr int CW = HPNFFT_F1024_CW;
     const size_t smem = sizeof(cplx) * (size_t)CW * (32 * 33 + 1);
-    HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_fft1024_strided<CW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_fft1024_strided<CW, false>),
                                             (int)smem),
                     "fft1024 smem attr");
     const int64_t blocks = outer * ((inner + CW - 1) / CW);
@@ -558,19 +561,19 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(cplx);
     const int64_t blocks = (outer + TC - 1) / TC;
     auto kern = k_fft_pass<LOGN, TC, true>;
-    HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
                                                                             o_start, o_total, a_lo, a_len, nullptr, 1, inv,
-                                                                            EnergyArgs{});
+                                                                            EnergyArgs{}, nullptr);
   } else {
     const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
     const int64_t blocks = outer * ((inner + TI - 1) / TI);
     auto kern = k_fft_pass<LOGN, TI, false>;
-    HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
-                                                     a_len, peers, NP, inv, EnergyArgs{});
+                                                     a_len, peers, NP, inv, EnergyArgs{}, peers ? p->dist_err : nullptr);
   }
   p->launches++;
   return check_launch(p, "fft pass");
@@ -656,7 +659,7 @@ static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_
   if (LOGN == 10 && !fft1024_disabled()) {
     constexpr int CW = HPNFFT_F1024_CW;
     const size_t smem = sizeof(cplx) * (size_t)CW * (32 * 33 + 1);
-    if (cudaFuncSetAttribute(k_fft1024_strided<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (set_max_smem(reinterpret_cast<const void*>(k_fft1024_strided<CW, true>), (int)smem) !=
         cudaSuccess) {
       fail(p, HPNFFT_E_CUDA, "fft1024 smem attr");
       return -1;
@@ -672,14 +675,14 @@ static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_
   const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
   const int64_t blocks = (inner + TI - 1) / TI;
   auto kern = k_fft_pass<LOGN, TI, false, true>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+  if (set_max_smem(reinterpret_cast<const void*>(kern), (int)smem) != cudaSuccess) {
     fail(p, HPNFFT_E_CUDA, "fft smem attr");
     return -1;
   }
   EnergyArgs ea{partial, e_a, k1_base, (int)p->N[1], (int)p->N[2]};
   kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, nullptr, 1, inner, (int)p->N[0], p->inv_c[0],
                                                    reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len,
-                                                   nullptr, 1, 0, ea);
+                                                   nullptr, 1, 0, ea, nullptr);
   p->launches++;
   return check_launch(p, "fft energy pass") ? -1 : blocks;
 }

@@ -188,7 +188,9 @@ int64_t scan_workspace_elems(int64_t nbins) { return scan_tmp_need(nbins + 1); }
 // bins of its own cell planes (one contiguous key range thanks to the chunk-major order).  Only
 // that range is zeroed and scanned per set_points; the bins outside stay 0 (zeroed at plan
 // time), so every lookup outside reads an empty range.
-static void key_range(const Plan* p, int s2, uint32_t& k_lo, uint32_t& k_hi) {
+void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi) {
+  int s2 = 0;
+  while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   k_lo = 0;
   k_hi = (uint32_t)p->nbins;
   if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
@@ -204,7 +206,7 @@ int sort_points(Plan* p, const double* x) {
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   uint32_t k_lo, k_hi;
-  key_range(p, s2, k_lo, k_hi);
+  key_range(p, k_lo, k_hi);
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count + k_lo, 0, sizeof(uint32_t) * ((size_t)(k_hi - k_lo) + 1), p->stream),
                   "memset bins");
   k_range_init<<<1, 2 * kRangeSlots + 1, 0, p->stream>>>(p->err_flag);

@@ -191,12 +191,14 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
 }
 
 // plane chunks spanned by sorted points [g0, g1): binary search of the bin table (multi-group).
-__global__ void k_group_chunks(const uint32_t* __restrict__ start, int64_t nbins, uint32_t g0, uint32_t g1,
-                               int64_t bins_per_chunk, int* chunks) {
+// Only bins [k_lo, k_hi] are non-decreasing: a grid-slab rank zeroes and scans its own key range
+// (sort.cu key_range) and every bin outside reads 0, so the search is confined to that range.
+__global__ void k_group_chunks(const uint32_t* __restrict__ start, int64_t k_lo, int64_t k_hi, uint32_t g0,
+                               uint32_t g1, int64_t bins_per_chunk, int* chunks) {
   const int which = threadIdx.x;   // 0: first point, 1: last point
   if (which > 1) return;
   const uint32_t target = which == 0 ? g0 : g1 - 1;
-  int64_t lo = 0, hi = nbins - 1;   // largest bin with start[bin] <= target
+  int64_t lo = k_lo, hi = k_hi - 1;   // largest bin in [k_lo, k_hi) with start[bin] <= target
   while (lo < hi) {
     int64_t mid = (lo + hi + 1) / 2;
     if (start[mid] <= target) lo = mid;
@@ -1264,7 +1266,7 @@ int prepare_tile_order(Plan* p, uint32_t g0, uint32_t g1) {
   int pad = 1;
   while (pad < tiles) pad <<= 1;
   const size_t osmem = sizeof(unsigned long long) * (size_t)pad;
-  HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_tile_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem),
+  HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_tile_order), (int)osmem),
                   "tile order smem attr");
   k_tile_order<<<1, 1024, osmem, p->side>>>(keys, (int)tiles, order);
   p->launches += 2;
@@ -1335,7 +1337,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   if constexpr (!INV) {
     if (merge) kern = k_spread_sweep<P1, P2, M_, false, true>;
   }
-  HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                   "sweep smem attr");
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
   prm.order = nullptr;
@@ -1344,8 +1346,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
     prm.order = p->sched_order;
     p->sched_pending = false;
   }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = device_sm_count();
   const int64_t slots = (int64_t)sms * C::kCtasPerSm;
   const int64_t blocks = tiles < slots ? tiles : slots;
   kern<<<(unsigned)blocks, C::kThreads, smem, p->stream>>>(prm);
@@ -1391,7 +1392,7 @@ int run_sweep(Plan* p, const double* f) {
     if (cnt > 0) {
       stage_begin(p, 7);
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
-      HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_point_records<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>),
                                               (int)rsmem),
                       "records smem attr");
       k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
@@ -1403,7 +1404,9 @@ int run_sweep(Plan* p, const double* f) {
     }
     if (multi) {
       const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1] * Chunk<M_>::CH;
-      k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, p->nbins, g0, g1, bins_per_chunk, p->group_rows);
+      uint32_t k_lo, k_hi;
+      key_range(p, k_lo, k_hi);
+      k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
       p->launches++;
     }
     const int var = sweep_variant();
@@ -1435,7 +1438,7 @@ int run_interp_sweep(Plan* p, double* fout) {
     }
     if (cnt > 0) {
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
-      HPNFFT_CUDA_TRY(p, cudaFuncSetAttribute(k_point_records<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>),
                                               (int)rsmem),
                       "records smem attr");
       k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
@@ -1446,7 +1449,9 @@ int run_interp_sweep(Plan* p, double* fout) {
     }
     if (multi) {
       const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1] * Chunk<M_>::CH;
-      k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, p->nbins, g0, g1, bins_per_chunk, p->group_rows);
+      uint32_t k_lo, k_hi;
+      key_range(p, k_lo, k_hi);
+      k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
       p->launches++;
     }
     const int rc = launch_sweep_group<8, 32, M_, true>(p, g0, g1, p->group_rows, multi, fout);

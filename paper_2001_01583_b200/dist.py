@@ -14,13 +14,12 @@ PAPER.md:174-200, a binomial tree of MPI Send/Recv).  Here every rank is one GPU
   cell-plane slabs for clustered inputs).  torch.distributed only carries the
   128-byte NCCL unique id from rank 0 to the others.
 
-The partition and the result layout are host logic exercised on CPU with the gloo backend in
-tests/test_dist_gloo.py, where the local transform is injected (``local_fn``) and the exchange
-is emulated with torch.distributed collectives.
+The partition helpers are host logic exercised on CPU with the gloo backend in
+tests/test_dist_gloo.py (which emulates the exchange itself, with torch.distributed collectives
+around the CPU oracle: test code, not product code); the library's exchange code runs on one GPU
+in tests/test_gpu_parity.py through hpnfft_plan_group (all ranks as plans on one device).
 """
 from __future__ import annotations
-
-from typing import Callable, Optional
 
 MODES = ("allreduce", "reduce", "reduce_scatter", "grid_slab")
 
@@ -136,18 +135,19 @@ def equal_count_edges(x, world: int):
 
 
 class DistPlan:
-    """Distributed adjoint NFFT: local Plan on this rank's points + one collective on fhat.
+    """Distributed adjoint NFFT: the library's multi-GPU plan (hpnfft_plan_dist) on this rank's
+    points; the exchange (NCCL collective or the grid-slab peer-memory steps) runs inside
+    libhpnfft.so.  torch.distributed only carries the 128-byte NCCL unique id.
 
     group   : torch.distributed process group (None = WORLD)
     mode    : "allreduce" | "reduce" | "reduce_scatter" | "grid_slab"
-    local_fn: optional callable (x_local, f_local) -> partial fhat tensor; defaults to the GPU
-              Plan (the only product path).  Tests inject the CPU oracle here to check the
-              partition/collective logic with the gloo backend.
     """
 
     def __init__(self, N, M_local: int, m: int = 6, sigma: float = 2.0, window="kb", group=None,
-                 mode: str = "allreduce", device=None, local_fn: Optional[Callable] = None, slab_edges=None):
+                 mode: str = "allreduce", device=None, slab_edges=None):
         import torch.distributed as dist
+
+        from . import Plan, get_unique_id
 
         if mode not in MODES:
             raise ValueError(f"mode must be one of {MODES}")
@@ -156,68 +156,27 @@ class DistPlan:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.local_fn = local_fn
-        self.plan = None
         if mode == "reduce_scatter" and self.N[0] % self.world:
             raise ValueError("reduce_scatter needs N0 divisible by the world size")
         if mode == "grid_slab" and self.N[1] % self.world:
             raise ValueError("grid_slab needs N1 divisible by the world size")
-        if local_fn is None:
-            from . import Plan, get_unique_id
-
-            uid = [get_unique_id() if self.rank == 0 else None]
-            src = dist.get_global_rank(group, 0) if group is not None else 0
-            dist.broadcast_object_list(uid, src=src, group=group)
-            self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device,
-                             dist=(self.world, self.rank, uid[0], mode))
-            if slab_edges is not None and self.world > 1:
-                self.plan.set_slabs(slab_edges)
+        uid = [get_unique_id() if self.rank == 0 else None]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(uid, src=src, group=group)
+        self.plan = Plan(self.N, M_local, m=m, sigma=sigma, window=window, device=device,
+                         dist=(self.world, self.rank, uid[0], mode))
+        if slab_edges is not None and self.world > 1:
+            self.plan.set_slabs(slab_edges)
 
     def set_points(self, x):
-        self._x = x
-        if self.plan is not None:
-            self.plan.set_points(x)
-
-    def partial(self, f):
-        """This rank's partial fhat_rank(k) (Eq. 8 term) from the injected local transform."""
-        return self.local_fn(self._x, f)
+        self.plan.set_points(x)
 
     def adjoint(self, f, out=None):
-        """fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate of Alg. 3).
-
-        Library plans run the whole exchange in libhpnfft.so (NCCL); with ``local_fn`` the
-        exchange is emulated with torch.distributed collectives (CPU tests)."""
-        import torch
-        import torch.distributed as dist
-
-        if self.plan is not None:
-            out = self.plan.adjoint(f, out=out)
-            return None if (self.mode == "reduce" and self.rank != 0) else out
-        fh = self.partial(f)
-        if self.world == 1:
-            return fh
-        if self.mode == "allreduce":
-            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
-            return fh
-        if self.mode == "reduce":
-            dist.reduce(fh, dst=0, op=dist.ReduceOp.SUM, group=self.group)
-            return fh if self.rank == 0 else None
-        if self.mode == "grid_slab":   # rank r receives fhat[:, k1 slab r, :]
-            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
-            cols = self.N[1] // self.world
-            return fh[:, self.rank * cols:(self.rank + 1) * cols].contiguous()
-        # reduce_scatter: rank r receives fhat[k0 slab r] (N0 / world planes)
-        rows = self.N[0] // self.world
-        if dist.get_backend(self.group) == "gloo":   # gloo has no reduce_scatter: reduce + slice
-            dist.all_reduce(fh, op=dist.ReduceOp.SUM, group=self.group)
-            return fh[self.rank * rows:(self.rank + 1) * rows].clone()
-        out = torch.empty((rows,) + self.N[1:], dtype=fh.dtype, device=fh.device)
-        if fh.is_complex():
-            dist.reduce_scatter_tensor(torch.view_as_real(out), torch.view_as_real(fh.contiguous()),
-                                       op=dist.ReduceOp.SUM, group=self.group)
-        else:
-            dist.reduce_scatter_tensor(out, fh.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
-        return out
+        """This rank's block of fhat = sum over ranks of the partial transforms (Eq. 8; Accumulate
+        of Alg. 3): the full fhat (allreduce; reduce on rank 0, None elsewhere), the k0 slab
+        (reduce_scatter) or the k1 slab (grid_slab)."""
+        out = self.plan.adjoint(f, out=out)
+        return None if (self.mode == "reduce" and self.rank != 0) else out
 
     def close(self):
         if self.plan is not None:

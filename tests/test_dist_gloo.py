@@ -25,6 +25,36 @@ def _free_port():
     return p
 
 
+class EmulatedDistPlan:
+    """Test-only emulation of the exchange of paper_2001_01583_b200.dist.DistPlan: the local
+    transform is the CPU oracle and the Accumulate step (Eq. 8, Alg. 3) is a torch.distributed
+    collective, so that the partition helpers and the result layouts of the four modes can be
+    checked on CPU with gloo.  (The library's own exchange runs on one GPU via hpnfft_plan_group
+    in tests/test_gpu_parity.py.)"""
+
+    def __init__(self, N, mode, local_fn):
+        self.N, self.mode, self.local_fn = tuple(N), mode, local_fn
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+
+    def set_points(self, x):
+        self._x = x
+
+    def adjoint(self, f):
+        fh = self.local_fn(self._x, f)
+        if self.mode == "allreduce":
+            dist.all_reduce(fh, op=dist.ReduceOp.SUM)
+            return fh
+        if self.mode == "reduce":
+            dist.reduce(fh, dst=0, op=dist.ReduceOp.SUM)
+            return fh if self.rank == 0 else None
+        dist.all_reduce(fh, op=dist.ReduceOp.SUM)   # gloo has no reduce_scatter: reduce + slice
+        if self.mode == "grid_slab":   # rank r receives fhat[:, k1 slab r, :]
+            cols = self.N[1] // self.world
+            return fh[:, self.rank * cols:(self.rank + 1) * cols].contiguous()
+        rows = self.N[0] // self.world   # reduce_scatter: fhat[k0 slab r]
+        return fh[self.rank * rows:(self.rank + 1) * rows].clone()
+
+
 def _worker(rank, world, port, mode, equal_count, outq):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -32,8 +62,7 @@ def _worker(rank, world, port, mode, equal_count, outq):
     try:
         import inputs
         import oracle
-        from paper_2001_01583_b200.dist import (DistPlan, equal_count_edges, grid_slab_edges, grid_slab_mask,
-                                                slab_mask)
+        from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_edges, grid_slab_mask, slab_mask
 
         x = torch.from_numpy(inputs.clustered_points(M, s=0.08) if equal_count else inputs.uniform_points(M))
         f = torch.from_numpy(inputs.uniform_values(M))
@@ -50,7 +79,7 @@ def _worker(rank, world, port, mode, equal_count, outq):
         def local(xx, ff):
             return torch.from_numpy(oracle.nfft_adjoint(xx.numpy(), ff.numpy(), N))
 
-        dp = DistPlan(N, int(mask.sum()), mode=mode, local_fn=local)
+        dp = EmulatedDistPlan(N, mode, local)
         dp.set_points(xl)
         out = dp.adjoint(fl)
         counts = torch.tensor([int(mask.sum())])
