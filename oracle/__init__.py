@@ -53,15 +53,16 @@ def _load():
         lib.oracle_ndft.argtypes = [ctypes.c_int, i64p, ctypes.c_int64, dp, dp, ctypes.c_int64, i64p, dp,
                                     ctypes.c_int]
         lib.oracle_ndft.restype = ctypes.c_int
-        lib.oracle_spread.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int64, dp, dp,
-                                      dp]
+        lib.oracle_spread.argtypes = [ctypes.c_int, i64p, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int64,
+                                      dp, dp, dp, ctypes.c_int]
         lib.oracle_spread.restype = ctypes.c_int
         lib.oracle_taps.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                     dp, i64p]
         lib.oracle_taps.restype = ctypes.c_int
         lib.oracle_ndft_inverse.argtypes = [ctypes.c_int, i64p, ctypes.c_int64, dp, dp, dp, ctypes.c_int]
         lib.oracle_ndft_inverse.restype = ctypes.c_int
-        lib.oracle_interp.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int64, dp, dp, dp]
+        lib.oracle_interp.argtypes = [ctypes.c_int, i64p, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int64,
+                                      dp, dp, dp, ctypes.c_int]
         lib.oracle_interp.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -145,17 +146,19 @@ def taps_1d(n: int, m: int, sigma: float, window: int, x: float):
     return w, idx
 
 
-def spread(x, f, n, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
-    """O2 step 1 (Spreading): g(l) = sum_j f_j prod_t Phi(n_t x_jt - l_t), l mod n."""
+def spread(x, f, n, m: int, sigma: float, window: int = KAISER_BESSEL, nthreads: int = 0) -> np.ndarray:
+    """O2 step 1 (Spreading): g(l) = sum_j f_j prod_t Phi(n_t x_jt - l_t), l mod n,
+    for d = len(n) in 1..3 (threads own grid planes; bit-identical for any thread count)."""
     n = tuple(int(v) for v in n)
-    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+    d = len(n)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, d)
     f = np.ascontiguousarray(np.asarray(f, dtype=np.complex128).reshape(-1))
     g = np.zeros(n + (2,), dtype=np.float64)
     M = x.shape[0]
     if M:
         fv = f.view(np.float64).copy()
         na = np.array(n, dtype=np.int64)
-        rc = _load().oracle_spread(_ip(na), m, sigma, window, M, _dp(x), _dp(fv), _dp(g))
+        rc = _load().oracle_spread(d, _ip(na), m, sigma, window, M, _dp(x), _dp(fv), _dp(g), int(nthreads))
         if rc:
             raise RuntimeError("oracle_spread failed")
     return g.view(np.complex128).reshape(n)
@@ -190,24 +193,26 @@ def fft_grid(g: np.ndarray) -> np.ndarray:
 def deconvolve_crop(ghat: np.ndarray, N, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
     """O2 step 3 (Scaling): fhat(k) = ghat(k mod n) / prod_t c_k, k in I_N."""
     N = _check_N(N)
+    d = len(N)
     n = ghat.shape
     out = ghat
-    for t in range(3):
+    for t in range(d):
         k = np.arange(-N[t] // 2, N[t] // 2)
         out = np.take(out, k % n[t], axis=t)
-    for t in range(3):
+    for t in range(d):
         c = windows.deconv_factors(N[t], n[t], m, sigma, window)
-        shape = [1, 1, 1]
+        shape = [1] * d
         shape[t] = N[t]
         out = out / c.reshape(shape)
     return out
 
 
 def nfft_adjoint(x, f, N, m: int = 6, sigma: float = 2.0, window: int = KAISER_BESSEL) -> np.ndarray:
-    """O2: the CPU NFFT of Eq. (5) in Alg. 2's order: spread -> FFT -> scale/crop."""
+    """O2: the CPU NFFT of Eq. (5) in Alg. 2's order: spread -> FFT -> scale/crop (d = len(N) in
+    1..3)."""
     N = _check_N(N)
-    if len(N) != 3:
-        raise ValueError("oracle NFFT is 3-D")
+    if not 1 <= len(N) <= 3:
+        raise ValueError("oracle NFFT: d must be 1, 2 or 3")
     n = grid_size(N, sigma)
     g = spread(x, f, n, m, sigma, window)
     return deconvolve_crop(fft_grid(g), N, m, sigma, window)
@@ -237,14 +242,15 @@ def subdivide(fhat, N, n, m: int, sigma: float, window: int = KAISER_BESSEL) -> 
     """O2i step 1 (Subdividing): ghat(k mod n) = fhat(k) / prod_t c_k for k in I_N,
     0 for the other k in I_n (the transpose of deconvolve_crop)."""
     N = _check_N(N)
+    d = len(N)
     fh = np.asarray(fhat, dtype=np.complex128).reshape(N)
-    for t in range(3):
+    for t in range(d):
         c = windows.deconv_factors(N[t], n[t], m, sigma, window)
-        shape = [1, 1, 1]
+        shape = [1] * d
         shape[t] = N[t]
         fh = fh / c.reshape(shape)
     ghat = np.zeros(tuple(n), dtype=np.complex128)
-    idx = np.ix_(*[np.arange(-N[t] // 2, N[t] // 2) % n[t] for t in range(3)])
+    idx = np.ix_(*[np.arange(-N[t] // 2, N[t] // 2) % n[t] for t in range(d)])
     ghat[idx] = fh
     return ghat
 
@@ -258,12 +264,14 @@ def ifft_grid(ghat: np.ndarray) -> np.ndarray:
 def interpolate(g: np.ndarray, x, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
     """O2i step 3 (Interpolating): f_j = sum_l g(l) prod_t Phi(n_t x_jt - l_t)."""
     n = g.shape
-    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+    d = len(n)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, d)
     M = x.shape[0]
     f = np.zeros(2 * max(M, 1), dtype=np.float64)
     if M:
         gv = np.ascontiguousarray(g, dtype=np.complex128).reshape(-1).view(np.float64)
-        rc = _load().oracle_interp(_ip(np.array(n, dtype=np.int64)), m, sigma, window, M, _dp(x), _dp(gv), _dp(f))
+        rc = _load().oracle_interp(d, _ip(np.array(n, dtype=np.int64)), m, sigma, window, M, _dp(x), _dp(gv), _dp(f),
+                                   0)
         if rc:
             raise RuntimeError("oracle_interp failed")
     return f.view(np.complex128)[:M].copy()

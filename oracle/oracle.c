@@ -12,7 +12,8 @@
  * O2a oracle_spread  : the "Spreading" step of CUNFFT (§2 Fig. 1 and
  *                      PAPER.md:162, §3): g(l) += f_j * prod_t Phi(u_t - l_t) over the
  *                      truncated neighbourhood J(x_j), l taken modulo n (periodic grid).
- *                      Plain serial loop over points, taps in natural order.
+ *                      Loop over points in order, taps in natural order; OpenMP threads own
+ *                      disjoint dimension-0 grid planes (bit-identical to the serial loop).
  * O1i oracle_ndft_inverse : direct inverse NDFT, Eq. (6) of PAPER.md:43 (§1),
  *                      f(x_j) = sum_{k in I_N} fhat(k) exp(+2 pi i k.x_j), Kahan-summed, one
  *                      output point at a time (OpenMP over points only).
@@ -141,38 +142,75 @@ static inline double window_value(double a, int m, double sigma, int window) {
   }
 }
 
-/* O2a: spread.  n: grid sizes [3]; x: [M][3]; f: [M][2]; g: [n0][n1][n2][2], accumulated
- * into (caller zeroes it).  Returns 0 on success. */
-int oracle_spread(const int64_t* n, int m, double sigma, int window, int64_t M,
-                  const double* x, const double* f, double* g) {
-  if (m < 1 || m > 16) return -1;
+/* The 2m taps of one coordinate: weights w[i] = Phi(u - l_i) and grid indices l_i mod n,
+ * l_i = floor(u) - m + 1 + i (strict truncation |u - l| < m, Q4).  A dimension t >= d
+ * of a d < 3 problem is the trivial one (n = 1): a single tap of weight exactly 1. */
+static int taps_of(int trivial, double xt, int64_t n, int m, double sigma, int window, double* w, int64_t* idx) {
+  if (trivial) {
+    w[0] = 1.0;
+    idx[0] = 0;
+    return 1;
+  }
   const int taps = 2 * m;
-  double w[3][32];
-  int64_t idx[3][32];
-  for (int64_t j = 0; j < M; ++j) {
-    for (int t = 0; t < 3; ++t) {
-      double u = (double)n[t] * x[j * 3 + t];
-      double c = floor(u);
-      double tt = u - c;
-      int64_t ci = (int64_t)c;
-      for (int i = 0; i < taps; ++i) {
-        int64_t l = ci - m + 1 + i;
-        /* |u - l| < m  <=>  not (i == 2m-1 and tt == 0) */
-        int inside = !(i == taps - 1 && tt == 0.0);
-        w[t][i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
-        int64_t lm = l % n[t];
-        if (lm < 0) lm += n[t];
-        idx[t][i] = lm;
-      }
-    }
-    const double fr = f[2 * j], fi = f[2 * j + 1];
-    for (int i0 = 0; i0 < taps; ++i0) {
-      for (int i1 = 0; i1 < taps; ++i1) {
-        for (int i2 = 0; i2 < taps; ++i2) {
-          double wt = w[0][i0] * w[1][i1] * w[2][i2];
-          int64_t off = ((idx[0][i0] * n[1] + idx[1][i1]) * n[2] + idx[2][i2]) * 2;
-          g[off] += fr * wt;
-          g[off + 1] += fi * wt;
+  double u = (double)n * xt;
+  double c = floor(u);
+  double tt = u - c;
+  int64_t ci = (int64_t)c;
+  for (int i = 0; i < taps; ++i) {
+    int64_t l = ci - m + 1 + i;
+    /* |u - l| < m  <=>  not (i == 2m-1 and tt == 0) */
+    int inside = !(i == taps - 1 && tt == 0.0);
+    w[i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
+    int64_t lm = l % n;
+    if (lm < 0) lm += n;
+    idx[i] = lm;
+  }
+  return taps;
+}
+
+/* O2a: spread.  d in 1..3; n: grid sizes [d]; x: [M][d]; f: [M][2]; g: [n0][n1][n2][2] (the
+ * d given dimensions, row-major), accumulated into (caller zeroes it).  Returns 0 on success.
+ * Parallel by grid-plane ownership: thread r owns the dimension-0 planes
+ * [r n0 / T, (r+1) n0 / T) and visits every point in input order, applying only the taps whose
+ * plane it owns.  Every grid node therefore receives its contributions in exactly the order of
+ * the serial loop (points in order, taps in natural order): no atomics, no private grids, the
+ * result is bit-identical to the serial loop for any thread count. */
+int oracle_spread(int d, const int64_t* n, int m, double sigma, int window, int64_t M,
+                  const double* x, const double* f, double* g, int nthreads) {
+  if (m < 1 || m > 16 || d < 1 || d > 3) return -1;
+  int64_t nn[3] = {1, 1, 1};
+  for (int t = 0; t < d; ++t) nn[t] = n[t];
+  int T = 1;
+#ifdef _OPENMP
+  T = nthreads > 0 ? nthreads : omp_get_max_threads();
+  if (T > nn[0]) T = (int)nn[0];
+#pragma omp parallel num_threads(T)
+#endif
+  {
+    int r = 0;
+#ifdef _OPENMP
+    r = omp_get_thread_num();
+#endif
+    const int64_t p_lo = nn[0] * r / T, p_hi = nn[0] * (r + 1) / T;
+    double w[3][32];
+    int64_t idx[3][32];
+    int nt[3];
+    for (int64_t j = 0; j < M; ++j) {
+      nt[0] = taps_of(0, x[j * d], nn[0], m, sigma, window, w[0], idx[0]);
+      int mine = 0;
+      for (int i0 = 0; i0 < nt[0]; ++i0) mine |= idx[0][i0] >= p_lo && idx[0][i0] < p_hi;
+      if (!mine) continue;
+      for (int t = 1; t < 3; ++t) nt[t] = taps_of(t >= d, t < d ? x[j * d + t] : 0.0, nn[t], m, sigma, window, w[t], idx[t]);
+      const double fr = f[2 * j], fi = f[2 * j + 1];
+      for (int i0 = 0; i0 < nt[0]; ++i0) {
+        if (idx[0][i0] < p_lo || idx[0][i0] >= p_hi) continue;
+        for (int i1 = 0; i1 < nt[1]; ++i1) {
+          for (int i2 = 0; i2 < nt[2]; ++i2) {
+            double wt = w[0][i0] * w[1][i1] * w[2][i2];
+            int64_t off = ((idx[0][i0] * nn[1] + idx[1][i1]) * nn[2] + idx[2][i2]) * 2;
+            g[off] += fr * wt;
+            g[off + 1] += fi * wt;
+          }
         }
       }
     }
@@ -182,17 +220,7 @@ int oracle_spread(const int64_t* n, int m, double sigma, int window, int64_t M,
 
 /* 1-D weights of one coordinate (exposed for the window/tap pins in tests). */
 int oracle_taps(int64_t n, int m, double sigma, int window, double x, double* w, int64_t* idx) {
-  double u = (double)n * x;
-  double c = floor(u);
-  double tt = u - c;
-  int64_t ci = (int64_t)c;
-  for (int i = 0; i < 2 * m; ++i) {
-    int inside = !(i == 2 * m - 1 && tt == 0.0);
-    w[i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
-    int64_t lm = (ci - m + 1 + i) % n;
-    if (lm < 0) lm += n;
-    idx[i] = lm;
-  }
+  taps_of(0, x, n, m, sigma, window, w, idx);
   return 0;
 }
 
@@ -239,35 +267,29 @@ int oracle_ndft_inverse(int d, const int64_t* N, int64_t M, const double* x, con
   return 0;
 }
 
-/* O2i: interpolate.  n: grid sizes [3]; g: [n0][n1][n2][2]; x: [M][3]; out f: [M][2].
- * Same taps and weights as oracle_spread (the interpolation is the spread's transpose). */
-int oracle_interp(const int64_t* n, int m, double sigma, int window, int64_t M, const double* x,
-                  const double* g, double* f) {
-  if (m < 1 || m > 16) return -1;
-  const int taps = 2 * m;
-  double w[3][32];
-  int64_t idx[3][32];
+/* O2i: interpolate.  d in 1..3; n: grid sizes [d]; g: [n0][n1][n2][2]; x: [M][d]; out f: [M][2].
+ * Same taps and weights as oracle_spread (the interpolation is the spread's transpose); every
+ * output is an independent serial sum (OpenMP over points only). */
+int oracle_interp(int d, const int64_t* n, int m, double sigma, int window, int64_t M, const double* x,
+                  const double* g, double* f, int nthreads) {
+  if (m < 1 || m > 16 || d < 1 || d > 3) return -1;
+  int64_t nn[3] = {1, 1, 1};
+  for (int t = 0; t < d; ++t) nn[t] = n[t];
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
   for (int64_t j = 0; j < M; ++j) {
-    for (int t = 0; t < 3; ++t) {
-      double u = (double)n[t] * x[j * 3 + t];
-      double c = floor(u);
-      double tt = u - c;
-      int64_t ci = (int64_t)c;
-      for (int i = 0; i < taps; ++i) {
-        int64_t l = ci - m + 1 + i;
-        int inside = !(i == taps - 1 && tt == 0.0);
-        w[t][i] = inside ? window_value(tt + (double)(m - 1 - i), m, sigma, window) : 0.0;
-        int64_t lm = l % n[t];
-        if (lm < 0) lm += n[t];
-        idx[t][i] = lm;
-      }
-    }
+    double w[3][32];
+    int64_t idx[3][32];
+    int nt[3];
+    for (int t = 0; t < 3; ++t) nt[t] = taps_of(t >= d, t < d ? x[j * d + t] : 0.0, nn[t], m, sigma, window, w[t], idx[t]);
     double sr = 0.0, si = 0.0;
-    for (int i0 = 0; i0 < taps; ++i0) {
-      for (int i1 = 0; i1 < taps; ++i1) {
-        for (int i2 = 0; i2 < taps; ++i2) {
+    for (int i0 = 0; i0 < nt[0]; ++i0) {
+      for (int i1 = 0; i1 < nt[1]; ++i1) {
+        for (int i2 = 0; i2 < nt[2]; ++i2) {
           double wt = w[0][i0] * w[1][i1] * w[2][i2];
-          int64_t off = ((idx[0][i0] * n[1] + idx[1][i1]) * n[2] + idx[2][i2]) * 2;
+          int64_t off = ((idx[0][i0] * nn[1] + idx[1][i1]) * nn[2] + idx[2][i2]) * 2;
           sr += g[off] * wt;
           si += g[off + 1] * wt;
         }

@@ -449,3 +449,75 @@ def test_O2i_accuracy_vs_O1i_paper_section4():
     errs = [oracle.rel_l2_error(oracle.nfft_inverse(x, fh, N, m=m), s) for m in (2, 4, 6)]
     assert errs[0] > errs[1] > errs[2]
     assert errs[2] < setup["north_star_e2_bar_m6"]
+
+
+# ------------------------------------------------ O2 parallel spread, d = 1 and 2 (NEXT #4) --
+def test_O2_spread_thread_count_invariant():
+    """The plane-ownership OpenMP spread gives every node its
+    contributions in the serial order: bit-identical results for 1, 3 and 8 threads, also on a
+    grid smaller than the stencil (n = 4 < 2m: the taps wrap onto the same planes)."""
+    for n, m, M in [((32, 16, 8), 6, 3000), ((4, 8, 16), 3, 500)]:
+        x = inputs.clustered_points(M, s=0.05, seed=32)
+        f = inputs.uniform_values(M, seed=32)
+        ref = oracle.spread(x, f, n, m, 2.0, nthreads=1)
+        for T in (3, 8):
+            assert np.array_equal(oracle.spread(x, f, n, m, 2.0, nthreads=T), ref)
+
+
+def _gather_low_dim(x, f, n, m, sigma, window):
+    """Spreading per lattice node as a gather over all points and periodic images,
+    for any d, written independently of oracle.c."""
+    d = len(n)
+    g = np.zeros(n, dtype=complex)
+    for j in range(x.shape[0]):
+        tot = []
+        for t in range(d):
+            u = n[t] * x[j, t]
+            l = np.arange(n[t])
+            tot.append(sum(windows.phi(u - (l + r * n[t]), m, sigma, window) for r in range(-3, 4)))
+        w = tot[0]
+        for t in range(1, d):
+            w = np.multiply.outer(w, tot[t])
+        g += f[j] * w
+    return g
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_O2_low_dim_spread_equals_lattice_gather(d):
+    """d = 1, 2 (I_N and Eq. 5 are defined for any d): the oracle's spread,
+    whose missing dimensions are a single tap of weight exactly 1, equals the per-node gather."""
+    n = (32,) if d == 1 else (16, 8)
+    x = inputs.uniform_points(25, seed=33, d=d)
+    x[0, 0] = 0.5
+    f = inputs.uniform_values(25, seed=33)
+    for win in (windows.KAISER_BESSEL, windows.GAUSSIAN):
+        a = oracle.spread(x, f, n, 3, 2.0, win)
+        assert a.shape == n
+        assert oracle.rel_l2_error(a, _gather_low_dim(x, f, n, 3, 2.0, win)) < 1e-13
+
+
+@pytest.mark.parametrize("d,N,M", [(1, (256,), 700), (2, (32, 64), 3000)])
+def test_O2_low_dim_accuracy_and_adjoint_identity(d, N, M):
+    """d = 1, 2: O2 against the direct NDFT within the KB error bound (and <= 1e-9 at m = 6,
+    north_star), exact grid-shift covariance, and the adjoint identity <A f, g> = <f, A^H g>
+    between the O2 and O2i chains."""
+    x = inputs.uniform_points(M, seed=34, d=d)
+    f = inputs.uniform_values(M, seed=34)
+    s = oracle.ndft_direct(x, f, N)
+    sigma = 2.0
+    for m in (2, 4, 6):
+        e = oracle.rel_l2_error(oracle.nfft_adjoint(x, f, N, m=m), s)
+        bound = 4 * np.pi * (np.sqrt(m) + m) * (1 - 1 / sigma) ** 0.25 * np.exp(-2 * np.pi * m * np.sqrt(1 - 1 / sigma))
+        assert bound / 1e3 < e < bound
+    assert oracle.rel_l2_error(oracle.nfft_adjoint(x, f, N), s) < 1e-9
+    n = oracle.grid_size(N, sigma)
+    shift = np.array([3.0 / n[t] for t in range(d)])
+    a = oracle.nfft_adjoint(inputs.wrap(x + shift), f, N)
+    k = np.meshgrid(*[np.arange(-v // 2, v // 2) for v in N], indexing="ij")
+    ph = np.exp(-2j * np.pi * sum(k[t] * shift[t] for t in range(d)))
+    assert oracle.rel_l2_error(a, oracle.nfft_adjoint(x, f, N) * ph) < 1e-14
+    rng = np.random.default_rng(d)
+    gh = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    lhs = np.vdot(gh, oracle.nfft_adjoint(x, f, N))
+    rhs = np.vdot(oracle.nfft_inverse(x, gh, N), f)
+    assert abs(lhs - rhs) < 1e-12 * abs(lhs)
