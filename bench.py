@@ -6,15 +6,18 @@
 
 Workload (BASELINE.json configs[3], the metric's config): d = 3, N = 256^3, M = 10^7 points,
 float64, Kaiser-Bessel m = 6, sigma = 2 (grid 512^3).  One step = one pass of the whole hot
-path: set_points (keys, bin sort) + adjoint (spread, 3 FFT passes with the
-fused deconvolve/crop); for N > 1 GPUs every rank owns the points of one equal-size x-slab
-("subcells with same size") and the partial fhat are summed with an NCCL
-all-reduce (Eq. 8 / Alg. 3).  Total work is fixed as N grows
-(strong scaling).  Inputs are resident in HBM before the timed region and are larger than
-L2 (x 240 MB, f 160 MB, grid 2.1 GB), so no explicit L2 flush is needed.
+path: set_points (keys, bin sort) + adjoint (records, sweep spread, 3 pruned
+FFT passes with the fused deconvolve/crop).  For N > 1 GPUs every rank generates and owns the
+points of one x-slab subcell ("subcells with same size") and the library's exchange
+combines the partial results (Eq. 8 / Alg. 3): by default option G
+(--exchange grid_slab: halo + distributed FFT over NVLink peer memory), or option A (NCCL
+collective on fhat).  Total work is fixed as N grows (strong scaling).  Inputs are resident in
+HBM before the timed region and are larger than L2 (x 240 MB, f 160 MB, grid 2.1 GB), so no
+explicit L2 flush is needed.
 
---impl reference times the CPU oracle (oracle/, the independent CPU NFFT) on the host cores
-on a bounded sample of the same workload.
+cpu_baseline: the oracle's whole transform of the workload once on all host cores.
+--impl reference: the oracle (oracle/, the independent CPU NFFT) timed on the host cores, each
+step a complete transform of a bounded sample of the workload's points.
 """
 from __future__ import annotations
 
@@ -38,11 +41,13 @@ CONFIGS = {
 }
 METRIC = "adjoint NFFT nonuniform points/s at N=256³ float64, 1/2/4/8 B200; E2 error"
 EXCHANGE_TEXT = {
-    "allreduce": "option A: ncclAllReduce of fhat inside libhpnfft.so",
-    "reduce": "option A: ncclReduce of fhat to rank 0 inside libhpnfft.so",
-    "reduce_scatter": "option A: ncclReduceScatter of fhat (k0 slabs) inside libhpnfft.so",
-    "grid_slab": "option G: grid halo ncclSend/Recv + distributed pruned FFT (all-to-all) inside libhpnfft.so, "
-                 "fhat left in k1 slabs",
+    "nccl_collective": "option A: one NCCL collective on fhat inside libhpnfft.so ({mode})",
+    "grid_slab_nvlink_p2p": "option G: grid halo pulled from the neighbours' grids + distributed pruned FFT whose "
+                            "y-pass epilogue stores into the destination ranks' grids (the all-to-all), over NVLink "
+                            "peer memory (CUDA IPC) inside libhpnfft.so; fhat left in k1 slabs",
+    "grid_slab_nccl_sendrecv": "option G over NCCL send/recv (peer memory unavailable): halo runs + pack + grouped "
+                               "all-to-all inside libhpnfft.so; fhat left in k1 slabs",
+    "none": "none",
 }
 M_WINDOW, SIGMA = 6, 2.0
 # FP64 tensor-core (DMMA m8n8k4) peak MEASURED on this pool's B200 with tools/ubench_dmma.cu /
@@ -153,21 +158,54 @@ def make_inputs(cfg, dist_kind, device):
     return x, f
 
 
-def slab_select(x, f, rank, ws, partition="equal_size", exchange="allreduce", n0=512):
-    """This rank's x-slab subcell: equal-size slabs, equal-count slabs, or the
-    cell-aligned equal-size slabs of the grid_slab exchange (option G)."""
-    from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_edges, grid_slab_mask, slab_mask
+def shard_inputs(cfg, dist_kind, device, rank, ws, partition="equal_size", exchange="grid_slab", n0=512):
+    """This rank's x-slab subcell of the seeded workload, generated in place: the
+    counter-based generator is streamed over the M points in chunks and only the rank's points
+    are kept (no full copy of the M points on any rank).  Equal-size slabs, equal-count slabs, or
+    the cell-aligned slabs of the grid_slab exchange (option G; equal-cost edges from the summed
+    plane histogram, every rank computes the same)."""
+    import torch
 
-    if ws == 1:
-        return x, f, None
+    import inputs.device as idev
+    from paper_2001_01583_b200.dist import equal_count_edges, grid_slab_edges_hist, grid_slab_mask, slab_mask
+
+    M = cfg["M"]
+    chunk = 1 << 25
+
+    def gen(start, cnt):
+        if dist_kind == "clustered":
+            xx = idev.clustered_points(cnt, s=0.05, start=start, device=device)
+        else:
+            xx = idev.uniform_points(cnt, start=start, device=device)
+        return xx, idev.uniform_values(cnt, start=start, device=device)
+
     edges = None
-    if exchange == "grid_slab":
-        # every rank holds the same full point set here: no histogram reduction needed
-        edges = grid_slab_edges(x, ws, n0, m=M_WINDOW, reduce=False) if partition == "equal_count" else None
-        mask = grid_slab_mask(x, rank, ws, n0, edges)
-    else:
-        mask = slab_mask(x, rank, ws, equal_count_edges(x, ws) if partition == "equal_count" else None)
-    return x[mask].contiguous(), f[mask].contiguous(), edges
+    if partition == "equal_count":   # a first pass over the chunks: the histogram / quantiles of all M points
+        if exchange == "grid_slab":
+            hist = torch.zeros(n0, dtype=torch.int64, device=device)
+            for s0 in range(0, M, chunk):
+                xx, _ = gen(s0, min(chunk, M - s0))
+                c0 = torch.floor(xx[:, 0] * float(n0)).to(torch.int64) % n0   # memory plane
+                hist += torch.bincount(c0, minlength=n0)
+            edges = grid_slab_edges_hist(hist, ws, n0, m=M_WINDOW)
+        else:
+            xs = [gen(s0, min(chunk, M - s0))[0][:, 0].clone() for s0 in range(0, M, chunk)]
+            edges = equal_count_edges(torch.cat(xs).unsqueeze(1), ws)
+    xs, fs = [], []
+    for s0 in range(0, M, chunk):
+        xx, ff = gen(s0, min(chunk, M - s0))
+        if exchange == "grid_slab":
+            mask = grid_slab_mask(xx, rank, ws, n0, edges)
+        else:
+            mask = slab_mask(xx, rank, ws, edges)
+        xs.append(xx[mask].contiguous())
+        fs.append(ff[mask].contiguous())
+        del xx, ff, mask
+    x = torch.cat(xs) if len(xs) > 1 else xs[0]
+    f = torch.cat(fs) if len(fs) > 1 else fs[0]
+    del xs, fs
+    torch.cuda.empty_cache()
+    return x, f, (edges if exchange == "grid_slab" else None)
 
 
 def run_ours(args):
@@ -185,9 +223,12 @@ def run_ours(args):
     cfg = CONFIGS[args.config]
     N = cfg["N"]
     M_total = cfg["M"]
-    x_all, f_all = make_inputs(cfg, args.dist, dev)
-    x, f, slab_edges = slab_select(x_all, f_all, rank, ws, args.partition, args.exchange, int(SIGMA * N[0]))
-    del x_all, f_all
+    if ws == 1:
+        x, f = make_inputs(cfg, args.dist, dev)
+        slab_edges = None
+    else:
+        x, f, slab_edges = shard_inputs(cfg, args.dist, dev, rank, ws, args.partition, args.exchange,
+                                        int(SIGMA * N[0]))
     M_local = x.shape[0]
     torch.cuda.synchronize()
 
@@ -297,40 +338,48 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (largest stage) ----
     # the spread stage = point-record kernel + sweep kernel; the sweep is timed as the difference
+    info = plan.info()
     kern = {k: v for k, v in stages.items() if k in ("fft_z", "fft_y", "fft_x_deconv")}
     if "spread" in stages:
         kern["sweep"] = stages["spread"] - stages.get("records", 0.0)
         kern["records"] = stages.get("records", 0.0)
     dom = max(kern, key=kern.get) if kern else "sweep"
     peaks = measured_peaks()
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(f"config{args.config}_{dom}")
-    except Exception:
-        pass
+    traffic, traffic_src = None, None
+    if ws == 1:   # the committed ncu capture is of the 1-GPU line of this config only
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tr.get(f"config{args.config}_{args.dist}_{dom}", tr.get(f"config{args.config}_{dom}"))
+            traffic_src = tr.get("_source")
+        except Exception:
+            pass
     if dom in ("sweep", "records"):
         fl = M_local * spread_flops_per_point(M_WINDOW)
         achieved = fl / (kern["sweep"] * 1e-3) / 1e12
         roof = {"kernel": "k_spread_sweep", "bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": "measured FP64 DMMA m8n8k4 (tools/ubench_dmma.cu, profiles/ubench_dmma.txt)",
-                "algorithmic": f"{spread_flops_per_point(M_WINDOW):.0f} flop/point x {M_local} points",
+                "algorithmic": f"{spread_flops_per_point(M_WINDOW):.0f} flop/point x {M_local} points (this rank)",
                 "timed_as": "spread stage - records stage (CUDA events on the plan stream)"}
     else:
-        byts = fft_bytes(N)[dom]
+        byts = info["pass_bytes"][dom]
         hbm = peaks.get("hbm_gbs", 6650.0)
         achieved = byts / (stages[dom] * 1e-3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
     fft_ms = sum(stages.get(k, 0.0) for k in ("fft_z", "fft_y", "fft_x_deconv"))
-    fbytes = sum(fft_bytes(N).values())
+    fbytes = sum(info["pass_bytes"].values())   # this rank's passes (its planes / k1 rows)
     extra = {
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "fft_hbm": {"achieved_gbs": fbytes / (fft_ms * 1e-3) / 1e9 if fft_ms else None,
-                    "frac": (fbytes / (fft_ms * 1e-3) / 1e9) / peaks.get("hbm_gbs", 6650.0) if fft_ms else None},
+                    "frac": (fbytes / (fft_ms * 1e-3) / 1e9) / peaks.get("hbm_gbs", 6650.0) if fft_ms else None,
+                    "bytes": fbytes, "per_pass_bytes": info["pass_bytes"],
+                    "how": "hpnfft_plan_info algorithmic bytes of this rank's three passes / their CUDA-event time"},
         "M_local": M_local,
+        "record_group": info["record_group"],
+        "workspace_bytes": info["workspace_bytes"],
     }
 
     cpu = None
@@ -357,7 +406,7 @@ def run_ours(args):
                        "points": args.dist, "partition": ((f"cell-aligned equal-cost x-slabs x{ws} (dist.grid_slab_edges)" if args.partition == "equal_count"
                                       else f"cell-aligned equal-size x-slabs x{ws}") if args.exchange == "grid_slab"
                                      else f"{args.partition} x-slabs x{ws}"),
-                       "exchange": (EXCHANGE_TEXT[args.exchange] if ws > 1 else "none"),
+                       "exchange": EXCHANGE_TEXT[info["exchange_path"]].format(mode=args.exchange),
                        "fhat_layout": ("full on every rank" if ws == 1 or args.exchange == "allreduce"
                                        else f"distributed: block {list(plan.out_shape)} per rank"),
                        "spread_method": args.method,
@@ -417,61 +466,79 @@ def _finish_inverse(args, plan, stages, ms_per_step, value, ws, rank, launches_p
 
 
 # ----------------------------------------------------------------------------- CPU oracle --
-def _oracle_timing(cfg, dist_kind, sample_points, fft_once=True):
-    """Time the CPU oracle (oracle.nfft_adjoint's steps, unmodified) on a bounded sample:
-    the serial C spread on `sample_points` of the M points and the FFT + deconvolve of the
-    full oversampled grid.  Returns (t_spread_per_point, t_fft)."""
-    import numpy as np
+def _host_cpu():
+    """Host facts for the CPU-baseline record: usable cores and the CPU model."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
 
+
+def _oracle_run(cfg, dist_kind, M_s):
+    """The CPU oracle (oracle.nfft_adjoint's three steps, unmodified: O2 spread on all host cores
+    by plane ownership, scipy FFT on all cores, deconvolve + crop) on the first M_s points of the
+    workload's seeded point set.  Returns (seconds total, seconds spread, seconds FFT+deconvolve);
+    input generation is outside the timed region."""
     import inputs
     import oracle
 
     N = cfg["N"]
     n = oracle.grid_size(N, SIGMA)
-    if dist_kind == "clustered":
-        x = inputs.clustered_points(sample_points, s=0.05)
-    else:
-        x = inputs.uniform_points(sample_points)
-    f = inputs.uniform_values(sample_points)
+    x = inputs.clustered_points(M_s, s=0.05) if dist_kind == "clustered" else inputs.uniform_points(M_s)
+    f = inputs.uniform_values(M_s)
     t0 = time.perf_counter()
     g = oracle.spread(x, f, n, M_WINDOW, SIGMA)
     t1 = time.perf_counter()
-    tf = None
-    if fft_once:
-        t2 = time.perf_counter()
-        oracle.deconvolve_crop(oracle.fft_grid(g), N, M_WINDOW, SIGMA)
-        tf = time.perf_counter() - t2
-    return (t1 - t0) / sample_points, tf
+    oracle.deconvolve_crop(oracle.fft_grid(g), N, M_WINDOW, SIGMA)
+    t2 = time.perf_counter()
+    return t2 - t0, t1 - t0, t2 - t1
 
 
 def cpu_baseline(cfg, dist_kind):
-    sample = 100000
-    t_pp, t_fft = _oracle_timing(cfg, dist_kind, sample)
-    t_est = t_pp * cfg["M"] + t_fft
-    return {"value": cfg["M"] / t_est, "unit": "points/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle/ CPU NFFT: serial C spread timed on {sample} of the {cfg['M']} points "
-                      f"({t_pp * 1e6:.2f} us/point, scaled to M) + numpy FFT/deconvolve of the full "
-                      f"grid timed once ({t_fft:.2f} s)",
-            "host_cpus": os.cpu_count()}
+    """The whole oracle transform of the workload (all M points, full grid) once on the host's
+    cores (config 4: ~10-20 s of CPU work); no extrapolation."""
+    cores, model = _host_cpu()
+    t, ts, tf = _oracle_run(cfg, dist_kind, cfg["M"])
+    return {"value": cfg["M"] / t, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "sample": f"the full workload once: oracle/ CPU NFFT of all {cfg['M']} points (O2 spread "
+                      f"{ts:.2f} s by grid-plane ownership on {cores} threads, scipy FFT + deconvolve/crop of "
+                      f"the full grid {tf:.2f} s on {cores} workers) = {t:.2f} s",
+            "cpu_model": model, "threads": cores}
+
+
+REF_SAMPLE = 10 ** 6   # points per reference step (bounded sample of config 4's 1e7)
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands, timed on the host cores.  One step = the oracle
+    transform of a bounded sample of the workload: the first min(M, 1e6) points of the seeded
+    point set, spread onto the FULL oversampled grid, full-grid FFT, deconvolve + crop (every
+    step is a complete transform of those points; value = points transformed / step time)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    sample = 20000
-    # the FFT + deconvolve of the full grid is timed once (warm-up); each step spreads a sample
-    _, t_fft = _oracle_timing(cfg, args.dist, 2000, fft_once=True)
+    M_s = min(cfg["M"], REF_SAMPLE)
+    cores, model = _host_cpu()
     for _ in range(args.warmup):
-        _oracle_timing(cfg, args.dist, sample, fft_once=False)
-    per = []
+        _oracle_run(cfg, args.dist, M_s)
+    per, sp, ff = [], [], []
     for _ in range(args.steps):
-        t_pp, _ = _oracle_timing(cfg, args.dist, sample, fft_once=False)
-        per.append(t_pp)
-    t_pp = statistics.median(per)
-    t_est = t_pp * cfg["M"] + t_fft
-    value = cfg["M"] / t_est
+        t, ts, tf = _oracle_run(cfg, args.dist, M_s)
+        per.append(t)
+        sp.append(ts)
+        ff.append(tf)
+    t_step = sum(per) / len(per)
+    value = M_s / t_step
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -480,17 +547,22 @@ def run_reference(args):
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": t_est * 1e3,
+        "ms_per_step": t_step * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": f"synthetic seeded {args.dist} points (inputs/)",
         "config": {"workload": f"BASELINE config {args.config}: d=3, N={cfg['N'][0]}^3, M={cfg['M']}, "
-                               f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "kind": "oracle", "cores": 1,
-                         "sample": f"each step: serial C spread of {sample} points (median us/point scaled to "
-                                   f"M={cfg['M']}); FFT+deconvolve of the full grid timed once ({t_fft:.2f} s)"},
+                               f"KB m={M_WINDOW}, sigma={SIGMA}, {args.dist}; each step transforms a bounded "
+                               f"sample of {M_s} of its points on the full grid"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "kind": "oracle", "cores": cores, "threads": cores,
+                         "cpu_model": model,
+                         "sample": f"each step: oracle/ CPU NFFT of the first {M_s} points (O2 spread by plane "
+                                   f"ownership, median {statistics.median(sp):.2f} s; scipy FFT + deconvolve/crop "
+                                   f"of the full {int(SIGMA * cfg['N'][0])}^3 grid, median "
+                                   f"{statistics.median(ff):.2f} s) on {cores} host threads; mean of {args.steps} "
+                                   f"timed steps (median {statistics.median(per):.2f} s)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -168,6 +168,22 @@ int64_t hpnfft_launch_count(hpnfft_plan_t p);
 int hpnfft_enable_timing(hpnfft_plan_t p, int on);
 int hpnfft_stage_times(hpnfft_plan_t p, float* out, int n);
 
+/*
+ * Plan facts for measurement (HOST int64 out[n]; returns the number written, <= 8):
+ *   out[0..2] algorithmic HBM bytes of the FFT passes z, y, x (+ deconvolve) of this plan's next
+ *             hpnfft_adjoint for the current points: each pass reads its input once and writes its
+ *             pruned output once (complex128; only the node planes the points reach, the rank's
+ *             slab and k1 rows for a grid-slab plan);
+ *   out[3]    exchange path: 0 none (one rank), 1 NCCL collective on fhat (option A), 2 grid slab
+ *             over NVLink peer memory (CUDA IPC), 3 grid slab over NCCL send/recv, 4 one-GPU rank
+ *             group (hpnfft_plan_group);
+ *   out[4]    node planes of dimension 0 the passes z and y process;
+ *   out[5]    points per record group of the sweep spread ("groups"; M = one group);
+ *   out[6]    the spread kernel HPNFFT_SPREAD_AUTO resolves to (HPNFFT_SPREAD_ATOMIC or _SWEEP);
+ *   out[7]    workspace bytes.
+ */
+int hpnfft_plan_info(hpnfft_plan_t p, int64_t* out, int n);
+
 /* Library version string. */
 const char* hpnfft_version(void);
 

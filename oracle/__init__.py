@@ -185,9 +185,19 @@ def spread_naive_gather(x, f, n, m: int, sigma: float, window: int = KAISER_BESS
     return g
 
 
+def _workers() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def fft_grid(g: np.ndarray) -> np.ndarray:
-    """O2 step 2 (FFT): ghat(k) = sum_l g(l) exp(-2 pi i k.l/n), unnormalised."""
-    return np.fft.fftn(g)
+    """O2 step 2 (FFT): ghat(k) = sum_l g(l) exp(-2 pi i k.l/n), unnormalised
+    (scipy.fft on all host cores)."""
+    import scipy.fft
+
+    return scipy.fft.fftn(g, workers=_workers())
 
 
 def deconvolve_crop(ghat: np.ndarray, N, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:
@@ -258,7 +268,9 @@ def subdivide(fhat, N, n, m: int, sigma: float, window: int = KAISER_BESSEL) -> 
 def ifft_grid(ghat: np.ndarray) -> np.ndarray:
     """O2i step 2 (Inverse FFT): g(l) = sum_k ghat(k) exp(+2 pi i k.l/n),
     unnormalised (numpy's ifftn divides by prod n_t)."""
-    return np.fft.ifftn(ghat) * float(np.prod(ghat.shape))
+    import scipy.fft
+
+    return scipy.fft.ifftn(ghat, workers=_workers()) * float(np.prod(ghat.shape))
 
 
 def interpolate(g: np.ndarray, x, m: int, sigma: float, window: int = KAISER_BESSEL) -> np.ndarray:

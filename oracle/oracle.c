@@ -196,10 +196,16 @@ int oracle_spread(int d, const int64_t* n, int m, double sigma, int window, int6
     int64_t idx[3][32];
     int nt[3];
     for (int64_t j = 0; j < M; ++j) {
-      nt[0] = taps_of(0, x[j * d], nn[0], m, sigma, window, w[0], idx[0]);
+      /* ownership test on the plane indices alone (no window evaluation for foreign points) */
+      const int64_t c0 = (int64_t)floor((double)nn[0] * x[j * d]);
       int mine = 0;
-      for (int i0 = 0; i0 < nt[0]; ++i0) mine |= idx[0][i0] >= p_lo && idx[0][i0] < p_hi;
+      for (int i0 = 0; i0 < 2 * m; ++i0) {
+        int64_t l = (c0 - m + 1 + i0) % nn[0];
+        if (l < 0) l += nn[0];
+        mine |= l >= p_lo && l < p_hi;
+      }
       if (!mine) continue;
+      nt[0] = taps_of(0, x[j * d], nn[0], m, sigma, window, w[0], idx[0]);
       for (int t = 1; t < 3; ++t) nt[t] = taps_of(t >= d, t < d ? x[j * d + t] : 0.0, nn[t], m, sigma, window, w[t], idx[t]);
       const double fr = f[2 * j], fi = f[2 * j + 1];
       for (int i0 = 0; i0 < nt[0]; ++i0) {

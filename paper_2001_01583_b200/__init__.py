@@ -102,6 +102,8 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_plan_group.restype = ctypes.c_int
     lib.hpnfft_adjoint_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp)]
     lib.hpnfft_adjoint_group.restype = ctypes.c_int
+    lib.hpnfft_plan_info.argtypes = [vp, i64p, ctypes.c_int]
+    lib.hpnfft_plan_info.restype = ctypes.c_int
     lib.hpnfft_output_shape.argtypes = [vp, i64p]
     lib.hpnfft_output_shape.restype = ctypes.c_int
     _lib = lib
@@ -272,6 +274,19 @@ class Plan:
     @property
     def workspace_bytes(self) -> int:
         return int(load_library().hpnfft_workspace_bytes(self._h))
+
+    EXCHANGE_PATHS = ("none", "nccl_collective", "grid_slab_nvlink_p2p", "grid_slab_nccl_sendrecv", "one_gpu_group")
+
+    def info(self) -> dict:
+        """hpnfft_plan_info: algorithmic FFT-pass bytes of the current geometry, exchange path, ..."""
+        buf = (ctypes.c_int64 * 8)()
+        w = load_library().hpnfft_plan_info(self._h, buf, 8)
+        if w < 0:
+            _check(w)
+        v = [int(buf[i]) for i in range(w)]
+        return {"pass_bytes": {"fft_z": v[0], "fft_y": v[1], "fft_x_deconv": v[2]},
+                "exchange_path": self.EXCHANGE_PATHS[v[3]], "planes": v[4], "record_group": v[5],
+                "spread_kernel": {1: "atomic", 2: "sweep"}[v[6]], "workspace_bytes": v[7]}
 
     def launch_count(self) -> int:
         return int(load_library().hpnfft_launch_count(self._h))

@@ -528,6 +528,34 @@ int64_t hpnfft_launch_count(hpnfft_plan_t h) {
   return p ? p->launches : -1;
 }
 
+int hpnfft_plan_info(hpnfft_plan_t h, int64_t* out, int n) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p || !out) {
+    set_error("NULL argument");
+    return HPNFFT_E_INVALID;
+  }
+  const int64_t c = 16;   // complex128
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2], N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
+  const bool slab = p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1;
+  const int64_t L = slab ? p->slab_len : p->plane_len;   // node planes of passes z and y
+  const int64_t N1r = slab ? N1 / p->nranks : N1;        // k1 rows of pass x
+  const int64_t xin = slab ? n0 : p->plane_len;          // planes pass x reads
+  int64_t v[8];
+  v[0] = c * L * n1 * (n2 + N2);
+  v[1] = c * L * N2 * (n1 + N1);
+  v[2] = c * N1r * N2 * (xin + N0);
+  v[3] = p->nranks <= 1 ? 0 : (!slab ? 1 : (p->virt ? 4 : (p->p2p ? 2 : 3)));
+  v[4] = p->plane_len;
+  v[5] = p->rec_group;
+  v[6] = (p->spread_method == HPNFFT_SPREAD_ATOMIC || (p->spread_method == HPNFFT_SPREAD_AUTO && !sweep_supported(p)))
+             ? HPNFFT_SPREAD_ATOMIC
+             : HPNFFT_SPREAD_SWEEP;
+  v[7] = (int64_t)p->ws_bytes;
+  int w = 0;
+  for (; w < n && w < 8; ++w) out[w] = v[w];
+  return w;
+}
+
 int hpnfft_enable_timing(hpnfft_plan_t h, int on) {
   Plan* p = reinterpret_cast<Plan*>(h);
   if (!p) {

@@ -103,6 +103,14 @@ def grid_slab_edges(x, world: int, n0: int, m: int = 6, group=None, reduce: bool
     hist = torch.bincount(mem, minlength=n0).to(torch.int64)
     if reduce and dist.is_available() and dist.is_initialized():
         dist.all_reduce(hist, group=group)
+    return grid_slab_edges_hist(hist, world, n0, m, plane_weight)
+
+
+def grid_slab_edges_hist(hist, world: int, n0: int, m: int = 6, plane_weight: float = 8000.0):
+    """The cut of grid_slab_edges on a histogram of the points over the MEMORY planes
+    (hist[c0], c0 = floor(n0 x0) mod n0; x = 0 is memory plane 0), e.g. accumulated chunk by chunk."""
+    import torch
+
     cost = hist.to(torch.float64) + float(plane_weight)
     cum = torch.cumsum(cost, 0).cpu().tolist()   # cum[e] = cost of the memory planes <= e
     total = cum[-1] if cum else 0
