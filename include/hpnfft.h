@@ -76,8 +76,9 @@ enum { HPNFFT_SPREAD_AUTO = 0, HPNFFT_SPREAD_ATOMIC = 1, HPNFFT_SPREAD_SWEEP = 2
  *   d      : dimension; only d = 3 is supported (else HPNFFT_E_UNSUPPORTED).
  *   N      : HOST array of d bandwidths N_t, each even and >= 2, else E_INVALID.
  *   M      : number of points this plan will be given (0 <= M < 2^31), else E_INVALID.
- *   m      : cut-off, 1 <= m <= 8 (PAPER.md:266 uses 1..15; GPU kernels are instantiated for
- *            1..8), else E_UNSUPPORTED.
+ *   m      : cut-off, 1 <= m <= 15 (PAPER.md:266 sweeps m = 1..15), else E_UNSUPPORTED.  The DMMA
+ *            sweep spread and gather serve m <= 8 (a chunk's CH + 2m - 1 node planes fit the
+ *            16-row accumulator); m = 9..15 run the generic atomic spread and warp gather.
  *   sigma  : oversampling factor > 1; n_t = sigma N_t must be an integer power of two >= 2m
  *            (PAPER.md:266 uses sigma = 2), else E_UNSUPPORTED (E_INVALID for sigma <= 1).
  *   window : HPNFFT_WINDOW_KAISER_BESSEL, _GAUSSIAN, _B_SPLINE or _SINC_POWER.

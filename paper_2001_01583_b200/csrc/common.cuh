@@ -12,7 +12,8 @@
 
 namespace hpnfft {
 
-constexpr int kMaxM = 8;          // GPU kernels are instantiated for m = kMinM..kMaxM
+constexpr int kMaxM = 15;         // GPU kernels are instantiated for m = kMinM..kMaxM
+constexpr int kMaxSweepM = 8;     // the sweep spread / gather: CH + 2m - 1 <= 16 accumulator rows
 constexpr int kMinM = 1;
 constexpr int kPolyDeg = 18;      // window tap polynomial degree (<= 2e-14
                                   // of Phi(0) for every window and m = 1..15, incl. the steep m = 1 Gaussian)

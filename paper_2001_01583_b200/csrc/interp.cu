@@ -25,7 +25,11 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
                                                       int64_t M, int n0, int n1, int n2) {
   constexpr int W = 2 * M_;
   constexpr int PD = kPolyDeg + 1;
-  static_assert(3 * W <= 64, "two shuffle rounds of taps");
+  // lanes (r, i2): R row groups of W lanes (R = 2 for 2m <= 16; m = 9..15: one group of 2m lanes)
+  constexpr int R = 2 * W <= 32 ? 2 : 1;
+  constexpr int NR = W / R;                 // rows i1 per lane
+  constexpr int TR = (3 * W + 31) / 32;     // shuffle rounds holding the 3 x 2m tap weights
+  static_assert(W <= 32, "one lane per tap along l2");
   __shared__ double poly[W * PD];
   for (int e = threadIdx.x; e < W * PD; e += blockDim.x) poly[e] = poly_g[e];
   __syncthreads();
@@ -46,23 +50,34 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
     const double tt = d == 0 ? a0.t : (d == 1 ? a1.t : a2.t);
     return q < 3 * W ? tap_weight(poly, i, tt, M_) : 0.0;
   };
-  const double tv0 = tap(lane), tv1 = tap(32 + lane);
-  auto weight = [&](int q) -> double {   // warp-uniform q
-    const double v0 = __shfl_sync(0xffffffffu, tv0, q & 31);
-    const double v1 = __shfl_sync(0xffffffffu, tv1, q & 31);
-    return q < 32 ? v0 : v1;
-  };
-  const int r = lane / W, i2 = lane - r * W;     // r in {0, 1} for the 2W active lanes
-  const bool act = lane < 2 * W;
-  const int l2 = (a2.c - M_ + 1 + (act ? i2 : 0)) & (n2 - 1);
-  // this lane's rows i1 = r, r + 2, ...: their w1 and grid row offsets, fetched once per point
-  double w1r[W / 2];
-  int row[W / 2];
+  double tv[TR];
 #pragma unroll
-  for (int q = 0; q < W / 2; ++q) {
-    const double wa = weight(W + 2 * q), wb = weight(W + 2 * q + 1);   // all lanes shuffle
-    w1r[q] = r == 0 ? wa : wb;
-    row[q] = ((a1.c - M_ + 1 + 2 * q + r) & (n1 - 1)) * n2 + l2;
+  for (int u = 0; u < TR; ++u) tv[u] = tap(32 * u + lane);
+  auto weight = [&](int q) -> double {   // warp-uniform q; every lane takes part in the shuffles
+    double v = 0.0;
+#pragma unroll
+    for (int u = 0; u < TR; ++u) {
+      const double s = __shfl_sync(0xffffffffu, tv[u], q & 31);
+      if ((q >> 5) == u) v = s;
+    }
+    return v;
+  };
+  const int r = lane / W, i2 = lane - r * W;     // r in [0, R) for the R W active lanes
+  const bool act = lane < R * W;
+  const int l2 = (a2.c - M_ + 1 + (act ? i2 : 0)) & (n2 - 1);
+  // this lane's rows i1 = r, r + R, ...: their w1 and grid row offsets, fetched once per point
+  double w1r[NR];
+  int row[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    double wq = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const double w = weight(W + R * q + rr);   // all lanes shuffle
+      if (rr == r) wq = w;
+    }
+    w1r[q] = wq;
+    row[q] = ((a1.c - M_ + 1 + R * q + r) & (n1 - 1)) * n2 + l2;
   }
   double sr = 0.0, si = 0.0, tr = 0.0, ti = 0.0;   // two accumulator pairs: shorter FMA chains
 #pragma unroll 2
@@ -71,15 +86,15 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
     const int l0 = (a0.c - M_ + 1 + i0) & (n0 - 1);
     const double2* plane = g + (size_t)l0 * n1 * n2;
     if (act) {
-      double2 v[W / 2];
+      double2 v[NR];
 #pragma unroll
-      for (int q = 0; q < W / 2; ++q) v[q] = __ldg(plane + row[q]);
+      for (int q = 0; q < NR; ++q) v[q] = __ldg(plane + row[q]);
 #pragma unroll
-      for (int q = 0; q < W / 2; q += 2) {
+      for (int q = 0; q < NR; q += 2) {
         const double wa = w0 * w1r[q];
         sr = fma(wa, v[q].x, sr);
         si = fma(wa, v[q].y, si);
-        if (q + 1 < W / 2) {
+        if (q + 1 < NR) {
           const double wb = w0 * w1r[q + 1];
           tr = fma(wb, v[q + 1].x, tr);
           ti = fma(wb, v[q + 1].y, ti);
@@ -89,7 +104,6 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
   }
   sr += tr;
   si += ti;
-  // (weight() shuffles: every lane calls it, the idle ones with a dummy index)
   const double w2raw = weight(2 * W + (act ? i2 : 0));
   const double w2 = act ? w2raw : 0.0;
   sr *= w2;
@@ -129,6 +143,13 @@ int interpolate(Plan* p, double* f) {
     case 6: return launch_interp<6>(p, f);
     case 7: return launch_interp<7>(p, f);
     case 8: return launch_interp<8>(p, f);
+    case 9: return launch_interp<9>(p, f);
+    case 10: return launch_interp<10>(p, f);
+    case 11: return launch_interp<11>(p, f);
+    case 12: return launch_interp<12>(p, f);
+    case 13: return launch_interp<13>(p, f);
+    case 14: return launch_interp<14>(p, f);
+    case 15: return launch_interp<15>(p, f);
     default:
       set_error("m not supported by the interpolation kernel");
       return HPNFFT_E_UNSUPPORTED;

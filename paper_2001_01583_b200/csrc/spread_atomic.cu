@@ -69,6 +69,13 @@ int spread_atomic(Plan* p, const double* f) {
     case 6: return launch_atomic<6>(p, f);
     case 7: return launch_atomic<7>(p, f);
     case 8: return launch_atomic<8>(p, f);
+    case 9: return launch_atomic<9>(p, f);
+    case 10: return launch_atomic<10>(p, f);
+    case 11: return launch_atomic<11>(p, f);
+    case 12: return launch_atomic<12>(p, f);
+    case 13: return launch_atomic<13>(p, f);
+    case 14: return launch_atomic<14>(p, f);
+    case 15: return launch_atomic<15>(p, f);
     default:
       set_error("m not supported by the spread kernels");
       return HPNFFT_E_UNSUPPORTED;

@@ -1466,6 +1466,7 @@ int run_interp_sweep(Plan* p, double* fout) {
 size_t record_bytes(int m) { return sizeof(double) * (22 + 4 * m); }
 
 bool sweep_supported(const Plan* p) {
+  if (p->m > kMaxSweepM) return false;   // m = 9..15: the generic atomic spread / warp gather
   const int W = 2 * p->m;
   const int P1 = 16, P2 = 32;   // largest extent of any patch variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;
