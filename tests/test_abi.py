@@ -59,7 +59,7 @@ def _plan(lib, N, M=10, m=6, sigma=2.0, window=0, d=None):
     ((15, 16, 16), {}, -1),            # odd bandwidth (N_t in 2N)
     ((0, 16, 16), {}, -1),
     ((16, 16), {}, -2),                # d = 2 not implemented on the GPU
-    ((16, 16, 16), {"m": 9}, -2),      # m outside the instantiated 1..8
+    ((16, 16, 16), {"m": 16}, -2),     # m outside PAPER.md:266 range 1..15
     ((16, 16, 16), {"m": 0}, -2),
     ((16, 16, 16), {"sigma": 1.0}, -1),
     ((16, 16, 16), {"sigma": 1.5}, -2),  # n_t = 24 is not a power of two
