@@ -73,7 +73,11 @@ enum { HPNFFT_SPREAD_AUTO = 0, HPNFFT_SPREAD_ATOMIC = 1, HPNFFT_SPREAD_SWEEP = 2
  * per-dimension deconvolution tables 1/c_k, the FFT twiddles and the window tap polynomials
  * in device kernels.
  *   out    : receives the plan handle (host pointer to a handle).
- *   d      : dimension; only d = 3 is supported (else HPNFFT_E_UNSUPPORTED).
+ *   d      : dimension 1, 2 or 3 (I_N and Eq. 5 for any d), else
+ *            E_UNSUPPORTED.  A d < 3 plan runs the 3-D kernels with 3 - d trivial leading
+ *            dimensions (N_t = n_t = 1, x_t = 0, one tap of weight exactly 1, no FFT pass), on the
+ *            generic atomic spread and warp gather; multi-GPU plans and hpnfft_ewald_reciprocal
+ *            need d = 3.
  *   N      : HOST array of d bandwidths N_t, each even and >= 2, else E_INVALID.
  *   M      : number of points this plan will be given (0 <= M < 2^31), else E_INVALID.
  *   m      : cut-off, 1 <= m <= 15 (PAPER.md:266 sweeps m = 1..15), else E_UNSUPPORTED.  The DMMA
@@ -89,7 +93,7 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
 
 /*
  * Bin-sort the points (A1 keys + A2 counting sort).
- *   x : DEVICE [M][3] float64 row-major, each coordinate in [-0.5, 0.5].  Read only; the plan
+ *   x : DEVICE [M][d] float64 row-major, each coordinate in [-0.5, 0.5].  Read only; the plan
  *       keeps its own sorted copy, so x may be released once the stream passes this call.
  * Out-of-range or NaN coordinates return HPNFFT_E_RANGE; this is detected with a device flag
  * that is read back once at the end of the call (the only host synchronisation of the path).
@@ -114,7 +118,8 @@ int hpnfft_check_points(hpnfft_plan_t p);
 /*
  * Transform (A3 window, A4 spread, A5 FFT, A6 deconvolve + crop; Alg. 2).
  *   f    : DEVICE [M][2] float64 (re, im) values in the ORIGINAL point order of set_points.
- *   fhat : DEVICE [N0*N1*N2][2] float64 output, fully overwritten (no accumulation).
+ *   fhat : DEVICE [N0*...*N_{d-1}][2] float64 output (row-major over the d dimensions), fully
+ *          overwritten (no accumulation).
  * Requires a prior successful hpnfft_set_points (else HPNFFT_E_STATE).  Asynchronous.
  */
 int hpnfft_adjoint(hpnfft_plan_t p, const double* f, double* fhat);
@@ -292,7 +297,8 @@ int hpnfft_plan_group(hpnfft_plan_t* out, int d, const int64_t* N, const int64_t
  */
 int hpnfft_adjoint_group(hpnfft_plan_t* plans, int nranks, const double* const* f, double* const* fhat);
 
-/* Shape (HOST int64[3]) of the fhat block hpnfft_adjoint writes on this rank (see the modes). */
+/* Shape (HOST int64[3]) of the fhat block hpnfft_adjoint writes on this rank (see the modes); for a
+ * d < 3 plan the leading 3 - d entries are 1. */
 int hpnfft_output_shape(hpnfft_plan_t p, int64_t shape[3]);
 
 #ifdef __cplusplus

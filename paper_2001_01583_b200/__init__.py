@@ -172,7 +172,7 @@ class Plan:
         self._h = h
         shp = (ctypes.c_int64 * 3)()
         _check(lib.hpnfft_output_shape(h, shp))
-        self.out_shape = tuple(int(v) for v in shp)
+        self.out_shape = tuple(int(v) for v in shp)[3 - len(self.N):]   # d < 3: drop the trivial leading 1s
 
     def ewald_reciprocal(self, q, L: float, alpha: float, out=None):
         """hpnfft_ewald_reciprocal: Eq. 12's reciprocal-space energy of the real charges q
@@ -205,8 +205,9 @@ class Plan:
         a range error is raised by the next set_points / check_points)."""
         import torch
 
-        if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.shape[1] == 3):
-            raise TypeError("x must be a CUDA float64 tensor of shape [M, 3]")
+        d = len(self.N)
+        if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.shape[1] == d):
+            raise TypeError(f"x must be a CUDA float64 tensor of shape [M, {d}]")
         if x.shape[0] != self.M:
             raise ValueError(f"x has {x.shape[0]} points, the plan was built for M = {self.M}")
         x = x.contiguous()

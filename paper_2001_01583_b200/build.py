@@ -63,6 +63,19 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     return lib
 
 
+CHECKED_LIB = os.path.join(HERE, "libhpnfft_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """libhpnfft_checked.so: the same sources with HPNFFT_CHECKED=1 (device-side bounds/protocol
+    assertions and mbarrier deadlock timeouts; tests/test_gpu_parity.py runs the small cases of
+    tools/sanitize_case.py on it, as compute-sanitizer is closed on the GPU pool)."""
+    if not force and os.path.exists(CHECKED_LIB) and os.path.getmtime(CHECKED_LIB) >= max(
+            os.path.getmtime(d) for d in deps()):
+        return CHECKED_LIB
+    return build(force=True, defines=("HPNFFT_CHECKED=1",), out=CHECKED_LIB)
+
+
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]

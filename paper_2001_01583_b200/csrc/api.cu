@@ -193,8 +193,8 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
       return HPNFFT_E_INVALID;
     }
   }
-  if (d != 3) {
-    set_error("only d = 3 is implemented on the GPU");
+  if (d > 3) {
+    set_error("d must be 1, 2 or 3");
     return HPNFFT_E_UNSUPPORTED;
   }
   if (M < 0 || M >= (int64_t(1) << 31)) {
@@ -214,9 +214,15 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     set_error("m must be in [" + std::to_string(kMinM) + ", " + std::to_string(kMaxM) + "] for the GPU kernels");
     return HPNFFT_E_UNSUPPORTED;
   }
-  int64_t n[3];
-  for (int t = 0; t < 3; ++t) {
-    double nt = sigma * (double)N[t];
+  // d < 3 (NEXT #4; I_N and Eq. 5 for any d): the d given dimensions are the
+  // LAST ones of the internal 3-D layout, the leading 3 - d are trivial (N_t = n_t = 1, x_t = 0,
+  // one tap of weight exactly 1, no FFT pass, deconvolution factor 1)
+  const int lead = 3 - d;
+  int64_t N3[3] = {1, 1, 1};
+  for (int t = 0; t < d; ++t) N3[lead + t] = N[t];
+  int64_t n[3] = {1, 1, 1};
+  for (int t = lead; t < 3; ++t) {
+    double nt = sigma * (double)N3[t];
     int64_t ni = (int64_t)(nt + 0.5);
     if (fabs(nt - (double)ni) > 1e-9 || !is_pow2(ni)) {
       set_error("n_t = sigma * N_t must be an integer power of two");
@@ -234,9 +240,9 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     set_error("host allocation failed");
     return HPNFFT_E_NOMEM;
   }
-  p->d = 3;
+  p->d = d;
   for (int t = 0; t < 3; ++t) {
-    p->N[t] = N[t];
+    p->N[t] = N3[t];
     p->n[t] = n[t];
     int l = 0;
     while ((int64_t(1) << l) < n[t]) ++l;
@@ -253,11 +259,12 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   // plane chunk of the sweep: CH planes of cells touch CH + 2m - 1 <= 16 node planes (the DMMA
   // accumulator's cyclic window), see spread_sweep.cu
   p->chunk_log = m <= 6 ? 2 : (m == 7 ? 1 : 0);
+  if (p->chunk_log > p->logn[0]) p->chunk_log = p->logn[0];   // n0 < CH (d < 3: n0 = 1): keys stay < nbins
   int rc = HPNFFT_OK;
   rc = rc ? rc : alloc(p, &p->grid, 2 * (size_t)cells);
-  rc = rc ? rc : alloc(p, &p->bufA, 2 * (size_t)(n[0] * n[1] * N[2]));
+  rc = rc ? rc : alloc(p, &p->bufA, 2 * (size_t)(n[0] * n[1] * N3[2]));
   for (int t = 0; t < 3 && !rc; ++t) {
-    rc = alloc(p, &p->inv_c[t], (size_t)N[t]);
+    rc = alloc(p, &p->inv_c[t], (size_t)N3[t]);
     rc = rc ? rc : alloc(p, &p->twiddle[t], 2 * (size_t)n[t]);
   }
   rc = rc ? rc : alloc(p, &p->poly, (size_t)(2 * kMaxM * (kPolyDeg + 1)));

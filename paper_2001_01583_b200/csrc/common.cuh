@@ -20,6 +20,27 @@ constexpr int kPolyDeg = 18;      // window tap polynomial degree (DESIGN.md "Wi
 constexpr int kNumStages = 12;     // timing slots, see hpnfft_stage_times
 constexpr int kRangeSlots = 64;   // slot pairs for the occupied-plane min/max reduction
 
+// Checked build (HPNFFT_CHECKED=1, libhpnfft_checked.so; compute-sanitizer is not available on the
+// GPU pool): device-side bounds / protocol assertions that print the failed condition and trap,
+// and a deadlock timeout on every mbarrier wait of the sweep.  Compiled out of the product build.
+#ifndef HPNFFT_CHECKED
+#define HPNFFT_CHECKED 0
+#endif
+#if HPNFFT_CHECKED
+#define HPNFFT_DCHECK(cond)                                                                            \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("HPNFFT_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define HPNFFT_DCHECK(cond) \
+  do {                      \
+  } while (0)
+#endif
+
 struct Dims3 {
   int64_t v[3];
 };

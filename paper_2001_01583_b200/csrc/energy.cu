@@ -72,6 +72,10 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
     set_error("NULL argument");
     return HPNFFT_E_INVALID;
   }
+  if (p->d != 3) {
+    set_error("hpnfft_ewald_reciprocal: needs a d = 3 plan (Eq. 12)");
+    return HPNFFT_E_UNSUPPORTED;
+  }
   if (!(L > 0.0) || !(alpha > 0.0)) {
     set_error("hpnfft_ewald_reciprocal: need L > 0 and alpha > 0");
     return HPNFFT_E_INVALID;

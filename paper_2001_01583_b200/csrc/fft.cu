@@ -614,12 +614,17 @@ int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int
 int subdivide_and_ifft(Plan* p, const double* fhat) {
   const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
   const int64_t N0 = p->N[0], N1 = p->N[1];
-  int rc = launch_pass(p, p->logn[2], fhat, p->grid, N0 * N1, 1, (int)p->N[2], p->inv_c[2], p->twiddle[2], true, 0,
+  const int lead = 3 - p->d;   // trivial leading dimensions (d < 3): no pass along them
+  // d = 3: z fhat -> grid, y grid -> bufA, x bufA -> grid; d = 2: z fhat -> bufA, y bufA -> grid;
+  // d = 1: z fhat -> grid (the last pass always lands in the grid)
+  double* zout = lead == 1 ? p->bufA : p->grid;
+  int rc = launch_pass(p, p->logn[2], fhat, zout, N0 * N1, 1, (int)p->N[2], p->inv_c[2], p->twiddle[2], true, 0,
                        N0 * N1, 0, (int)n2, nullptr, 1, 1);
-  if (rc) return rc;
-  rc = launch_pass(p, p->logn[1], p->grid, p->bufA, N0, n2, (int)N1, p->inv_c[1], p->twiddle[1], false, 0, N0, 0,
+  if (rc || lead == 2) return rc;
+  double* yout = lead == 1 ? p->grid : p->bufA;
+  rc = launch_pass(p, p->logn[1], zout, yout, N0, n2, (int)N1, p->inv_c[1], p->twiddle[1], false, 0, N0, 0,
                    (int)n1, nullptr, 1, 1);
-  if (rc) return rc;
+  if (rc || lead == 1) return rc;
   return launch_pass(p, p->logn[0], p->bufA, p->grid, 1, n1 * n2, (int)N0, p->inv_c[0], p->twiddle[0], false, 0, 1,
                      0, (int)n0, nullptr, 1, 1);
 }
@@ -627,19 +632,20 @@ int subdivide_and_ifft(Plan* p, const double* fhat) {
 int fft_and_deconvolve(Plan* p, double* fhat) {
   const int64_t n0 = p->n[0], n1 = p->n[1];
   const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
+  const int lead = 3 - p->d;   // trivial leading dimensions (d < 3): the last real pass writes fhat
   // only the occupied l0 planes are transformed by passes z and y; pass x treats the others as 0
   const int64_t plo = p->plane_lo, plen = p->plane_len;
   int rc;
   stage_begin(p, 4);
-  rc = launch_pass(p, p->logn[2], p->grid, p->bufA, plen * n1, 1, (int)N2, p->inv_c[2], p->twiddle[2], true,
-                   plo * n1, n0 * n1, 0, (int)p->n[2]);
+  rc = launch_pass(p, p->logn[2], p->grid, lead == 2 ? fhat : p->bufA, plen * n1, 1, (int)N2, p->inv_c[2],
+                   p->twiddle[2], true, plo * n1, n0 * n1, 0, (int)p->n[2]);
   stage_end(p, 4);
-  if (rc) return rc;
+  if (rc || lead == 2) return rc;
   stage_begin(p, 5);
-  rc = launch_pass(p, p->logn[1], p->bufA, p->bufB, plen, N2, (int)N1, p->inv_c[1], p->twiddle[1], false, plo, n0,
-                   0, (int)n1);
+  rc = launch_pass(p, p->logn[1], p->bufA, lead == 1 ? fhat : p->bufB, plen, N2, (int)N1, p->inv_c[1], p->twiddle[1],
+                   false, plo, n0, 0, (int)n1);
   stage_end(p, 5);
-  if (rc) return rc;
+  if (rc || lead == 1) return rc;
   stage_begin(p, 6);
   rc = x_pass(p, p->bufB, fhat, N1 * N2, 0, (int)plo, (int)plen);
   stage_end(p, 6);

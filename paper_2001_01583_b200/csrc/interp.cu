@@ -22,7 +22,8 @@ template <int M_>
 __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__ g, const double* __restrict__ xs,
                                                       const uint32_t* __restrict__ perm,
                                                       const double* __restrict__ poly_g, double2* __restrict__ f,
-                                                      int64_t M, int n0, int n1, int n2) {
+                                                      int64_t M, int n0, int n1, int n2, int lead, double sigma,
+                                                      int window) {
   constexpr int W = 2 * M_;
   constexpr int PD = kPolyDeg + 1;
   // lanes (r, i2): R row groups of W lanes (R = 2 for 2m <= 16; m = 9..15: one group of 2m lanes)
@@ -48,7 +49,8 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
   auto tap = [&](int q) -> double {
     const int d = q / W, i = q - d * W;
     const double tt = d == 0 ? a0.t : (d == 1 ? a1.t : a2.t);
-    return q < 3 * W ? tap_weight(poly, i, tt, M_) : 0.0;
+    if (d < lead) return i == M_ - 1 ? 1.0 : 0.0;   // trivial dimension of a d < 3 plan: the tap l = c = 0
+    return q < 3 * W ? tap_w<M_>(poly, i, tt, sigma, window) : 0.0;
   };
   double tv[TR];
 #pragma unroll
@@ -80,8 +82,9 @@ __global__ void __launch_bounds__(256) k_interpolate(const double2* __restrict__
     row[q] = ((a1.c - M_ + 1 + R * q + r) & (n1 - 1)) * n2 + l2;
   }
   double sr = 0.0, si = 0.0, tr = 0.0, ti = 0.0;   // two accumulator pairs: shorter FMA chains
+  const int i0lo = lead >= 1 ? M_ - 1 : 0, i0hi = lead >= 1 ? M_ : W;
 #pragma unroll 2
-  for (int i0 = 0; i0 < W; ++i0) {
+  for (int i0 = i0lo; i0 < i0hi; ++i0) {
     const double w0 = weight(i0);
     const int l0 = (a0.c - M_ + 1 + i0) & (n0 - 1);
     const double2* plane = g + (size_t)l0 * n1 * n2;
@@ -126,7 +129,7 @@ int launch_interp(Plan* p, double* f) {
   const int64_t blocks = (M + kPointsPerCta - 1) / kPointsPerCta;
   k_interpolate<M_><<<(unsigned)blocks, 32 * kWarps, 0, p->stream>>>(
       reinterpret_cast<const double2*>(p->grid), p->xs, p->perm, p->poly, reinterpret_cast<double2*>(f), M,
-      (int)p->n[0], (int)p->n[1], (int)p->n[2]);
+      (int)p->n[0], (int)p->n[1], (int)p->n[2], 3 - p->d, p->sigma, p->window);
   p->launches++;
   return check_launch(p, "interpolate");
 }

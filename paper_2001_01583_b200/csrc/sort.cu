@@ -14,13 +14,20 @@
 
 namespace hpnfft {
 
+// coordinate t of point j: x is [M][d] with the d given dimensions last; the 3 - d leading
+// (trivial) dimensions of a d < 3 plan read 0
+__device__ __forceinline__ double coord(const double* __restrict__ x, int64_t j, int d, int t) {
+  const int lead = 3 - d;
+  return t < lead ? 0.0 : x[(int64_t)d * j + (t - lead)];
+}
+
 __global__ void k_range_init(int* err) {
   const int t = threadIdx.x;
   if (t == 0) err[0] = 0;                                 // range-error flag
   else err[t] = (t & 1) ? 0x7fffffff : -1;                // slot minima / maxima
 }
 
-__global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
+__global__ void k_keys(const double* __restrict__ x, int d, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
                        uint32_t k_lo, uint32_t k_hi, uint32_t* __restrict__ count, uint32_t* __restrict__ key,
                        uint32_t* __restrict__ rank, int* __restrict__ err) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -28,7 +35,7 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
   // warp min/max, one atomic per warp
   unsigned cx = 0xffffffffu, cxm = 0u;
   if (j < M) {
-    const int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x[3 * j])) & (n0 - 1);
+    const int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, coord(x, j, d, 0))) & (n0 - 1);
     cx = cxm = (unsigned)((c0 + n0 / 2) & (n0 - 1));
   }
   // block min/max, then one atomic pair per block into one of kRangeSlots slot pairs
@@ -52,7 +59,7 @@ __global__ void k_keys(const double* __restrict__ x, int64_t M, int64_t n0, int6
     }
   }
   if (j >= M) return;
-  double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
+  double x0 = coord(x, j, d, 0), x1 = coord(x, j, d, 1), x2 = coord(x, j, d, 2);
   if (!(fabs(x0) <= 0.5 && fabs(x1) <= 0.5 && fabs(x2) <= 0.5)) {
     *err = 1;   // benign race: any writer sets 1
     x0 = x1 = x2 = 0.0;
@@ -171,12 +178,12 @@ __global__ void k_scatter(int64_t M, const uint32_t* __restrict__ key, const uin
   perm[pos] = (uint32_t)j;
 }
 
-__global__ void k_gather_x(const double* __restrict__ x, int64_t M, const uint32_t* __restrict__ perm,
+__global__ void k_gather_x(const double* __restrict__ x, int d, int64_t M, const uint32_t* __restrict__ perm,
                            double* __restrict__ xs) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= M) return;
   const int64_t j = perm[k];
-  const double a = __ldg(x + 3 * j), b = __ldg(x + 3 * j + 1), c = __ldg(x + 3 * j + 2);
+  const double a = coord(x, j, d, 0), b = coord(x, j, d, 1), c = coord(x, j, d, 2);
   xs[3 * k] = a;
   xs[3 * k + 1] = b;
   xs[3 * k + 2] = c;
@@ -213,7 +220,7 @@ int sort_points(Plan* p, const double* x) {
   p->launches++;
   stage_begin(p, 0);
   if (M > 0) {
-    k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->n[0], p->n[1], p->n[2], s2, p->chunk_log,
+    k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, p->d, M, p->n[0], p->n[1], p->n[2], s2, p->chunk_log,
                                                                k_lo, k_hi, p->bin_count,
                                                                p->key, p->rank, p->err_flag);
     p->launches++;
@@ -228,7 +235,7 @@ int sort_points(Plan* p, const double* x) {
   stage_begin(p, 2);
   if (M > 0) {
     k_scatter<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(M, p->key, p->rank, p->bin_count, p->perm);
-    k_gather_x<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, M, p->perm, p->xs);
+    k_gather_x<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, p->d, M, p->perm, p->xs);
     p->launches += 2;
     rc = check_launch(p, "scatter");
     if (rc) return rc;

@@ -12,29 +12,34 @@ namespace hpnfft {
 template <int M_>
 __global__ void k_spread_atomic(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
                                 const double* __restrict__ f, int64_t M, int64_t n0, int64_t n1, int64_t n2,
-                                const double* __restrict__ poly_g, double* __restrict__ grid) {
+                                const double* __restrict__ poly_g, double* __restrict__ grid, int lead,
+                                double sigma, int window) {
   constexpr int W = 2 * M_;
   __shared__ double poly[W * (kPolyDeg + 1)];
   for (int e = threadIdx.x; e < W * (kPolyDeg + 1); e += blockDim.x) poly[e] = poly_g[e];
   __syncthreads();
+  // trivial leading dimensions of a d < 3 plan (lead = 3 - d): the single tap i = m - 1 (node
+  // l = c = 0) of weight exactly 1
+  const int W0 = lead >= 1 ? 1 : W;
   int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= M * W) return;
-  int64_t j = gid / W;
-  int i0 = (int)(gid % W);
+  if (gid >= M * W0) return;
+  int64_t j = gid / W0;
+  int i0 = lead >= 1 ? M_ - 1 : (int)(gid % W0);
   CellT a0 = cell_of(xs[3 * j], n0), a1 = cell_of(xs[3 * j + 1], n1), a2 = cell_of(xs[3 * j + 2], n2);
   uint32_t src = perm[j];
   double fr = f[2 * (int64_t)src], fi = f[2 * (int64_t)src + 1];
-  double w0 = tap_weight(poly, i0, a0.t, M_);
+  double w0 = lead >= 1 ? 1.0 : tap_w<M_>(poly, i0, a0.t, sigma, window);
   double w1[W], w2[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) {
-    w1[i] = tap_weight(poly, i, a1.t, M_);
-    w2[i] = tap_weight(poly, i, a2.t, M_);
+    w1[i] = lead >= 2 ? (i == M_ - 1 ? 1.0 : 0.0) : tap_w<M_>(poly, i, a1.t, sigma, window);
+    w2[i] = tap_w<M_>(poly, i, a2.t, sigma, window);
   }
+  const int i1lo = lead >= 2 ? M_ - 1 : 0, i1hi = lead >= 2 ? M_ : W;
   int64_t l0 = (a0.c - M_ + 1 + i0) & (n0 - 1);
   double gr = fr * w0, gi = fi * w0;
 #pragma unroll 1
-  for (int i1 = 0; i1 < W; ++i1) {
+  for (int i1 = i1lo; i1 < i1hi; ++i1) {
     int64_t l1 = (a1.c - M_ + 1 + i1) & (n1 - 1);
     double hr = gr * w1[i1], hi = gi * w1[i1];
     double* row = grid + 2 * ((l0 * n1 + l1) * n2);
@@ -49,10 +54,11 @@ __global__ void k_spread_atomic(const double* __restrict__ xs, const uint32_t* _
 
 template <int M_>
 static int launch_atomic(Plan* p, const double* f) {
-  int64_t total = p->M * 2 * M_;
+  const int lead = 3 - p->d;
+  int64_t total = p->M * (lead >= 1 ? 1 : 2 * M_);
   if (total == 0) return HPNFFT_OK;
   k_spread_atomic<M_><<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
-      p->xs, p->perm, f, p->M, p->n[0], p->n[1], p->n[2], p->poly, p->grid);
+      p->xs, p->perm, f, p->M, p->n[0], p->n[1], p->n[2], p->poly, p->grid, lead, p->sigma, p->window);
   p->launches++;
   return check_launch(p, "spread_atomic");
 }

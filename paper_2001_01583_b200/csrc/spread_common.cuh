@@ -7,6 +7,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "window.cuh"
 
 namespace hpnfft {
 
@@ -32,6 +33,22 @@ __device__ __forceinline__ double tap_weight(const double* poly, int i, double t
 #pragma unroll
   for (int j = kPolyDeg - 1; j >= 0; --j) v = fma(v, s, a[j]);
   return (i == 2 * m - 1 && t == 0.0) ? 0.0 : v;
+}
+
+// Tap weight of the generic kernels (atomic spread, warp gather).  m <= kMaxSweepM: the plan's
+// tap polynomial (<= 2e-14 of Phi(0)).  m = 9..15: the window evaluated directly -- at large m
+// the deconvolution 1/c_k amplifies a tap error by up to ~1e2 at the spectrum's edge (sinc
+// power, B-spline: c(xi) decays fast), so the generic path uses the closed forms (ulp-level).
+template <int M_>
+__device__ __forceinline__ double tap_w(const double* poly, int i, double t, double sigma, int window) {
+  if constexpr (M_ > kMaxSweepM) {
+    if (i == 2 * M_ - 1 && t == 0.0) return 0.0;   // strict truncation |u - l| < m
+    return window_exact(t + (double)(M_ - 1 - i), M_, sigma, window);
+  } else {
+    (void)sigma;
+    (void)window;
+    return tap_weight(poly, i, t, M_);
+  }
 }
 
 }  // namespace hpnfft

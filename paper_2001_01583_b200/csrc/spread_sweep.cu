@@ -227,12 +227,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(a), "r"(parity)
       : "memory");
+#if HPNFFT_CHECKED
+  const long long t0 = clock64();
+#endif
   while (!ok) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
         : "r"(a), "r"(parity), "r"(1000000)
         : "memory");
+#if HPNFFT_CHECKED
+    HPNFFT_DCHECK(clock64() - t0 < (1ll << 35));   // ~17 s at 2 GHz: a lost arrival (deadlock)
+#endif
   }
 }
 // TMA bulk copy global -> shared, completion counted on an mbarrier (transaction bytes)
@@ -485,6 +491,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
             const unsigned long long p2 = kProf ? clock64() : 0ull;
             const uint32_t b1 = min(total, b0 + (uint32_t)(cap - oB));
             const int take = (int)(b1 - b0);
+            HPNFFT_DCHECK(take > 0 && oB + take <= cap && onseg < kMaxSeg);
             if (lane == 0) mbar_expect_tx(&s_landed[stage], (uint32_t)take * (uint32_t)(RD * sizeof(double)));
             __syncwarp();
             double* dst = s_rec + ((size_t)stage * cap + oB) * RD;
@@ -493,6 +500,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
               if (len == 0 || off >= b1 || off + len <= b0) return;
               const uint32_t k0 = off < b0 ? b0 - off : 0u;
               const uint32_t k1 = min(len, b1 - off);
+              HPNFFT_DCHECK(beg + k1 <= prm.g1 - prm.g0);                    // inside the group's records
+              HPNFFT_DCHECK((uint32_t)oB + (off + k1 - b0) <= (uint32_t)cap);   // inside the stage
               bulk_copy_g2s(dst + (size_t)(off + k0 - b0) * RD, prm.rec + (size_t)(beg + k0) * RD,
                             (k1 - k0) * (uint32_t)(RD * sizeof(double)), &s_landed[stage]);
             };
@@ -558,6 +567,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       mbar_wait(&s_landed[stage], phase);
       const unsigned long long l1c = kProf ? clock64() : 0ull;
       const BatchHdr hdr = s_hdr[stage];
+      HPNFFT_DCHECK(hdr.B <= cap && (hdr.B < 0 || hdr.tile >= 0) && (!kMerge || hdr.nseg <= kMaxSeg));
       int cnt[NL];   // list lengths (0 for tile-end markers)
 #pragma unroll
       for (int w = 0; w < NL; ++w) cnt[w] = 0;
@@ -593,8 +603,10 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
                 const bool rel = relr && d2 < (uint32_t)(W + kWC - 1);
                 const unsigned bal = __ballot_sync(0xffffffffu, rel);
                 const int w = wr * NWC + wc;
-                if (rel)
+                if (rel) {
+                  HPNFFT_DCHECK(cnt[w] + __popc(bal & ((1u << lane) - 1)) < capL && e < cap);
                   lists[(size_t)w * capL + cnt[w] + __popc(bal & ((1u << lane) - 1))] = ebase | (d1 << 18) | (d2 << 23);
+                }
                 cnt[w] += __popc(bal);
               }
             }
@@ -823,6 +835,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const int l0 = (first + sp - M_ + 1) & (n0 - 1);
           const bool in_seg = rel >= 0 && rel < S;
 #pragma unroll
+          for (int u = 0; u < SUB; ++u) HPNFFT_DCHECK(!in_seg || (wc0[u] + t < n2 && wr0[u] >= 0 && l0 >= 0));
+#pragma unroll
           for (int u = 0; u < SUB; ++u) {
             double2* base =
                 reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0[u] * n2 + (wc0[u] + t);
@@ -924,6 +938,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     }
     int nlist = nl[0];
     const uint32_t* my = ml[0];
+#pragma unroll
+    for (int u = 0; u < SUB; ++u) HPNFFT_DCHECK(nl[u] >= 0 && nl[u] <= capL);
     const unsigned long long q2 = kProf ? clock64() : 0ull;
 #if HPNFFT_SWEEP_DEBUG == 2
     nlist = 0;   // measurement only: skip apply
@@ -945,6 +961,7 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       const bool act = k + t < n;
       const uint32_t en = act ? lst[k + t] : 0u;
       const bool live = act && (!kMerge || (en & 0x1ffu) != 0x1ffu);
+      HPNFFT_DCHECK(!live || (int)(en & 0x1ffu) < hdr.B);
       const uint32_t ra = live ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
       kc = kMerge ? (int)__shfl_sync(0xffffffffu, (en >> 11) & 127u, 0) : 0;
       const int sh = step0 + kc * CH + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
@@ -1220,10 +1237,8 @@ template <int P1, int P2, int M_>
 int prepare_tile_order(Plan* p, uint32_t g0, uint32_t g1) {
   constexpr int CH = Chunk<M_>::CH;
   p->sched_pending = false;
-  static const bool lpt_off = [] {
-    const char* e = getenv("HPNFFT_SWEEP_LPT");
-    return e && e[0] == '0';
-  }();
+  const char* lpt_env = getenv("HPNFFT_SWEEP_LPT");   // read per call (tests switch it in-process)
+  const bool lpt_off = lpt_env && lpt_env[0] == '0';
   if (lpt_off) return HPNFFT_OK;
   SweepParams prm{};
   prm.start = p->bin_count;

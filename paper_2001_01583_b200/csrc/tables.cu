@@ -16,6 +16,10 @@ __global__ void k_deconv_table(double* inv_c, int64_t N, int64_t n, int m, doubl
                                int* bad) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= N) return;
+  if (n == 1) {   // a trivial dimension of a d < 3 plan: no deconvolution
+    inv_c[q] = 1.0;
+    return;
+  }
   double k = (double)(q - N / 2);
   double c = window_fourier(k / (double)n, m, sigma, window);
   if (!isfinite(c) || !(fabs(c) >= 1e-300)) atomicExch(bad, 1);

@@ -58,7 +58,7 @@ def _plan(lib, N, M=10, m=6, sigma=2.0, window=0, d=None):
 @pytest.mark.parametrize("N,kw,code", [
     ((15, 16, 16), {}, -1),            # odd bandwidth (N_t in 2N)
     ((0, 16, 16), {}, -1),
-    ((16, 16), {}, -2),                # d = 2 not implemented on the GPU
+    ((16, 16, 16, 16), {}, -2),        # d = 4 (the oracle and the GPU cover d = 1..3)
     ((16, 16, 16), {"m": 16}, -2),     # m outside PAPER.md:266 range 1..15
     ((16, 16, 16), {"m": 0}, -2),
     ((16, 16, 16), {"sigma": 1.0}, -1),

@@ -345,6 +345,101 @@ def test_multi_gpu_modes_match_single_gpu():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+# ---------------------------------------------- race / protocol checks without a sanitizer --
+def _run_py(code, env_extra=None, timeout=900):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=timeout)
+    return r
+
+
+def test_checked_build_all_kernel_families():
+    """compute-sanitizer is closed on the GPU pool, so libhpnfft_checked.so (HPNFFT_CHECKED=1:
+    device-side bounds and protocol assertions in the sweep's producer / list / consumer roles,
+    mbarrier deadlock timeouts) runs the small cases of every kernel family (tools/sanitize_case.py,
+    each compared with the CPU oracle): a violated assertion traps and fails the run."""
+    from paper_2001_01583_b200 import build as pb
+
+    lib = pb.build_checked()
+    r = _run_py("import runpy; runpy.run_path('tools/sanitize_case.py', run_name='__main__')", {"HPNFFT_LIB": lib})
+    assert r.returncode == 0 and "all cases ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_sweep_bitwise_reproducible_and_schedule_invariant(monkeypatch):
+    """Every grid node of the sweep is accumulated by one warp in a fixed record order, so with the
+    points sorted once the result is bitwise identical over repeated calls and under another tile
+    schedule (longest-first vs index order, i.e. other CTAs taking the tiles in another order): a
+    race between the copy, list and consumer roles or a stage reused too early would show up as a
+    differing bit (clustered points: heavy tiles, chunks overflowing the ring's stages)."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    N, M = (64, 64, 64), 200003
+    x, f = inputs.clustered_points(M, s=0.05, seed=60), inputs.uniform_values(M, seed=60)
+    p = hp.Plan(N, M, device=dev)
+    p.set_spread_method("sweep")
+    p.set_points(torch.from_numpy(x).to(dev))
+    ft = torch.from_numpy(f).to(dev)
+    ref = p.adjoint(ft).clone()
+    for _ in range(150):
+        assert torch.equal(p.adjoint(ft), ref)
+    monkeypatch.setenv("HPNFFT_SWEEP_LPT", "0")
+    for _ in range(5):
+        assert torch.equal(p.adjoint(ft), ref)
+    p.close()
+    assert oracle.rel_l2_error(ref.cpu().numpy(), oracle.nfft_adjoint(x, f, N)) <= 1e-12
+
+
+# ------------------------------------------------------------ d = 1, 2 plans (NEXT #4) --
+@pytest.mark.parametrize("N,M,m,window", [((256,), 1000, 6, "kb"), ((512,), 3001, 6, "kb"), ((64,), 700, 11, "kb"),
+                                          ((64, 32), 5003, 6, "kb"), ((512, 16), 4001, 4, "gaussian"),
+                                          ((16, 128), 2999, 13, "kb"), ((32, 32), 2000, 2, "b_spline")])
+def test_low_dim_adjoint_and_inverse(N, M, m, window):
+    """d = 1, 2 (I_N and Eq. 5 for any d): adjoint vs O2 at 1e-12 and O1 at the
+    method's error; inverse (Eq. 6) vs O2i at 1e-12; n = 1024 lines included."""
+    from oracle import windows
+
+    wid = {"kb": windows.KAISER_BESSEL, "gaussian": windows.GAUSSIAN, "b_spline": windows.B_SPLINE}[window]
+    d = len(N)
+    x = inputs.uniform_points(M, seed=50 + d, d=d)
+    x[0, 0] = 0.5
+    f = inputs.uniform_values(M, seed=50 + d)
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, M, m=m, window=window, device=dev)
+    assert plan.out_shape == N
+    plan.set_points(torch.from_numpy(x).to(dev))
+    g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+    fh = _spectrum(N, 51)
+    fl = plan.inverse(torch.from_numpy(fh).to(dev)).cpu().numpy()
+    plan.close()
+    assert g.shape == N
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= 1e-12
+    assert oracle.rel_l2_error(fl, oracle.nfft_inverse(x, fh, N, m=m, window=wid)) <= 1e-12
+    if window == "kb" and m >= 6:
+        assert oracle.rel_l2_error(g, oracle.ndft_direct(x, f, N)) <= 1e-9
+        assert oracle.rel_l2_error(fl, oracle.ndft_inverse_direct(x, fh, N)) <= 1e-9
+
+
+def test_low_dim_empty_and_errors():
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    p = hp.Plan((32, 16), 0, device=dev)
+    p.set_points(torch.zeros((0, 2), dtype=torch.float64, device=dev))
+    assert torch.all(p.adjoint(torch.zeros(0, dtype=torch.complex128, device=dev)) == 0)
+    p.close()
+    p = hp.Plan((32,), 3, device=dev)
+    with pytest.raises(ValueError):
+        p.set_points(torch.tensor([[0.1], [0.7], [0.2]], dtype=torch.float64, device=dev))
+    with pytest.raises(NotImplementedError):
+        p.ewald_reciprocal(torch.zeros(3, dtype=torch.float64, device=dev), 1.0, 1.0)
+    p.close()
+
+
 # ------------------------------------- the exchange code on ONE GPU (hpnfft_plan_group) --
 def _group_adjoint(x, f, N, P, mode, edges=None, m=6):
     """All P ranks of a multi-GPU plan as one group of plans on cuda:0: the grid-slab path runs
@@ -823,7 +918,13 @@ def test_fig12_precision_vs_m_all_windows():
             fl = plan.inverse(torch.from_numpy(s).to(dev)).cpu().numpy()
             plan.close()
             g = g.cpu().numpy()
-            assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m, window=wid)) <= 1e-12
+            o2 = oracle.nfft_adjoint(x, f, N, m=m, window=wid)
+            # the bar: 1e-12, or 4x the oracle's own rounding floor where that is higher -- O2 with
+            # its points summed in reverse order (Q21: sums are not order-invariant);
+            # only the sinc power at m >= 13 needs it (floor 1.4e-12 .. 1.2e-11, the deconvolution
+            # 1/c_k of that window grows steeply with m)
+            floor = oracle.rel_l2_error(oracle.nfft_adjoint(x[::-1], f[::-1], N, m=m, window=wid), o2)
+            assert oracle.rel_l2_error(g, o2) <= max(1e-12, 4 * floor), (name, m, floor)
             ea.append(oracle.rel_l2_error(g, s))
             eb.append(oracle.rel_l2_error(fl, fl_ref))
         table[name] = (ea, eb)
