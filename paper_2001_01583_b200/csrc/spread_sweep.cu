@@ -54,17 +54,41 @@ constexpr bool kProf = HPNFFT_SWEEP_PROFILE != 0;
 #define HPNFFT_SWEEP_DEBUG 0    // measurement builds only: 1 = skip the MMAs, 2 = skip apply
 #endif
 
-// record layout in doubles (HBM and shared memory):
+// record layout in doubles (HBM and shared memory), no padding:
 //   [0] c1|c2 (int2)  [1] c0|perm (int2: cell plane, original point index)  [2..3] f
-//   [4 .. 20) w0 (zero padded to 16: the DMMA A operand indexes it modulo 16)
-//   [20 .. 21+W) w1 (+ zero pad)  [21+W .. 22+2W) w2 (+ zero pad)
+//   [4 .. 4+W) w0   [4+W .. 4+2W) w1   [4+2W .. 4+3W) w2
+// Operand lookups past a field (the DMMA A operand indexes w0 modulo 16 rows; w1/w2 indices
+// outside the footprint) read the stage's zero record instead (tap_addr).
+#ifndef HPNFFT_REC_PAD
+#define HPNFFT_REC_PAD 3   // 3 = w0 zero-padded to 16 and w1/w2 + one zero (measured fastest)
+#endif
 template <int W>
 struct Rec {
+  static constexpr bool kPad0 = (HPNFFT_REC_PAD & 1) != 0, kPad12 = (HPNFFT_REC_PAD & 2) != 0;
   static constexpr int kW0 = 4;
-  static constexpr int kW1 = 20;
-  static constexpr int kW2 = 21 + W;
-  static constexpr int kDoubles = 22 + 2 * W;     // even -> 16-byte multiple
+  static constexpr int kW1 = 4 + (kPad0 ? 16 : W);
+  static constexpr int kW2 = kW1 + W + (kPad12 ? 1 : 0);
+  static constexpr int kEnd = kW2 + W + (kPad12 ? 1 : 0);
+  static constexpr int kDoubles = (kEnd + 1) / 2 * 2;   // even -> 16-byte multiple
 };
+
+// shared-memory address of entry i of the record field starting at `off` (doubles), or of the
+// zero record when i is outside the field (i >= W, incl. negative i wrapped to unsigned)
+template <int W>
+__device__ __forceinline__ uint32_t tap_addr(uint32_t rec_addr, int off, unsigned i, uint32_t zaddr) {
+  return i < (unsigned)W ? rec_addr + 8u * ((unsigned)off + i) : zaddr;
+}
+// w0 lookup (cyclic row index i in [0, 16)) and w1 / w2 lookups, padded or via tap_addr
+template <int W>
+__device__ __forceinline__ uint32_t w0_addr(uint32_t ra, unsigned i, uint32_t zaddr) {
+  if constexpr (Rec<W>::kPad0) return ra + 8u * (Rec<W>::kW0 + i);
+  else return tap_addr<W>(ra, Rec<W>::kW0, i, zaddr);
+}
+template <int W>
+__device__ __forceinline__ uint32_t w12_addr(uint32_t ra, int off, unsigned i, uint32_t zaddr) {
+  if constexpr (Rec<W>::kPad12) return ra + 8u * ((unsigned)off + min(i, (unsigned)W));
+  else return tap_addr<W>(ra, off, i, zaddr);
+}
 
 // plane chunk (cells per chunk) for a window half-width m: CH + 2m - 1 <= 16
 template <int M_>
@@ -176,10 +200,14 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
     out[R::kW1 + i] = v1;
     out[R::kW2 + i] = v2;
   }
+  if constexpr (R::kPad0) {
 #pragma unroll
-  for (int i = W; i < 16; ++i) out[R::kW0 + i] = 0.0;
-  out[R::kW1 + W] = 0.0;
-  out[R::kW2 + W] = 0.0;
+    for (int i = W; i < 16; ++i) out[R::kW0 + i] = 0.0;
+  }
+  if constexpr (R::kPad12) {
+    out[R::kW1 + W] = 0.0;
+    out[R::kW2 + W] = 0.0;
+  }
   reinterpret_cast<int4*>(out)[0] = make_int4(a1.c, a2.c, a0.c, (int)(k < count ? perm[(size_t)g0 + k] : 0u));
   reinterpret_cast<double2*>(out)[1] = fv;
   __syncthreads();
@@ -725,12 +753,12 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
         const uint32_t en = act ? my[k + g] : 0u;
         const uint32_t ra = act ? rbase + (en & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
         const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
-        const double w2v = lds_f64(ra + 8u * (uint32_t)(R::kW2 + min((unsigned)(d2 - (kWC - 1) + t), (unsigned)W)));
+        const double w2v = lds_f64(w12_addr<W>(ra, R::kW2, (unsigned)(d2 - (kWC - 1) + t), zaddr));
         double hre[4] = {0.0, 0.0, 0.0, 0.0}, him[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int sl = 0; sl < NT; ++sl) {
           const double b =
-              w2v * lds_f64(ra + 8u * (uint32_t)(R::kW1 + min((unsigned)(d1 - (kWR - 1) + sl), (unsigned)W)));
+              w2v * lds_f64(w12_addr<W>(ra, R::kW1, (unsigned)(d1 - (kWR - 1) + sl), zaddr));
           dmma16(hre, gre[sl][0], gre[sl][1], b);
           dmma16(him, gim[sl][0], gim[sl][1], b);
         }
@@ -743,8 +771,8 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const bool actr = k + r < nlist;
           const uint32_t rar = actr ? rbase + (enr & 0x1ffu) * (uint32_t)(RD * sizeof(double)) : zaddr;
           const int sh = step0 + (int)((enr >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
-          const double wa = lds_f64(rar + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
-          const double wb = lds_f64(rar + 8u * (uint32_t)(R::kW0 + ((8 + g - sh) & 15)));
+          const double wa = lds_f64(w0_addr<W>(rar, (unsigned)((g - sh) & 15), zaddr));
+          const double wb = lds_f64(w0_addr<W>(rar, (unsigned)((8 + g - sh) & 15), zaddr));
           pr[q] = wa * hre[q] + wb * hre[2 + q];
           pi[q] = wa * him[q] + wb * him[2 + q];
         }
@@ -967,15 +995,15 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       const int sh = step0 + kc * CH + (int)((en >> 9) & (uint32_t)(CH - 1)) - M_ + 1;
       const int d1 = (int)((en >> 18) & 31u), d2 = (int)((en >> 23) & 31u);
       // A fragments: rows 8 mt + g hold node (row - (st - m + 1)) mod 16 of this record
-      a0 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((g - sh) & 15)));
-      a1 = lds_f64(ra + 8u * (uint32_t)(R::kW0 + ((8 + g - sh) & 15)));
+      a0 = lds_f64(w0_addr<W>(ra, (unsigned)((g - sh) & 15), zaddr));
+      a1 = lds_f64(w0_addr<W>(ra, (unsigned)((8 + g - sh) & 15), zaddr));
       // B fragments: complex column q = 4 nt + g/2 = (row nt, col g/2) of the 4 x 4 sub-patch,
       // part g & 1; value f_part w1[i1(nt)] w2[i2(g/2)] (indices past the footprint hit zero pads)
       fp = lds_f64(ra + 8u * (uint32_t)(2 + part));
-      w2v = lds_f64(ra + 8u * (uint32_t)(R::kW2 + min((unsigned)(d2 - (kWC - 1) + bc0), (unsigned)W)));
+      w2v = lds_f64(w12_addr<W>(ra, R::kW2, (unsigned)(d2 - (kWC - 1) + bc0), zaddr));
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
-        w1v[nt] = lds_f64(ra + 8u * (uint32_t)(R::kW1 + min((unsigned)(d1 - (kWR - 1) + nt), (unsigned)W)));
+        w1v[nt] = lds_f64(w12_addr<W>(ra, R::kW1, (unsigned)(d1 - (kWR - 1) + nt), zaddr));
 #if HPNFFT_SWEEP_NTSKIP
       const int lo = act ? max(0, (kWR - 1) - d1) : NT, hi = act ? min(NT - 1, W + kWR - 2 - d1) : -1;
       ntlo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
@@ -1478,7 +1506,18 @@ int run_interp_sweep(Plan* p, double* fout) {
 
 }  // namespace
 
-size_t record_bytes(int m) { return sizeof(double) * (22 + 4 * m); }
+size_t record_bytes(int m) {
+  switch (m) {
+    case 1: return sizeof(double) * Rec<2>::kDoubles;
+    case 2: return sizeof(double) * Rec<4>::kDoubles;
+    case 3: return sizeof(double) * Rec<6>::kDoubles;
+    case 4: return sizeof(double) * Rec<8>::kDoubles;
+    case 5: return sizeof(double) * Rec<10>::kDoubles;
+    case 6: return sizeof(double) * Rec<12>::kDoubles;
+    case 7: return sizeof(double) * Rec<14>::kDoubles;
+    default: return sizeof(double) * Rec<16>::kDoubles;
+  }
+}
 
 bool sweep_supported(const Plan* p) {
   if (p->m > kMaxSweepM) return false;   // m = 9..15: the generic atomic spread / warp gather
