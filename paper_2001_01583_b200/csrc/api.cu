@@ -124,6 +124,9 @@ static void free_plan(Plan* p) {
     cudaFree(p->inv_c[t]);
     cudaFree(p->twiddle[t]);
   }
+  cudaFree(p->twiddle_half);
+  cudaFree(p->inv_c_ext[0]);
+  cudaFree(p->inv_c_ext[1]);
   cudaFree(p->poly);
   cudaFree(p->bin_count);
   cudaFree(p->key);
@@ -267,6 +270,9 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     rc = alloc(p, &p->inv_c[t], (size_t)N3[t]);
     rc = rc ? rc : alloc(p, &p->twiddle[t], 2 * (size_t)n[t]);
   }
+  rc = rc ? rc : alloc(p, &p->twiddle_half, (size_t)(n[2] > 1 ? n[2] : 2));
+  rc = rc ? rc : alloc(p, &p->inv_c_ext[0], (size_t)(N3[0] + 2));
+  rc = rc ? rc : alloc(p, &p->inv_c_ext[1], (size_t)(N3[1] + 2));
   rc = rc ? rc : alloc(p, &p->poly, (size_t)(2 * kMaxM * (kPolyDeg + 1)));
   rc = rc ? rc : alloc(p, &p->bin_count, (size_t)(p->nbins + 1));
   rc = rc ? rc : alloc(p, &p->key, (size_t)M);

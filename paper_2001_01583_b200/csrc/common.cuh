@@ -64,6 +64,9 @@ struct Plan {
   double* e_partial = nullptr;
   int64_t e_nparts = 0, e_cap = 0;
   double* fq = nullptr;   // [M] complex (q, 0) of hpnfft_ewald_reciprocal
+  // real values (the ENUF charges, NEXT #2): spread onto a REAL grid [n0][n1][n2] (doubles) and
+  // the R2C path of fft.cu (energy_r2c); set only inside hpnfft_ewald_reciprocal
+  bool real_values = false;
   bool failed = false;
   bool points_set = false;
 
@@ -73,6 +76,10 @@ struct Plan {
   double* bufB = nullptr;       // [n0][N1][N2] complex (aliases grid)
   double* inv_c[3] = {nullptr, nullptr, nullptr};   // 1/c_k per dim, index k + N/2
   double* twiddle[3] = {nullptr, nullptr, nullptr}; // exp(-2 pi i t/n_t), t < n_t (complex)
+  // real-charge energy path (energy_r2c): exp(-2 pi i t/(n2/2)), t < n2/2, and 1/c_k on the
+  // extended ranges k in [-N_t/2 - 1, N_t/2] (index k + N_t/2 + 1) of dimensions 0 and 1
+  double* twiddle_half = nullptr;
+  double* inv_c_ext[2] = {nullptr, nullptr};
   double* poly = nullptr;       // window tap polynomials [2m][kPolyDeg+1]
   // bin sort
   int64_t nbins = 0;            // n1 * (n2/8) * n0 bins (sort.cu: key order plane chunk, c1, c2/8, c0)
@@ -165,6 +172,9 @@ int spread_sweep(Plan* p, const double* f);
 bool sweep_supported(const Plan* p);
 size_t record_bytes(int m);
 int fft_and_deconvolve(Plan* p, double* fhat);
+// Eq. 12 for real charges (NEXT #2): R2C z pass + extended y pass + multiplicity-weighted x pass
+// over the real grid the REAL spread produced (fft.cu)
+int energy_r2c(Plan* p);
 // the last (x) pass of the adjoint: lines k1 in [k1_base, k1_base + inner / N2) of B[n0][.][N2],
 // deconvolved into fhat, or (p->energy) summed into Eq. 12's partials
 int x_pass(Plan* p, const double* in, double* fhat, int64_t inner, int64_t k1_base, int a_lo, int a_len);

@@ -9,6 +9,7 @@
 // |fhat|^2 per CTA instead of storing fhat (fft.cu x_pass); one CTA then adds the partials and
 // the self term in a fixed order (deterministic).  Grid-slab multi-GPU plans sum their k1 slabs'
 // terms and their own points' self terms, then all-reduce the scalar.
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace hpnfft {
@@ -122,7 +123,16 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
   p->energy = true;
   p->e_a = pi * pi / ((alpha * L) * (alpha * L));
   p->e_nparts = 0;
-  rc = dist_adjoint(p, p->fq, nullptr);   // single GPU: spread + FFT; grid slab: + exchange steps
+  const char* cenv = getenv("HPNFFT_ENERGY_COMPLEX");   // measurement / tests: the complex path
+  if (p->nranks <= 1 && !(cenv && cenv[0] == '1')) {
+    // one GPU: real charges -> the REAL spread onto a real grid and the R2C path (NEXT #2)
+    p->real_values = true;
+    rc = spread(p, p->fq);
+    if (!rc) rc = energy_r2c(p);
+    p->real_values = false;
+  } else {
+    rc = dist_adjoint(p, p->fq, nullptr);   // grid slab: complex spread + FFT + exchange steps
+  }
   p->energy = false;
   if (rc) return rc;
   k_energy_final<<<1, kThreads, 0, p->stream>>>(p->e_partial, p->e_nparts, q2_partial, kChargeBlocks,

@@ -78,6 +78,28 @@ __host__ __device__ constexpr int radix_of(int logn, int k) {
 }
 __host__ __device__ constexpr int ns_of(int logn, int k) { return k == 0 ? 1 : ns_of(logn, k - 1) * radix_of(logn, k - 1); }
 
+// kernel argument of the energy variant of the x pass: per-CTA partial sums go to partial[]
+struct EnergyArgs {
+  double* partial;
+  double e_a;
+  int64_t k1_base;
+  int N1, N2;
+  // real charges (NEXT #2, energy_r2c): the x pass runs over the Hermitian half spectrum
+  // k2 in [0, N2o/2] (N2 = N2o/2 + 1 columns, no shift) with k0, k1 extended to [-N/2, N/2]
+  // (N0 + 2, N1 + 2 outputs, shift N/2 + 1); every output counts for the points of I_N it
+  // represents: itself and its mirror -k (|S(-k)| = |S(k)| for real charges, Eq. 12)
+  int real_half;
+  int N0o, N1o, N2o;
+};
+
+// multiplicity of the half-spectrum frequency k (k2 >= 0) in Eq. 12's sum over I_N: k itself
+// (k2 < N2/2, k0, k1 in I) plus its mirror -k (k2 >= 1, -k0, -k1 in I)
+__device__ __forceinline__ double half_mult(int k0, int k1, int k2, const EnergyArgs& ea) {
+  const bool in0 = k0 >= -ea.N0o / 2 && k0 < ea.N0o / 2, in1 = k1 >= -ea.N1o / 2 && k1 < ea.N1o / 2;
+  const bool mi0 = -k0 >= -ea.N0o / 2 && -k0 < ea.N0o / 2, mi1 = -k1 >= -ea.N1o / 2 && -k1 < ea.N1o / 2;
+  return (double)((k2 < ea.N2o / 2 && in0 && in1) ? 1 : 0) + (double)((k2 >= 1 && mi0 && mi1) ? 1 : 0);
+}
+
 // Line context of one thread: its column in the shared tile, its global input/output line.
 struct LineIO {
   const cplx* gin;       // element a of the line at gin[a * istride]
@@ -103,14 +125,7 @@ struct LineIO {
   int64_t k1_base;
   int N1e, N2e;
   double esum;
-};
-
-// kernel argument of the energy variant of the x pass: per-CTA partial sums go to partial[]
-struct EnergyArgs {
-  double* partial;
-  double e_a;
-  int64_t k1_base;
-  int N1, N2;
+  EnergyArgs ea;
 };
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
@@ -200,10 +215,12 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
           const double sc = io.inv_c[k];
           const double re = v[b][r].x * sc, im = v[b][r].y * sc;
           const int64_t k1 = io.k1_base + io.line_i / io.N2e;
-          const double a0 = (double)(k - N / 2), a1 = (double)(k1 - io.N1e / 2),
-                       a2 = (double)(io.line_i % io.N2e - io.N2e / 2);
+          const int i0 = k - N / 2, i1 = (int)(k1 - io.N1e / 2);
+          const int i2 = io.ea.real_half ? (int)(io.line_i % io.N2e) : (int)(io.line_i % io.N2e - io.N2e / 2);
+          const double a0 = (double)i0, a1 = (double)i1, a2 = (double)i2;
           const double nn = a0 * a0 + a1 * a1 + a2 * a2;
-          if (nn > 0.0) io.esum += exp(-io.e_a * nn) / nn * (re * re + im * im);
+          const double mult = io.ea.real_half ? half_mult(i0, i1, i2, io.ea) : 1.0;
+          if (nn > 0.0 && mult > 0.0) io.esum += mult * exp(-io.e_a * nn) / nn * (re * re + im * im);
         }
       } else if (OUT_G && io.inv) {
         if (io.valid) io.gout[(int64_t)q * io.ostride] = {v[b][r].x, -v[b][r].y};
@@ -230,6 +247,14 @@ __device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cpl
   constexpr int NS = n_stages(LOGN);
   stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, K == NS - 1, EN>(buf, col, tj, tw, io);
   if constexpr (K + 1 < NS) run_stages<LOGN, TI, CONTIG, EN, K + 1>(buf, col, tj, tw, io);
+}
+
+// all stages into the shared tile (the R2C z pass post-processes the complex half-length transform)
+template <int LOGN, int TI, bool CONTIG, int K>
+__device__ __forceinline__ void run_stages_to_smem(cplx* buf, int col, int tj, const cplx* __restrict__ tw, LineIO& io) {
+  constexpr int NS = n_stages(LOGN);
+  stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, false, false>(buf, col, tj, tw, io);
+  if constexpr (K + 1 < NS) run_stages_to_smem<LOGN, TI, CONTIG, K + 1>(buf, col, tj, tw, io);
 }
 
 // Batched pruned pass.  Lines are indexed by (outer o, column i); element a of a line sits at
@@ -289,6 +314,7 @@ k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, i
   io.N1e = ea.N1;
   io.N2e = ea.N2 > 0 ? ea.N2 : 1;
   io.esum = 0.0;
+  io.ea = ea;
   run_stages<LOGN, TI, CONTIG, EN, 0>(smem, col, tj, tw, io);
   if constexpr (EN) {   // CTA partial of Eq. 12's sum, fixed order (deterministic)
     __shared__ double red[32];
@@ -479,7 +505,9 @@ __global__ void __launch_bounds__(32 * CW) k_fft1024_strided(const cplx* __restr
     double esum = 0.0;
     if (valid) {
       const int N2e = ea.N2 > 0 ? ea.N2 : 1;
-      const double b1 = (double)(ea.k1_base + ic / N2e - ea.N1 / 2), b2 = (double)(ic % N2e - N2e / 2);
+      const int i1 = (int)(ea.k1_base + ic / N2e - ea.N1 / 2);
+      const int i2 = ea.real_half ? (int)(ic % N2e) : (int)(ic % N2e - N2e / 2);
+      const double b1 = (double)i1, b2 = (double)i2;
 #pragma unroll
       for (int k2 = 0; k2 < 32; ++k2) {
         const int q = k1 + 32 * k2;
@@ -489,7 +517,8 @@ __global__ void __launch_bounds__(32 * CW) k_fft1024_strided(const cplx* __restr
           const double sc = inv_c[k];
           const double re = v[k2].x * sc, im = v[k2].y * sc, b0 = (double)(k - N / 2);
           const double nn = b0 * b0 + b1 * b1 + b2 * b2;
-          if (nn > 0.0) esum += exp(-ea.e_a * nn) / nn * (re * re + im * im);
+          const double mult = ea.real_half ? half_mult(k - N / 2, i1, i2, ea) : 1.0;
+          if (nn > 0.0 && mult > 0.0) esum += mult * exp(-ea.e_a * nn) / nn * (re * re + im * im);
         }
       }
     }
@@ -653,28 +682,106 @@ int fft_and_deconvolve(Plan* p, double* fhat) {
   return rc;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Real charges (Eq. 12 with real q): the z pass of a REAL grid line
+// x[0 .. n2) (the real sweep's output, read as h = n2/2 complex z[j] = x[2j] + i x[2j+1]): one
+// complex length-h Stockham transform Z in the shared tile, then the split
+//   X(k) = (Z(k) + conj Z(h-k))/2 - i exp(-2 pi i k/n2) (Z(k) - conj Z(h-k))/2,   k = 0 .. N2/2,
+// deconvolved by 1/c_k2 and stored as the Hermitian half line out[line][0 .. N2/2] (N2/2 + 1
+// complex): half the bytes of the complex pass, the other half follows from X(-k) = conj X(k).
+template <int LOGH, int TC>
+__global__ void __launch_bounds__(TC*((1 << LOGH) >= 8 ? (1 << LOGH) / 8 : 1))
+k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int N2,
+            const double* __restrict__ inv_c, const cplx* __restrict__ tw_h, const cplx* __restrict__ tw_n,
+            int64_t o_start, int64_t o_total) {
+  constexpr int h = 1 << LOGH;
+  constexpr int T = (h >= 8 ? h / 8 : 1);
+  extern __shared__ cplx smem[];
+  const int tid = threadIdx.x;
+  const int col = tid / T, tj = tid % T;
+  LineIO io;
+  const int64_t o = (int64_t)blockIdx.x * TC + col;
+  io.valid = o < outer;
+  const int64_t oc = io.valid ? (o_start + o) % o_total : 0;
+  io.gin = in + oc * (int64_t)h;
+  io.istride = 1;
+  io.a_lo = 0;
+  io.a_len = h;
+  io.inv = false;
+  io.peers = nullptr;
+  run_stages_to_smem<LOGH, TC, true, 0>(smem, col, tj, tw_h, io);
+  if (!io.valid) return;
+  const int N2h = N2 / 2 + 1;
+  cplx* gout = out + oc * (int64_t)N2h;
+  for (int k = tj; k < N2h; k += T) {
+    const cplx zk = smem[slot<LOGH, TC, true>(k & (h - 1), col)];
+    const cplx zr = smem[slot<LOGH, TC, true>((h - k) & (h - 1), col)];
+    const cplx e = {0.5 * (zk.x + zr.x), 0.5 * (zk.y - zr.y)};    // (Z(k) + conj Z(h-k)) / 2
+    const cplx d = {0.5 * (zk.x - zr.x), 0.5 * (zk.y + zr.y)};    // (Z(k) - conj Z(h-k)) / 2
+    const cplx wd = cmul(tw_n[k], d);                              // exp(-2 pi i k / n2) d
+    const double sc = inv_c[k < N2 / 2 ? k + N2 / 2 : 0];          // c_k even: c(N2/2) = c(-N2/2)
+    gout[k] = {(e.x + wd.y) * sc, (e.y - wd.x) * sc};              // e - i wd
+  }
+}
+
+template <int LOGH>
+static int launch_r2c_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int N2, const double* inv_c,
+                        const cplx* tw_h, const cplx* tw_n, int64_t o_start, int64_t o_total) {
+  constexpr int TC = tile_cols_contig<LOGH>();
+  constexpr int h = 1 << LOGH;
+  if (outer <= 0) return HPNFFT_OK;
+  const size_t smem = tile_elems<LOGH, TC, true>() * sizeof(cplx);
+  auto kern = k_fft_r2c_z<LOGH, TC>;
+  HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), smem), "r2c smem attr");
+  kern<<<(unsigned)((outer + TC - 1) / TC), TC * (h >= 8 ? h / 8 : 1), smem, p->stream>>>(in, out, outer, N2, inv_c,
+                                                                                       tw_h, tw_n, o_start, o_total);
+  p->launches++;
+  return check_launch(p, "fft r2c z pass");
+}
+
+static int launch_r2c(Plan* p, int logh, const double* in, double* out, int64_t outer, int64_t o_start,
+                      int64_t o_total) {
+  const cplx* ci = reinterpret_cast<const cplx*>(in);
+  cplx* co = reinterpret_cast<cplx*>(out);
+  const cplx* th = reinterpret_cast<const cplx*>(p->twiddle_half);
+  const cplx* tn = reinterpret_cast<const cplx*>(p->twiddle[2]);
+  const int N2 = (int)p->N[2];
+  const double* ic = p->inv_c[2];
+  switch (logh) {
+    case 1: return launch_r2c_n<1>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 2: return launch_r2c_n<2>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 3: return launch_r2c_n<3>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 4: return launch_r2c_n<4>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 5: return launch_r2c_n<5>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 6: return launch_r2c_n<6>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 7: return launch_r2c_n<7>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 8: return launch_r2c_n<8>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 9: return launch_r2c_n<9>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    default:
+      set_error("R2C length not supported");
+      return HPNFFT_E_UNSUPPORTED;
+  }
+}
+
 // x pass of Eq. 12 (ENUF reciprocal energy): the x lines of B[n0][L1][N2] (L1 = the k1 rows
 // this plan holds, starting at k1_base) with the deconvolution applied and the weighted |fhat|^2
 // summed per CTA into partial[] (nothing is stored).  Returns the number of partials (CTAs).
 template <int LOGN>
-static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_a, int64_t k1_base, double* partial,
-                               int a_lo, int a_len) {
+static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, int N0, const double* inv_c0,
+                               const EnergyArgs& ea, int a_lo, int a_len) {
   constexpr int TI = tile_cols<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
   if (LOGN == 10 && !fft1024_disabled()) {
     constexpr int CW = HPNFFT_F1024_CW;
     const size_t smem = sizeof(cplx) * (size_t)CW * (32 * 33 + 1);
-    if (set_max_smem(reinterpret_cast<const void*>(k_fft1024_strided<CW, true>), (int)smem) !=
-        cudaSuccess) {
+    if (set_max_smem(reinterpret_cast<const void*>(k_fft1024_strided<CW, true>), (int)smem) != cudaSuccess) {
       fail(p, HPNFFT_E_CUDA, "fft1024 smem attr");
       return -1;
     }
     const int64_t blocks = (inner + CW - 1) / CW;
-    EnergyArgs ea{partial, e_a, k1_base, (int)p->N[1], (int)p->N[2]};
     k_fft1024_strided<CW, true><<<(unsigned)blocks, 32 * CW, smem, p->stream>>>(
-        in, nullptr, inner, (int)p->N[0], p->inv_c[0], reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len,
-        ea);
+        in, nullptr, inner, N0, inv_c0, reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len, ea);
     p->launches++;
     return check_launch(p, "fft energy pass (n = 1024)") ? -1 : blocks;
   }
@@ -685,38 +792,64 @@ static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, double e_
     fail(p, HPNFFT_E_CUDA, "fft smem attr");
     return -1;
   }
-  EnergyArgs ea{partial, e_a, k1_base, (int)p->N[1], (int)p->N[2]};
-  kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, nullptr, 1, inner, (int)p->N[0], p->inv_c[0],
+  kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, nullptr, 1, inner, N0, inv_c0,
                                                    reinterpret_cast<const cplx*>(p->twiddle[0]), 0, 1, a_lo, a_len,
                                                    nullptr, 1, 0, ea, nullptr);
   p->launches++;
   return check_launch(p, "fft energy pass") ? -1 : blocks;
 }
 
-static int64_t energy_x_pass(Plan* p, const double* in, int64_t inner, double e_a, int64_t k1_base, double* partial,
-                             int a_lo, int a_len) {
+static int64_t energy_x_pass(Plan* p, const double* in, int64_t inner, int N0, const double* inv_c0,
+                             const EnergyArgs& ea, int a_lo, int a_len) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
   switch (p->logn[0]) {
-    case 2: return launch_energy_n<2>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 3: return launch_energy_n<3>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 4: return launch_energy_n<4>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 5: return launch_energy_n<5>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 6: return launch_energy_n<6>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 7: return launch_energy_n<7>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 8: return launch_energy_n<8>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 9: return launch_energy_n<9>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
-    case 10: return launch_energy_n<10>(p, ci, inner, e_a, k1_base, partial, a_lo, a_len);
+    case 2: return launch_energy_n<2>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 3: return launch_energy_n<3>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 4: return launch_energy_n<4>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 5: return launch_energy_n<5>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 6: return launch_energy_n<6>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 7: return launch_energy_n<7>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 8: return launch_energy_n<8>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 9: return launch_energy_n<9>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
+    case 10: return launch_energy_n<10>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
     default:
       set_error("FFT length not supported");
       return -1;
   }
 }
 
+// Eq. 12 for real charges on one GPU: R2C z pass (half lines k2 in [0, N2/2]) -> y pass with k1
+// extended to [-N1/2, N1/2] -> x pass with k0 extended to [-N0/2, N0/2] summing every half-spectrum
+// frequency with its multiplicity in I_N (half_mult).  Exact: the same sum as the complex path.
+int energy_r2c(Plan* p) {
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2], N2h = N2 / 2 + 1;
+  const int64_t plo = p->plane_lo, plen = p->plane_len;
+  stage_begin(p, 4);
+  int rc = launch_r2c(p, p->logn[2] - 1, p->grid, p->bufA, plen * n1, plo * n1, n0 * n1);
+  stage_end(p, 4);
+  if (rc) return rc;
+  stage_begin(p, 5);
+  rc = launch_pass(p, p->logn[1], p->bufA, p->grid, plen, N2h, (int)N1 + 2, p->inv_c_ext[1], p->twiddle[1], false,
+                   plo, n0, 0, (int)n1);
+  stage_end(p, 5);
+  if (rc) return rc;
+  stage_begin(p, 6);
+  EnergyArgs ea{p->e_partial, p->e_a, 0, (int)N1 + 2, (int)N2h, 1, (int)N0, (int)N1, (int)N2};
+  const int64_t nb = energy_x_pass(p, p->grid, (N1 + 2) * N2h, (int)N0 + 2, p->inv_c_ext[0], ea, (int)plo, (int)plen);
+  stage_end(p, 6);
+  if (nb < 0) return p->failed ? HPNFFT_E_CUDA : HPNFFT_E_UNSUPPORTED;
+  p->e_nparts = nb;
+  (void)n2;
+  return HPNFFT_OK;
+}
+
 int x_pass(Plan* p, const double* in, double* fhat, int64_t inner, int64_t k1_base, int a_lo, int a_len) {
   if (!p->energy)
     return launch_pass(p, p->logn[0], in, fhat, 1, inner, (int)p->N[0], p->inv_c[0], p->twiddle[0], false, 0, 1, a_lo,
                        a_len);
-  const int64_t nb = energy_x_pass(p, in, inner, p->e_a, k1_base, p->e_partial, a_lo, a_len);
+  EnergyArgs ea{p->e_partial, p->e_a, k1_base, (int)p->N[1], (int)p->N[2]};
+  const int64_t nb = energy_x_pass(p, in, inner, (int)p->N[0], p->inv_c[0], ea, a_lo, a_len);
   if (nb < 0) return p->failed ? HPNFFT_E_CUDA : HPNFFT_E_UNSUPPORTED;
   p->e_nparts = nb;
   return HPNFFT_OK;

@@ -13,7 +13,7 @@ template <int M_>
 __global__ void k_spread_atomic(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
                                 const double* __restrict__ f, int64_t M, int64_t n0, int64_t n1, int64_t n2,
                                 const double* __restrict__ poly_g, double* __restrict__ grid, int lead,
-                                double sigma, int window) {
+                                double sigma, int window, int real) {
   constexpr int W = 2 * M_;
   __shared__ double poly[W * (kPolyDeg + 1)];
   for (int e = threadIdx.x; e < W * (kPolyDeg + 1); e += blockDim.x) poly[e] = poly_g[e];
@@ -42,6 +42,12 @@ __global__ void k_spread_atomic(const double* __restrict__ xs, const uint32_t* _
   for (int i1 = i1lo; i1 < i1hi; ++i1) {
     int64_t l1 = (a1.c - M_ + 1 + i1) & (n1 - 1);
     double hr = gr * w1[i1], hi = gi * w1[i1];
+    if (real) {   // real values onto the REAL grid [n0][n1][n2] (NEXT #2)
+      double* row = grid + (l0 * n1 + l1) * n2;
+#pragma unroll
+      for (int i2 = 0; i2 < W; ++i2) atomicAdd(row + ((a2.c - M_ + 1 + i2) & (n2 - 1)), hr * w2[i2]);
+      continue;
+    }
     double* row = grid + 2 * ((l0 * n1 + l1) * n2);
 #pragma unroll
     for (int i2 = 0; i2 < W; ++i2) {
@@ -58,13 +64,14 @@ static int launch_atomic(Plan* p, const double* f) {
   int64_t total = p->M * (lead >= 1 ? 1 : 2 * M_);
   if (total == 0) return HPNFFT_OK;
   k_spread_atomic<M_><<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
-      p->xs, p->perm, f, p->M, p->n[0], p->n[1], p->n[2], p->poly, p->grid, lead, p->sigma, p->window);
+      p->xs, p->perm, f, p->M, p->n[0], p->n[1], p->n[2], p->poly, p->grid, lead, p->sigma, p->window,
+      p->real_values ? 1 : 0);
   p->launches++;
   return check_launch(p, "spread_atomic");
 }
 
 int spread_atomic(Plan* p, const double* f) {
-  size_t bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
+  size_t bytes = sizeof(double) * (p->real_values ? 1 : 2) * (size_t)(p->n[0] * p->n[1] * p->n[2]);
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->grid, 0, bytes, p->stream), "zero grid");
   switch (p->m) {
     case 1: return launch_atomic<1>(p, f);

@@ -338,7 +338,10 @@ __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap, bool merge) {
 
 // ------------------------------------------------------------------------------------------
 // A4: the warp-specialised persistent sweep (see the file header).
-template <int P1, int P2, int M_, bool INV, bool MERGE>
+// REAL (the ENUF charges): real values f_j = q_j onto a REAL grid
+// [n0][n1][n2] (doubles; the R2C z pass reads it as n2/2 complex per line): an n-tile is then 8
+// real columns = 2 rows x 4 columns of the 4 x 4 sub-patch, half the DMMAs of the complex sweep.
+template <int P1, int P2, int M_, bool INV, bool MERGE, bool REAL = false>
 __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((SweepCfg<P1, P2, M_>::kMaxRegs))
     k_spread_sweep(SweepParams prm) {
   using C = SweepCfg<P1, P2, M_>;
@@ -823,9 +826,16 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
     wc_off[u] = (spid % (P2 / kWC)) * kWC;
   }
   const int g = lane >> 2, t = lane & 3;
-  constexpr int NT = kWR * kWC / 4;       // n-tiles of 8 real columns (4 complex)
-  const int part = g & 1;                 // B: real (0) or imaginary (1) part of the column
-  const int bc0 = g >> 1;                 // B: column c of complex column q = 4 nt + g/2 (row nt)
+  static_assert(!(REAL && INV), "the real sweep is a spread");
+  // n-tiles of 8 real columns: complex = 4 complex columns (row nt, cols 0..3, re/im); REAL = 8
+  // real columns (rows 2 nt, 2 nt + 1, cols 0..3)
+  constexpr int NT = REAL ? kWR * kWC / 8 : kWR * kWC / 4;
+  const int part = REAL ? 0 : (g & 1);    // B: real (0) or imaginary (1) part of the column
+  const int bc0 = REAL ? (g & 3) : (g >> 1);   // B: sub-patch column of B's column g
+  const int br0 = REAL ? (g >> 2) : 0;    // B: row of B's column g within the n-tile (REAL)
+  // C: the complex column (row nt, col t) | REAL: the real columns 2t, 2t + 1 = (row 2 nt + t/2,
+  // cols 2 (t & 1), + 1) -- either way one 16-byte store per accumulator row
+  const int cr0 = REAL ? (t >> 1) : 0, cc0 = REAL ? 2 * (t & 1) : t;
   int cur_tile = -1;
   int first = 0, off = 0, S = 0, nsteps = 0;
   int wr0[SUB], wc0[SUB];
@@ -843,6 +853,15 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
   // rows g and g + 8 if they belong to a step of the block: nodes inside the tile's planes
   // [L0, L0 + S) (node - L0 = sp - m + 1 - off) go to the grid, then the row is zeroed.
   const size_t plane = (size_t)n1 * n2;
+  // row (within the sub-patch) and grid address of this lane's C columns of n-tile nt, plane l0
+  auto node_row = [&](int nt) { return REAL ? 2 * nt + cr0 : nt; };
+  auto node_dst = [&](int u, int l0, int nt) -> double2* {
+    if constexpr (REAL)
+      return reinterpret_cast<double2*>(prm.grid + (size_t)l0 * plane + (size_t)(wr0[u] + node_row(nt)) * n2 +
+                                        (wc0[u] + cc0));
+    else
+      return reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)(wr0[u] + nt) * n2 + (wc0[u] + cc0);
+  };
   auto advance = [&](int upto) {
 #if HPNFFT_SWEEP_DEBUG == 3
     cur = upto > cur ? upto : cur;   // measurement only: no flush
@@ -863,17 +882,15 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const int l0 = (first + sp - M_ + 1) & (n0 - 1);
           const bool in_seg = rel >= 0 && rel < S;
 #pragma unroll
-          for (int u = 0; u < SUB; ++u) HPNFFT_DCHECK(!in_seg || (wc0[u] + t < n2 && wr0[u] >= 0 && l0 >= 0));
+          for (int u = 0; u < SUB; ++u) HPNFFT_DCHECK(!in_seg || (wc0[u] + cc0 < n2 && wr0[u] >= 0 && l0 >= 0));
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
-            double2* base =
-                reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0[u] * n2 + (wc0[u] + t);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const double vx = a0 ? acc[u][nt][0] : acc[u][nt][2];
               const double vy = a0 ? acc[u][nt][1] : acc[u][nt][3];
-              if (in_seg && wr0[u] + nt < n1) {
-                double2* dst = base + (size_t)nt * n2;
+              if (in_seg && wr0[u] + node_row(nt) < n1) {
+                double2* dst = node_dst(u, l0, nt);
                 if (prm.accumulate) {
                   double2 o = *dst;
                   o.x += vx;
@@ -904,12 +921,10 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
           const int l0 = (first + sp - M_ + 1) & (n0 - 1);
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
-            double2* base =
-                reinterpret_cast<double2*>(prm.grid) + (size_t)l0 * plane + (size_t)wr0[u] * n2 + (wc0[u] + t);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {   // complex column (row nt, col t) of the sub-patch
-              if (rel >= 0 && rel < S && wr0[u] + nt < n1) {
-                double2* dst = base + (size_t)nt * n2;
+            for (int nt = 0; nt < NT; ++nt) {   // the lane's C columns of n-tile nt
+              if (rel >= 0 && rel < S && wr0[u] + node_row(nt) < n1) {
+                double2* dst = node_dst(u, l0, nt);
                 if (prm.accumulate) {
                   double2 o = *dst;
                   o.x += acc[u][nt][2 * h];
@@ -1003,8 +1018,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       w2v = lds_f64(w12_addr<W>(ra, R::kW2, (unsigned)(d2 - (kWC - 1) + bc0), zaddr));
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
-        w1v[nt] = lds_f64(w12_addr<W>(ra, R::kW1, (unsigned)(d1 - (kWR - 1) + nt), zaddr));
+        w1v[nt] = lds_f64(w12_addr<W>(ra, R::kW1, (unsigned)(d1 - (kWR - 1) + (REAL ? 2 * nt + br0 : nt)), zaddr));
 #if HPNFFT_SWEEP_NTSKIP
+      static_assert(!REAL, "n-tile skipping: complex sweep only");
       const int lo = act ? max(0, (kWR - 1) - d1) : NT, hi = act ? min(NT - 1, W + kWR - 2 - d1) : -1;
       ntlo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
       nthi = __reduce_max_sync(0xffffffffu, hi + 1) - 1;
@@ -1321,7 +1337,7 @@ int prepare_tile_order(Plan* p, uint32_t g0, uint32_t g1) {
   return HPNFFT_OK;
 }
 
-template <int P1, int P2, int M_, bool INV = false>
+template <int P1, int P2, int M_, bool INV = false, bool REAL = false>
 int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, bool accumulate, double* fout = nullptr) {
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
@@ -1376,9 +1392,9 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   }
   prm.prof = prof;
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->tile_counter, 0, sizeof(int), p->stream), "tile counter");
-  auto kern = k_spread_sweep<P1, P2, M_, INV, false>;
+  auto kern = k_spread_sweep<P1, P2, M_, INV, false, REAL>;
   if constexpr (!INV) {
-    if (merge) kern = k_spread_sweep<P1, P2, M_, false, true>;
+    if (merge) kern = k_spread_sweep<P1, P2, M_, false, true, REAL>;
   }
   HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                   "sweep smem attr");
@@ -1415,8 +1431,9 @@ int run_sweep(Plan* p, const double* f) {
   const uint32_t M = (uint32_t)p->M;
   const uint32_t G = (uint32_t)p->rec_group;
   const bool multi = M > G;
+  const bool real = p->real_values;   // real f (ENUF charges): the REAL sweep onto a real grid
   if (multi) {
-    const size_t bytes = sizeof(double) * 2 * (size_t)(p->n[0] * p->n[1] * p->n[2]);
+    const size_t bytes = sizeof(double) * (real ? 1 : 2) * (size_t)(p->n[0] * p->n[1] * p->n[2]);
     HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->grid, 0, bytes, p->stream), "zero grid");
   }
   uint32_t g0 = 0;
@@ -1424,7 +1441,7 @@ int run_sweep(Plan* p, const double* f) {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
     {
-      const int v = sweep_variant();
+      const int v = real ? 0 : sweep_variant();
       const int rco = v == 4 ? prepare_tile_order<12, 16, M_>(p, g0, g1)
                     : v == 3 ? prepare_tile_order<8, 16, M_>(p, g0, g1)
                     : v == 1 ? prepare_tile_order<12, 32, M_>(p, g0, g1)
@@ -1435,8 +1452,7 @@ int run_sweep(Plan* p, const double* f) {
     if (cnt > 0) {
       stage_begin(p, 7);
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
-      HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>),
-                                              (int)rsmem),
+      HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>), (int)rsmem),
                       "records smem attr");
       k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
           p->xs, p->perm, f, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
@@ -1452,12 +1468,17 @@ int run_sweep(Plan* p, const double* f) {
       k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
       p->launches++;
     }
-    const int var = sweep_variant();
-    const int rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
-                 : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
-                 : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
-                 : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                            : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
+    int rc;
+    if (real) {
+      rc = launch_sweep_group<8, 32, M_, false, true>(p, g0, g1, p->group_rows, multi);
+    } else {
+      const int var = sweep_variant();
+      rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
+         : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
+         : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
+         : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
+                    : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
+    }
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);

@@ -12,15 +12,17 @@
 
 namespace hpnfft {
 
-__global__ void k_deconv_table(double* inv_c, int64_t N, int64_t n, int m, double sigma, int window,
+// inv_c[q] = 1 / c(k / n) for k = q - koff, q < count (koff = N/2: k in I_N; the extended tables
+// of the real-charge path: count N + 2, koff N/2 + 1)
+__global__ void k_deconv_table(double* inv_c, int64_t count, int64_t koff, int64_t n, int m, double sigma, int window,
                                int* bad) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= N) return;
+  if (q >= count) return;
   if (n == 1) {   // a trivial dimension of a d < 3 plan: no deconvolution
     inv_c[q] = 1.0;
     return;
   }
-  double k = (double)(q - N / 2);
+  double k = (double)(q - koff);
   double c = window_fourier(k / (double)n, m, sigma, window);
   if (!isfinite(c) || !(fabs(c) >= 1e-300)) atomicExch(bad, 1);
   inv_c[q] = 1.0 / c;
@@ -76,10 +78,15 @@ int build_tables(Plan* p) {
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(bad, 0, sizeof(int), p->stream), "memset flag");
   for (int t = 0; t < 3; ++t) {
     int64_t N = p->N[t];
-    k_deconv_table<<<(unsigned)((N + 255) / 256), 256, 0, p->stream>>>(p->inv_c[t], N, p->n[t], p->m, p->sigma,
+    k_deconv_table<<<(unsigned)((N + 255) / 256), 256, 0, p->stream>>>(p->inv_c[t], N, N / 2, p->n[t], p->m, p->sigma,
                                                                      p->window, bad);
     k_twiddle_table<<<(unsigned)((p->n[t] + 255) / 256), 256, 0, p->stream>>>(p->twiddle[t], p->n[t]);
+    if (t < 2)
+      k_deconv_table<<<(unsigned)((N + 2 + 255) / 256), 256, 0, p->stream>>>(p->inv_c_ext[t], N + 2, N / 2 + 1, p->n[t],
+                                                                           p->m, p->sigma, p->window, bad);
   }
+  if (p->n[2] >= 2)
+    k_twiddle_table<<<(unsigned)((p->n[2] / 2 + 255) / 256), 256, 0, p->stream>>>(p->twiddle_half, p->n[2] / 2);
   k_window_poly<<<1, 32, 0, p->stream>>>(p->poly, p->m, p->sigma, p->window);
   int rc = check_launch(p, "table kernels");
   if (rc) return rc;

@@ -847,6 +847,35 @@ def test_fft_n1024_lines_four_step(N):
     assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N)) <= 1e-12
 
 
+@pytest.mark.parametrize("N", [(32, 16, 64), (16, 64, 8), (512, 8, 16), (8, 16, 512), (64, 64, 64)])
+@pytest.mark.parametrize("dist", ["uniform", "sparse"])
+def test_ewald_real_path_equals_complex_path(N, dist, monkeypatch):
+    """NEXT #2 (Eq. 12): real charges through the REAL sweep, the R2C z pass
+    (half lines k2 in [0, N2/2]) and the multiplicity-weighted x pass give the same energy as the
+    complex path (q + 0i through the complex spread and full spectrum), to rounding, and both
+    match Eq. 12 on the CPU NFFT's fhat (O2)."""
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    M = 5003 if dist == "uniform" else 301
+    x = inputs.uniform_points(M, seed=70)
+    q = np.random.default_rng(70).standard_normal(M)
+    L, alpha = 7.0, 0.8
+    vals = {}
+    for path in ("1", "0"):
+        monkeypatch.setenv("HPNFFT_ENERGY_COMPLEX", path)
+        p = hp.Plan(N, M, device=dev)
+        p.set_points(torch.from_numpy(x).to(dev))
+        vals[path] = p.ewald_reciprocal(torch.from_numpy(q).to(dev), L, alpha).item()
+        p.close()
+    fh = oracle.nfft_adjoint(x, q.astype(complex), N)
+    k = np.meshgrid(*[np.arange(-v // 2, v // 2) for v in N], indexing="ij")
+    nn = sum(kk.astype(float) ** 2 for kk in k)
+    w = np.where(nn > 0, np.exp(-np.pi ** 2 * nn / (alpha * L) ** 2) / np.where(nn > 0, nn, 1), 0.0)
+    ref = (w * np.abs(fh) ** 2).sum() / (2 * np.pi * L) - alpha / np.sqrt(np.pi) * (q ** 2).sum()
+    assert abs(vals["0"] - vals["1"]) <= 1e-13 * abs(ref)
+    assert abs(vals["0"] - ref) <= 1e-11 * abs(ref)
+
+
 @pytest.mark.parametrize("N", [(512, 8, 16), (16, 8, 32)])
 def test_ewald_reciprocal_x_pass_variants(N):
     """The energy x pass in both kernels (Stockham tile; four-step n0 = 1024) vs Eq. 12 on the
