@@ -15,7 +15,8 @@
 
 namespace hpnfft {
 
-struct cplx {
+// 16-byte aligned: every global and shared access of an element is one 128-bit load / store
+struct __align__(16) cplx {
   double x, y;
 };
 
