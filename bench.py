@@ -465,6 +465,85 @@ def _finish_inverse(args, plan, stages, ms_per_step, value, ws, rank, launches_p
         tdist.destroy_process_group()
 
 
+def run_f32(args):
+    """--precision f32: the FP32 plan (float coordinates, complex64
+    values, grid, FFT and fhat; shared-memory box spread) on config 4's points at --m (default 3,
+    the survey's low-m FP32 regime).  One step = set_points_f32 + adjoint_f32; its own JSON line."""
+    import torch
+
+    import paper_2001_01583_b200 as hp
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS[args.config]
+    N, M = cfg["N"], cfg["M"]
+    m = args.m if args.m else 3
+    x64, f64 = make_inputs(cfg, args.dist, dev)
+    x, f = x64.to(torch.float32), f64.to(torch.complex64)
+    del x64, f64
+    plan = hp.Plan(N, M, m=m, sigma=SIGMA, window="kb", device=dev, precision="f32")
+    out = torch.empty(plan.out_shape, dtype=torch.complex64, device=dev)
+
+    def step():
+        plan.set_points(x)
+        plan.adjoint(f, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = plan.launch_count()
+    plan.enable_timing(True)
+    plan.stage_times()
+    sampler = ClockSampler(0)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    stages = plan.stage_times()
+    ms = e0.elapsed_time(e1) / args.steps
+    info = plan.info()
+    n = [int(SIGMA * v) for v in N]
+    cells = n[0] * n[1] * n[2]
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    # the spread's algorithmic bytes: sorted coordinates (the plan's float64 copy, 24 B) + permutation
+    # (4 B) + complex64 value (8 B) per point, the complex64 grid zeroed and written once (2 x 8 B/cell)
+    sp_bytes = M * (24 + 4 + 8) + 2 * 8 * cells
+    fft_ms = sum(stages.get(k, 0.0) for k in ("fft_z", "fft_y", "fft_x_deconv"))
+    fft_b = sum(info["pass_bytes"].values()) // 2   # complex64: half the float64 pass bytes
+    dom = "spread" if stages.get("spread", 0.0) >= fft_ms else "fft"
+    if dom == "spread":
+        ach = sp_bytes / (stages["spread"] * 1e-3) / 1e9
+        roof = {"kernel": "k_spread_box_f32 (+ grid zero fill)", "bound": "hbm", "achieved": ach, "peak": hbm,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "algorithmic": "36 B/point (float64 sorted x, perm, complex64 f) + 16 B/cell (zero + write)"}
+    else:
+        ach = fft_b / (fft_ms * 1e-3) / 1e9
+        roof = {"kernel": "k_fft_pass<complex64> z, y, x", "bound": "hbm", "achieved": ach, "peak": hbm,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": None, "algorithmic": "pruned pass bytes (complex64)"}
+    line = {
+        "metric": f"adjoint NFFT (FP32 variant, NEXT #4) nonuniform points/s at N={N[0]}^3, KB m={m}",
+        "value": M / (ms * 1e-3), "unit": "points/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic seeded {args.dist} points (inputs/), rounded to float32",
+        "config": {"workload": f"config {args.config} points, FP32 plan: d=3, N={N[0]}^3, M={M}, KB m={m}, "
+                               f"sigma={SIGMA}, {args.dist}", "precision": "f32",
+                   "l2": "inputs larger than L2; no flush"},
+        "e2e": None, "gpu_launches": int(launches * args.steps), "roofline": roof, "cpu_baseline": None,
+        "clocks": clocks,
+        "detail": {"stages_ms": {k: round(v, 4) for k, v in stages.items()},
+                   "fft_hbm_frac": (fft_b / (fft_ms * 1e-3) / 1e9) / hbm if fft_ms else None},
+    }
+    print(json.dumps(line), flush=True)
+    plan.close()
+
+
 # ----------------------------------------------------------------------------- CPU oracle --
 def _host_cpu():
     """Host facts for the CPU-baseline record: usable cores and the CPU model."""
@@ -579,6 +658,9 @@ def main():
     ap.add_argument("--method", default="auto", choices=["auto", "atomic", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", default="equal_size", choices=["equal_size", "equal_count"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="f32 = the FP32 plan (NEXT #4), its own JSON line")
+    ap.add_argument("--m", type=int, default=0, help="window cut-off of the --precision f32 line (default 3)")
     ap.add_argument("--direction", default="adjoint", choices=["adjoint", "inverse"],
                     help="adjoint = Eq. 5 (the BASELINE metric); inverse = Eq. 6 (NEXT #1)")
     ap.add_argument("--exchange", default="grid_slab", choices=["allreduce", "reduce", "reduce_scatter", "grid_slab"],
@@ -588,6 +670,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.precision == "f32":
+        run_f32(args)
     else:
         run_ours(args)
 

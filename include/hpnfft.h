@@ -65,6 +65,9 @@ enum {
   HPNFFT_E_DEGENERATE_WINDOW = -8   /* a Fourier weight c_k is not finite or below 1e-300 */
 };
 
+/* Arithmetic precision of a plan (the FP32 variant). */
+enum { HPNFFT_PRECISION_F64 = 0, HPNFFT_PRECISION_F32 = 1 };
+
 /* Spread kernel selection (for measurement; HPNFFT_SPREAD_AUTO is the product default). */
 enum { HPNFFT_SPREAD_AUTO = 0, HPNFFT_SPREAD_ATOMIC = 1, HPNFFT_SPREAD_SWEEP = 2 };
 
@@ -139,6 +142,23 @@ int hpnfft_adjoint(hpnfft_plan_t p, const double* f, double* fhat);
  * workspace, so it must not overlap an hpnfft_adjoint of the same plan.  Asynchronous.
  */
 int hpnfft_inverse(hpnfft_plan_t p, const double* fhat, double* f);
+
+/*
+ * FP32 plans (the lower-precision variant): the same operation (Eq. 5)
+ * and conventions in float -- complex64 values, grid, FFT passes and fhat -- on float coordinates.
+ * Arguments as hpnfft_plan; m in [1, 8].  Spreading: shared-memory box accumulation (native float
+ * shared atomics, one vector float2 reduction per node into the zeroed grid); FFT: the pruned
+ * Stockham passes on complex64.  Accuracy: the method's error at m (E2 vs Eq. 5) plus float
+ * rounding (~1e-6 relative).  FP32 plans take only the _f32 calls below (plus
+ * destroy / last_error / workspace / stream / timing / info); the float64 calls on them (and the
+ * _f32 calls on a float64 plan) return HPNFFT_E_INVALID; no inverse, energy or multi-GPU plans.
+ */
+int hpnfft_plan_f32(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
+                    void* stream);
+/* x : DEVICE [M][d] float32 coordinates in [-0.5, 0.5] (as hpnfft_set_points). */
+int hpnfft_set_points_f32(hpnfft_plan_t p, const float* x);
+/* f : DEVICE [M][2] float32 (re, im) in the original point order; fhat : DEVICE [N0*..][2] float32. */
+int hpnfft_adjoint_f32(hpnfft_plan_t p, const float* f, float* fhat);
 
 /* Release the plan and its workspace (synchronises the plan's stream).  NULL is a no-op. */
 int hpnfft_destroy(hpnfft_plan_t p);

@@ -102,6 +102,12 @@ def load_library(path: str = LIB_PATH):
     lib.hpnfft_plan_group.restype = ctypes.c_int
     lib.hpnfft_adjoint_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp)]
     lib.hpnfft_adjoint_group.restype = ctypes.c_int
+    lib.hpnfft_plan_f32.argtypes = lib.hpnfft_plan.argtypes
+    lib.hpnfft_plan_f32.restype = ctypes.c_int
+    lib.hpnfft_set_points_f32.argtypes = [vp, dp]
+    lib.hpnfft_set_points_f32.restype = ctypes.c_int
+    lib.hpnfft_adjoint_f32.argtypes = [vp, dp, dp]
+    lib.hpnfft_adjoint_f32.restype = ctypes.c_int
     lib.hpnfft_plan_info.argtypes = [vp, i64p, ctypes.c_int]
     lib.hpnfft_plan_info.restype = ctypes.c_int
     lib.hpnfft_output_shape.argtypes = [vp, i64p]
@@ -141,7 +147,7 @@ class Plan:
     """
 
     def __init__(self, N, M: int, m: int = 6, sigma: float = 2.0, window="kb", stream=None, device=None, dist=None,
-                 _handle=None):
+                 _handle=None, precision: str = "f64"):
         import torch
 
         lib = load_library()
@@ -152,6 +158,9 @@ class Plan:
         self.m = int(m)
         self.sigma = float(sigma)
         self.window = WINDOWS[window] if isinstance(window, str) else int(window)
+        if precision not in ("f64", "f32"):
+            raise ValueError("precision must be 'f64' or 'f32'")
+        self.precision = precision   # f32: hpnfft_plan_f32 (float x, complex64 f and fhat; NEXT #4)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._stream = stream
         arr = (ctypes.c_int64 * len(self.N))(*self.N)
@@ -160,8 +169,8 @@ class Plan:
             if _handle is not None:   # a member of a PlanGroup (created by hpnfft_plan_group)
                 h = ctypes.c_void_p(_handle)
             elif dist is None:
-                _check(lib.hpnfft_plan(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window,
-                                       _stream_ptr(stream)))
+                fn = lib.hpnfft_plan_f32 if precision == "f32" else lib.hpnfft_plan
+                _check(fn(ctypes.byref(h), len(self.N), arr, self.M, self.m, self.sigma, self.window, _stream_ptr(stream)))
             else:
                 nranks, rank, uid, mode = dist
                 mode = DIST_MODES[mode] if isinstance(mode, str) else int(mode)
@@ -206,12 +215,16 @@ class Plan:
         import torch
 
         d = len(self.N)
-        if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.shape[1] == d):
-            raise TypeError(f"x must be a CUDA float64 tensor of shape [M, {d}]")
+        xt = torch.float32 if self.precision == "f32" else torch.float64
+        if not (x.is_cuda and x.dtype == xt and x.dim() == 2 and x.shape[1] == d):
+            raise TypeError(f"x must be a CUDA {xt} tensor of shape [M, {d}]")
         if x.shape[0] != self.M:
             raise ValueError(f"x has {x.shape[0]} points, the plan was built for M = {self.M}")
         x = x.contiguous()
         self._sync_stream()
+        if self.precision == "f32":
+            _check(load_library().hpnfft_set_points_f32(self._h, ctypes.c_void_p(x.data_ptr())))
+            return
         fn = load_library().hpnfft_set_points if sync else load_library().hpnfft_set_points_async
         _check(fn(self._h, ctypes.c_void_p(x.data_ptr())))
 
@@ -222,16 +235,17 @@ class Plan:
     def adjoint(self, f, out=None):
         import torch
 
-        if not (f.is_cuda and f.dtype == torch.complex128 and f.numel() == self.M):
-            raise TypeError("f must be a CUDA complex128 tensor with M elements")
+        ct = torch.complex64 if self.precision == "f32" else torch.complex128
+        if not (f.is_cuda and f.dtype == ct and f.numel() == self.M):
+            raise TypeError(f"f must be a CUDA {ct} tensor with M elements")
         f = f.contiguous()
         if out is None:
-            out = torch.empty(self.out_shape, dtype=torch.complex128, device=f.device)
-        elif not (out.is_cuda and out.dtype == torch.complex128 and tuple(out.shape) == self.out_shape
-                  and out.is_contiguous()):
-            raise TypeError(f"out must be a contiguous CUDA complex128 tensor of shape {self.out_shape}")
+            out = torch.empty(self.out_shape, dtype=ct, device=f.device)
+        elif not (out.is_cuda and out.dtype == ct and tuple(out.shape) == self.out_shape and out.is_contiguous()):
+            raise TypeError(f"out must be a contiguous CUDA {ct} tensor of shape {self.out_shape}")
         self._sync_stream()
-        _check(load_library().hpnfft_adjoint(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+        fn = load_library().hpnfft_adjoint_f32 if self.precision == "f32" else load_library().hpnfft_adjoint
+        _check(fn(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr())))
         return out
 
     def inverse(self, fhat, out=None):

@@ -125,6 +125,11 @@ static void free_plan(Plan* p) {
     cudaFree(p->twiddle[t]);
   }
   cudaFree(p->twiddle_half);
+  cudaFree(p->wpeak);
+  for (int t = 0; t < 3; ++t) {
+    cudaFree(p->twiddle_f[t]);
+    cudaFree(p->inv_cf[t]);
+  }
   cudaFree(p->inv_c_ext[0]);
   cudaFree(p->inv_c_ext[1]);
   cudaFree(p->poly);
@@ -175,8 +180,52 @@ const char* hpnfft_version(void) { return "hpnfft-b200 0.1 (sm_100a)"; }
 
 const char* hpnfft_last_error(void) { return g_last_error.c_str(); }
 
+}  // extern "C"
+
+namespace hpnfft {
+// dst = (float)(src * (scale ? *scale : 1))
+__global__ void k_to_float(float* __restrict__ dst, const double* __restrict__ src, int64_t count,
+                           const double* __restrict__ scale) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = (float)(scale ? src[i] * *scale : src[i]);
+}
+// FP32 plans: Phi(0) from the tap polynomial of tap m - 1 at t = 0 (s = -1).  The float kernels
+// use the window divided by Phi(0) and the deconvolution factors multiplied by it (per
+// dimension), which leaves fhat unchanged and keeps the products of three taps inside the float
+// range (KB m = 8: Phi(0)^3 ~ 1e45 would overflow)
+__global__ void k_window_peak(const double* __restrict__ poly, int m, double* __restrict__ peak) {
+  const double* a = poly + (m - 1) * (kPolyDeg + 1);
+  double v = a[kPolyDeg];
+  for (int j = kPolyDeg - 1; j >= 0; --j) v = fma(v, -1.0, a[j]);
+  *peak = v;
+}
+static int create_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
+                       void* stream, int precision);
+}  // namespace hpnfft
+
+extern "C" {
+
 int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
                 void* stream) {
+  return create_plan(out, d, N, M, m, sigma, window, stream, HPNFFT_PRECISION_F64);
+}
+
+int hpnfft_plan_f32(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
+                    void* stream) {
+  if (m > kMaxSweepM) {
+    if (out) *out = nullptr;
+    set_error("FP32 plans: m must be in [1, 8]");
+    return HPNFFT_E_UNSUPPORTED;
+  }
+  return create_plan(out, d, N, M, m, sigma, window, stream, HPNFFT_PRECISION_F32);
+}
+
+}  // extern "C"
+
+namespace hpnfft {
+
+static int create_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, double sigma, int window,
+                       void* stream, int precision) {
   if (!out) {
     set_error("hpnfft_plan: out is NULL");
     return HPNFFT_E_INVALID;
@@ -253,6 +302,7 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   }
   p->M = M;
   p->m = m;
+  p->precision = precision;
   p->sigma = sigma;
   p->window = window;
   p->stream = reinterpret_cast<cudaStream_t>(stream);
@@ -264,8 +314,10 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   p->chunk_log = m <= 6 ? 2 : (m == 7 ? 1 : 0);
   if (p->chunk_log > p->logn[0]) p->chunk_log = p->logn[0];   // n0 < CH (d < 3: n0 = 1): keys stay < nbins
   int rc = HPNFFT_OK;
-  rc = rc ? rc : alloc(p, &p->grid, 2 * (size_t)cells);
-  rc = rc ? rc : alloc(p, &p->bufA, 2 * (size_t)(n[0] * n[1] * N3[2]));
+  // complex grid and z-pass buffer: complex128, or complex64 for an FP32 plan
+  const size_t cdoubles = precision == HPNFFT_PRECISION_F32 ? 1 : 2;
+  rc = rc ? rc : alloc(p, &p->grid, cdoubles * (size_t)cells);
+  rc = rc ? rc : alloc(p, &p->bufA, cdoubles * (size_t)(n[0] * n[1] * N3[2]));
   for (int t = 0; t < 3 && !rc; ++t) {
     rc = alloc(p, &p->inv_c[t], (size_t)N3[t]);
     rc = rc ? rc : alloc(p, &p->twiddle[t], 2 * (size_t)n[t]);
@@ -326,6 +378,26 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
     }
   }
   if (!rc) rc = build_tables(p);
+  if (!rc && precision == HPNFFT_PRECISION_F32) {
+    rc = alloc(p, &p->wpeak, 1);
+    if (!rc) {
+      k_window_peak<<<1, 1, 0, p->stream>>>(p->poly, m, p->wpeak);
+      rc = check_launch(p, "window peak");
+    }
+    for (int t = 0; t < 3 && !rc; ++t) {
+      rc = alloc(p, &p->twiddle_f[t], 2 * (size_t)n[t]);
+      rc = rc ? rc : alloc(p, &p->inv_cf[t], (size_t)N3[t]);
+      if (!rc) {
+        k_to_float<<<(unsigned)((2 * n[t] + 255) / 256), 256, 0, p->stream>>>(p->twiddle_f[t], p->twiddle[t], 2 * n[t],
+                                                                             nullptr);
+        // trivial dimensions (n = 1) keep the factor 1: their single tap is exactly 1, not Phi
+        k_to_float<<<(unsigned)((N3[t] + 255) / 256), 256, 0, p->stream>>>(p->inv_cf[t], p->inv_c[t], N3[t],
+                                                                          n[t] > 1 ? p->wpeak : nullptr);
+        rc = check_launch(p, "float tables");
+      }
+    }
+    if (!rc && cudaStreamSynchronize(p->stream) != cudaSuccess) rc = fail(p, HPNFFT_E_CUDA, "float tables");
+  }
   if (rc) {
     free_plan(p);
     return rc;
@@ -333,6 +405,10 @@ int hpnfft_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, int m, d
   *out = reinterpret_cast<hpnfft_plan_t>(p);
   return HPNFFT_OK;
 }
+
+}  // namespace hpnfft
+
+extern "C" {
 
 namespace {
 
@@ -361,12 +437,12 @@ int check_pending(Plan* p) {
   return check_flags(p);
 }
 
-int set_points(Plan* p, const double* x, bool async) {
+int set_points(Plan* p, const double* x, bool async, const float* xf = nullptr) {
   if (p->failed) {
     set_error("plan is in a failed state (an earlier CUDA error)");
     return HPNFFT_E_STATE;
   }
-  if (!x && p->M > 0) {
+  if (!x && !xf && p->M > 0) {
     set_error("x is NULL");
     return HPNFFT_E_INVALID;
   }
@@ -374,7 +450,7 @@ int set_points(Plan* p, const double* x, bool async) {
   if (rc) return rc;
   p->points_set = false;
   p->launches = 0;
-  rc = sort_points(p, x);
+  rc = xf ? sort_points_f32(p, xf) : sort_points(p, x);
   if (rc) return rc;
   k_flags_to_host<<<1, 2 + 2 * kRangeSlots, 0, p->stream>>>(p->err_flag, 1 + 2 * kRangeSlots, p->dist_err,
                                                              p->err_flag_host_dev);
@@ -419,13 +495,59 @@ int set_points(Plan* p, const double* x, bool async) {
 
 }  // namespace
 
+static int precision_guard(Plan* p, int want) {
+  if (p->precision != want) {
+    set_error(want == HPNFFT_PRECISION_F64 ? "an FP32 plan takes the _f32 calls (float x, complex64 f, fhat)"
+                                           : "the _f32 calls need a plan made by hpnfft_plan_f32");
+    return HPNFFT_E_INVALID;
+  }
+  return HPNFFT_OK;
+}
+
 int hpnfft_set_points(hpnfft_plan_t h, const double* x) {
   Plan* p = reinterpret_cast<Plan*>(h);
   if (!p) {
     set_error("NULL plan");
     return HPNFFT_E_INVALID;
   }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F64)) return rc;
   return set_points(p, x, false);
+}
+
+int hpnfft_set_points_f32(hpnfft_plan_t h, const float* x) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F32)) return rc;
+  return set_points(p, nullptr, false, x);
+}
+
+int hpnfft_adjoint_f32(hpnfft_plan_t h, const float* f, float* fhat) {
+  Plan* p = reinterpret_cast<Plan*>(h);
+  if (!p) {
+    set_error("NULL plan");
+    return HPNFFT_E_INVALID;
+  }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F32)) return rc;
+  if (p->failed) {
+    set_error("plan is in a failed state (an earlier CUDA error)");
+    return HPNFFT_E_STATE;
+  }
+  if (!p->points_set) {
+    set_error("hpnfft_adjoint_f32 called before a successful hpnfft_set_points_f32");
+    return HPNFFT_E_STATE;
+  }
+  if (!fhat || (!f && p->M > 0)) {
+    set_error("f or fhat is NULL");
+    return HPNFFT_E_INVALID;
+  }
+  stage_begin(p, 3);
+  int rc = spread_f32(p, f);
+  stage_end(p, 3);
+  if (rc) return rc;
+  return fft_and_deconvolve_f32(p, fhat);
 }
 
 int hpnfft_set_points_async(hpnfft_plan_t h, const double* x) {
@@ -434,6 +556,7 @@ int hpnfft_set_points_async(hpnfft_plan_t h, const double* x) {
     set_error("NULL plan");
     return HPNFFT_E_INVALID;
   }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F64)) return rc;
   return set_points(p, x, true);
 }
 
@@ -460,6 +583,7 @@ int hpnfft_adjoint(hpnfft_plan_t h, const double* f, double* fhat) {
     set_error("hpnfft_adjoint called before a successful hpnfft_set_points");
     return HPNFFT_E_STATE;
   }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F64)) return rc;
   if (!fhat || (!f && p->M > 0)) {
     set_error("f or fhat is NULL");
     return HPNFFT_E_INVALID;
@@ -484,6 +608,7 @@ int hpnfft_inverse(hpnfft_plan_t h, const double* fhat, double* f) {
     set_error("hpnfft_inverse called before a successful hpnfft_set_points");
     return HPNFFT_E_STATE;
   }
+  if (int rc = precision_guard(p, HPNFFT_PRECISION_F64)) return rc;
   if (!fhat || (!f && p->M > 0)) {
     set_error("fhat or f is NULL");
     return HPNFFT_E_INVALID;

@@ -55,6 +55,7 @@ struct Plan {
   int m = 6;
   double sigma = 2.0;
   int window = HPNFFT_WINDOW_KAISER_BESSEL;
+  int precision = HPNFFT_PRECISION_F64;   // HPNFFT_PRECISION_F32: complex64 grid, FFT, values (NEXT #4)
   cudaStream_t stream = nullptr;
   int spread_method = HPNFFT_SPREAD_AUTO;
   // ENUF reciprocal energy (energy.cu): while `energy` is set, the last FFT pass (x_pass) sums
@@ -79,6 +80,10 @@ struct Plan {
   // real-charge energy path (energy_r2c): exp(-2 pi i t/(n2/2)), t < n2/2, and 1/c_k on the
   // extended ranges k in [-N_t/2 - 1, N_t/2] (index k + N_t/2 + 1) of dimensions 0 and 1
   double* twiddle_half = nullptr;
+  // FP32 plans: float copies of the twiddle and deconvolution tables
+  float* twiddle_f[3] = {nullptr, nullptr, nullptr};
+  float* inv_cf[3] = {nullptr, nullptr, nullptr};   // 1/c_k * Phi(0): the float kernels use Phi / Phi(0)
+  double* wpeak = nullptr;                          // device Phi(0) (FP32 plans)
   double* inv_c_ext[2] = {nullptr, nullptr};
   double* poly = nullptr;       // window tap polynomials [2m][kPolyDeg+1]
   // bin sort
@@ -164,6 +169,10 @@ void stage_end(Plan* p, int slot);
 // kernels' host launchers (each returns HPNFFT_OK or an error code)
 int build_tables(Plan* p);
 int sort_points(Plan* p, const double* x);
+int sort_points_f32(Plan* p, const float* x);   // FP32 plans: float coordinates, same keys
+// FP32 plans: shared-memory box spread (spread_f32.cu) and the complex64 FFT passes (fft.cu)
+int spread_f32(Plan* p, const float* f);
+int fft_and_deconvolve_f32(Plan* p, float* fhat);
 // bin keys [k_lo, k_hi) this plan's points may use (a grid-slab rank: its own planes' keys only;
 // the bin table is zeroed and scanned over that range only, sort.cu)
 void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi);

@@ -595,7 +595,7 @@ int check_dist_args(const char* fn, int nranks, int mode) {
 int init_dist_fields(Plan* p, int nranks, int rank, int mode) {
   const int64_t n0 = p->n[0];
   const int m = p->m;
-  if (p->d != 3 && nranks > 1) {
+  if ((p->d != 3 || p->precision != HPNFFT_PRECISION_F64) && nranks > 1) {
     set_error("multi-GPU plans need d = 3 (x-slab subcells of dimension 0, PAPER.md:93)");
     return HPNFFT_E_UNSUPPORTED;
   }

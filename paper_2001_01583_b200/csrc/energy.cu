@@ -73,8 +73,8 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
     set_error("NULL argument");
     return HPNFFT_E_INVALID;
   }
-  if (p->d != 3) {
-    set_error("hpnfft_ewald_reciprocal: needs a d = 3 plan (Eq. 12)");
+  if (p->d != 3 || p->precision != HPNFFT_PRECISION_F64) {
+    set_error("hpnfft_ewald_reciprocal: needs a float64 d = 3 plan (Eq. 12)");
     return HPNFFT_E_UNSUPPORTED;
   }
   if (!(L > 0.0) || !(alpha > 0.0)) {

@@ -15,57 +15,63 @@
 
 namespace hpnfft {
 
-// 16-byte aligned: every global and shared access of an element is one 128-bit load / store
-struct __align__(16) cplx {
-  double x, y;
+// Complex element of the FFT passes: double (the hot path) or float (the FP32 plans, NEXT #4).
+// Aligned to its size: every global and shared access of an element is one 128-bit (64-bit) load
+// or store.
+template <typename R>
+struct alignas(2 * sizeof(R)) CplxT {
+  using real = R;
+  R x, y;
 };
+using cplx = CplxT<double>;
+using cplxf = CplxT<float>;
 
-__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
-__device__ __forceinline__ cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
-__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
   return {fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
 }
-__device__ __forceinline__ cplx mul_minus_i(cplx a) { return {a.y, -a.x}; }   // a * (-i)
+template <typename C>
+__device__ __forceinline__ C mul_minus_i(C a) { return {a.y, -a.x}; }   // a * (-i)
 
-template <int R>
-__device__ __forceinline__ void dft(cplx* v);
-
-template <>
-__device__ __forceinline__ void dft<2>(cplx* v) {
-  cplx a = v[0], b = v[1];
-  v[0] = cadd(a, b);
-  v[1] = csub(a, b);
-}
-
-template <>
-__device__ __forceinline__ void dft<4>(cplx* v) {
-  cplx t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-  cplx t2 = cadd(v[1], v[3]), t3 = mul_minus_i(csub(v[1], v[3]));
-  v[0] = cadd(t0, t2);
-  v[2] = csub(t0, t2);
-  v[1] = cadd(t1, t3);
-  v[3] = csub(t1, t3);
-}
-
-template <>
-__device__ __forceinline__ void dft<8>(cplx* v) {
-  const double h = 0.70710678118654752440084436210484903;
-  cplx e[4] = {v[0], v[2], v[4], v[6]};
-  cplx o[4] = {v[1], v[3], v[5], v[7]};
-  dft<4>(e);
-  dft<4>(o);
-  // twiddles W8^k = exp(-i pi k/4)
-  cplx o1 = {h * (o[1].x + o[1].y), h * (o[1].y - o[1].x)};
-  cplx o2 = mul_minus_i(o[2]);
-  cplx o3 = {h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y)};
-  v[0] = cadd(e[0], o[0]);
-  v[4] = csub(e[0], o[0]);
-  v[1] = cadd(e[1], o1);
-  v[5] = csub(e[1], o1);
-  v[2] = cadd(e[2], o2);
-  v[6] = csub(e[2], o2);
-  v[3] = cadd(e[3], o3);
-  v[7] = csub(e[3], o3);
+// in-register DFT of RAD = 2, 4, 8 points
+template <int RAD, typename C>
+__device__ __forceinline__ void dft(C* v) {
+  using Rl = typename C::real;
+  if constexpr (RAD == 2) {
+    C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (RAD == 4) {
+    C t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    C t2 = cadd(v[1], v[3]), t3 = mul_minus_i(csub(v[1], v[3]));
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  } else {
+    static_assert(RAD == 8, "radix 2, 4 or 8");
+    const Rl h = (Rl)0.70710678118654752440084436210484903;
+    C e[4] = {v[0], v[2], v[4], v[6]};
+    C o[4] = {v[1], v[3], v[5], v[7]};
+    dft<4>(e);
+    dft<4>(o);
+    // twiddles W8^k = exp(-i pi k/4)
+    C o1 = {h * (o[1].x + o[1].y), h * (o[1].y - o[1].x)};
+    C o2 = mul_minus_i(o[2]);
+    C o3 = {h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y)};
+    v[0] = cadd(e[0], o[0]);
+    v[4] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], o1);
+    v[5] = csub(e[1], o1);
+    v[2] = cadd(e[2], o2);
+    v[6] = csub(e[2], o2);
+    v[3] = cadd(e[3], o3);
+    v[7] = csub(e[3], o3);
+  }
 }
 
 // Radix plan of an n = 2^LOGN point transform: as many radix-8 stages as possible, then one
@@ -102,17 +108,18 @@ __device__ __forceinline__ double half_mult(int k0, int k1, int k2, const Energy
 }
 
 // Line context of one thread: its column in the shared tile, its global input/output line.
-struct LineIO {
-  const cplx* gin;       // element a of the line at gin[a * istride]
-  cplx* gout;            // output k' at gout[k' * ostride]
+template <typename C>
+struct LineIOT {
+  const C* gin;          // element a of the line at gin[a * istride]
+  C* gout;               // output k' at gout[k' * ostride]
   int64_t istride, ostride;
   int N;                 // kept outputs
-  const double* inv_c;   // 1/c_k per kept output
+  const typename C::real* inv_c;   // 1/c_k per kept output
   bool valid;
   int a_lo, a_len;       // elements a with (a - a_lo) mod n < a_len are loaded, the others are 0
   // peer-memory output (multi-GPU grid-slab y pass): output k of line (o, i) is stored over
   // NVLink into rank k / NP's buffer at ((o NP + k mod NP) ostride + i); null = local output
-  cplx* const* peers;
+  C* const* peers;
   int NP;
   int64_t line_o, line_i;
   // inverse transform (Eq. 6 direction): the line's input is the compact N-entry line of fhat
@@ -128,6 +135,7 @@ struct LineIO {
   double esum;
   EnergyArgs ea;
 };
+using LineIO = LineIOT<cplx>;
 
 // One Stockham stage (radix R, sub-transform length Ns) on the line held in column `col` of the
 // shared tile.  Thread slot tj handles 8/R butterflies.  The first stage reads the line straight
@@ -148,13 +156,13 @@ constexpr size_t tile_elems() {
   return CONTIG ? (size_t)TI * ((1 << LOGN) + (1 << LOGN) / 8) : (size_t)(1 << LOGN) * (TI + 1);
 }
 
-template <int LOGN, int R, int Ns, int TI, bool CONTIG, bool IN_G, bool OUT_G, bool EN>
-__device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const cplx* __restrict__ tw,
-                                               LineIO& io) {
+template <int LOGN, int R, int Ns, int TI, bool CONTIG, bool IN_G, bool OUT_G, bool EN, typename C>
+__device__ __forceinline__ void stockham_stage(C* buf, int col, int tj, const C* __restrict__ tw, LineIOT<C>& io) {
+  using Rl = typename C::real;
   constexpr int n = 1 << LOGN;
   constexpr int BPT = (n >= 8 ? 8 : n) / R;   // butterflies per thread
   constexpr int T = (n >= 8 ? n / 8 : 1);     // threads per column
-  cplx v[BPT][R];
+  C v[BPT][R];
 #pragma unroll
   for (int b = 0; b < BPT; ++b) {
     const int j = tj + b * T;
@@ -167,15 +175,15 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
           const bool lo = a < N / 2, hi = a >= n - N / 2;
           const int k = lo ? a + N / 2 : a - (n - N / 2);
           if (io.valid && (lo || hi)) {
-            const cplx u = io.gin[(int64_t)k * io.istride];
-            const double sc = io.inv_c[k];
+            const C u = io.gin[(int64_t)k * io.istride];
+            const Rl sc = io.inv_c[k];
             v[b][r] = {u.x * sc, -u.y * sc};
           } else {
-            v[b][r] = {0.0, 0.0};
+            v[b][r] = {(Rl)0, (Rl)0};
           }
         } else {
           v[b][r] = (io.valid && ((a - io.a_lo) & (n - 1)) < io.a_len) ? io.gin[(int64_t)a * io.istride]
-                                                                        : cplx{0.0, 0.0};
+                                                                        : C{(Rl)0, (Rl)0};
         }
       } else {
         v[b][r] = buf[slot<LOGN, TI, CONTIG>(a, col)];
@@ -192,10 +200,10 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
       // products (one L1 load instead of seven; a few ulp per power, far below the 1e-12 bar)
       const int step = jm * (n / (Ns * R));
       if (R == 8) {
-        const cplx w1 = tw[step & (n - 1)];
-        const cplx w2 = cmul(w1, w1), w4 = cmul(w2, w2);
-        const cplx w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
-        const cplx ws[8] = {w1, w1, w2, w3, w4, w5, w6, w7};
+        const C w1 = tw[step & (n - 1)];
+        const C w2 = cmul(w1, w1), w4 = cmul(w2, w2);
+        const C w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+        const C ws[8] = {w1, w1, w2, w3, w4, w5, w6, w7};
 #pragma unroll
         for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], ws[r]);
       } else {
@@ -213,8 +221,8 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
         const bool lo = q < N / 2, hi = q >= n - N / 2;
         if (io.valid && (lo || hi)) {
           const int k = lo ? q + N / 2 : q - (n - N / 2);
-          const double sc = io.inv_c[k];
-          const double re = v[b][r].x * sc, im = v[b][r].y * sc;
+          const double sc = (double)io.inv_c[k];
+          const double re = (double)v[b][r].x * sc, im = (double)v[b][r].y * sc;
           const int64_t k1 = io.k1_base + io.line_i / io.N2e;
           const int i0 = k - N / 2, i1 = (int)(k1 - io.N1e / 2);
           const int i2 = io.ea.real_half ? (int)(io.line_i % io.N2e) : (int)(io.line_i % io.N2e - io.N2e / 2);
@@ -230,9 +238,9 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
         const bool lo = q < N / 2, hi = q >= n - N / 2;
         if (io.valid && (lo || hi)) {
           const int k = lo ? q + N / 2 : q - (n - N / 2);
-          const double sc = io.inv_c[k];
-          cplx* dst = io.peers ? io.peers[k / io.NP] + ((io.line_o * io.NP + k % io.NP) * io.ostride + io.line_i)
-                               : io.gout + (int64_t)k * io.ostride;
+          const Rl sc = io.inv_c[k];
+          C* dst = io.peers ? io.peers[k / io.NP] + ((io.line_o * io.NP + k % io.NP) * io.ostride + io.line_i)
+                            : io.gout + (int64_t)k * io.ostride;
           *dst = {v[b][r].x * sc, v[b][r].y * sc};
         }
       } else {
@@ -243,16 +251,16 @@ __device__ __forceinline__ void stockham_stage(cplx* buf, int col, int tj, const
   if (!OUT_G) __syncthreads();   // the tile is complete before the next stage reads it
 }
 
-template <int LOGN, int TI, bool CONTIG, bool EN, int K>
-__device__ __forceinline__ void run_stages(cplx* buf, int col, int tj, const cplx* __restrict__ tw, LineIO& io) {
+template <int LOGN, int TI, bool CONTIG, bool EN, int K, typename C>
+__device__ __forceinline__ void run_stages(C* buf, int col, int tj, const C* __restrict__ tw, LineIOT<C>& io) {
   constexpr int NS = n_stages(LOGN);
   stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, K == NS - 1, EN>(buf, col, tj, tw, io);
   if constexpr (K + 1 < NS) run_stages<LOGN, TI, CONTIG, EN, K + 1>(buf, col, tj, tw, io);
 }
 
 // all stages into the shared tile (the R2C z pass post-processes the complex half-length transform)
-template <int LOGN, int TI, bool CONTIG, int K>
-__device__ __forceinline__ void run_stages_to_smem(cplx* buf, int col, int tj, const cplx* __restrict__ tw, LineIO& io) {
+template <int LOGN, int TI, bool CONTIG, int K, typename C>
+__device__ __forceinline__ void run_stages_to_smem(C* buf, int col, int tj, const C* __restrict__ tw, LineIOT<C>& io) {
   constexpr int NS = n_stages(LOGN);
   stockham_stage<LOGN, radix_of(LOGN, K), ns_of(LOGN, K), TI, CONTIG, K == 0, false, false>(buf, col, tj, tw, io);
   if constexpr (K + 1 < NS) run_stages_to_smem<LOGN, TI, CONTIG, K + 1>(buf, col, tj, tw, io);
@@ -264,16 +272,17 @@ __device__ __forceinline__ void run_stages_to_smem(cplx* buf, int col, int tj, c
 // outers.  Output k' in [0,N) goes to out + (o * N + k') * inner + i, scaled by inv_c[k'].
 // Thread mapping: strided passes put consecutive lanes on consecutive columns (coalesced rows of
 // TI complex); the contiguous pass puts consecutive lanes on consecutive butterflies of a line.
-template <int LOGN, int TI, bool CONTIG, bool EN = false>
+template <int LOGN, int TI, bool CONTIG, bool EN = false, typename C = cplx>
 __global__ void __launch_bounds__(TI*((1 << LOGN) >= 8 ? (1 << LOGN) / 8 : 1))
-k_fft_pass(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int64_t inner, int N,
-           const double* __restrict__ inv_c, const cplx* __restrict__ tw, int64_t o_start, int64_t o_total, int a_lo,
-           int a_len, cplx* const* peers, int NP, int inv, EnergyArgs ea, const int* __restrict__ abort_flag) {
+k_fft_pass(const C* __restrict__ in, C* __restrict__ out, int64_t outer, int64_t inner, int N,
+           const typename C::real* __restrict__ inv_c, const C* __restrict__ tw, int64_t o_start, int64_t o_total,
+           int a_lo, int a_len, C* const* peers, int NP, int inv, EnergyArgs ea, const int* __restrict__ abort_flag) {
   constexpr int n = 1 << LOGN;
   constexpr int T = (n >= 8 ? n / 8 : 1);
-  extern __shared__ cplx smem[];
+  extern __shared__ __align__(16) unsigned char smem_bytes[];
+  C* smem = reinterpret_cast<C*>(smem_bytes);
   const int tid = threadIdx.x;
-  LineIO io;
+  LineIOT<C> io;
   io.N = N;
   io.inv_c = inv_c;
   io.a_lo = a_lo;
@@ -560,15 +569,17 @@ static bool fft1024_disabled() {   // HPNFFT_FFT1024=0: the generic Stockham pas
   return off;
 }
 
-template <int LOGN>
-static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int64_t inner, int N,
-                         const double* inv_c, const cplx* tw, bool contig, int64_t o_start, int64_t o_total,
-                         int a_lo, int a_len, cplx* const* peers, int NP, int inv) {
+template <int LOGN, typename C = cplx>
+static int launch_pass_n(Plan* p, const C* in, C* out, int64_t outer, int64_t inner, int N,
+                         const typename C::real* inv_c, const C* tw, bool contig, int64_t o_start, int64_t o_total,
+                         int a_lo, int a_len, C* const* peers, int NP, int inv) {
+  constexpr bool kF64 = sizeof(typename C::real) == 8;
   constexpr int TI = tile_cols<LOGN>();
   constexpr int TC = tile_cols_contig<LOGN>();
   constexpr int n = 1 << LOGN;
   constexpr int NT = TI * (n >= 8 ? n / 8 : 1);
   if (outer <= 0 || inner <= 0) return HPNFFT_OK;
+  if constexpr (kF64) {
   if (LOGN == 10 && contig && !inv && a_lo == 0 && a_len == n && !fft1024_disabled()) {
     k_fft1024_contig<<<(unsigned)((outer + kF1024Lines - 1) / kF1024Lines), 32 * kF1024Lines, 0, p->stream>>>(
         in, out, outer, N, inv_c, tw, o_start, o_total);
@@ -587,19 +598,20 @@ static int launch_pass_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int6
     p->launches++;
     return check_launch(p, "fft pass (n = 1024, strided)");
   }
+  }
   if (contig) {
-    const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(cplx);
+    const size_t smem = tile_elems<LOGN, TC, true>() * sizeof(C);
     const int64_t blocks = (outer + TC - 1) / TC;
-    auto kern = k_fft_pass<LOGN, TC, true>;
+    auto kern = k_fft_pass<LOGN, TC, true, false, C>;
     HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, TC * (n >= 8 ? n / 8 : 1), smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw,
                                                                             o_start, o_total, a_lo, a_len, nullptr, 1, inv,
                                                                             EnergyArgs{}, nullptr);
   } else {
-    const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(cplx);
+    const size_t smem = tile_elems<LOGN, TI, false>() * sizeof(C);
     const int64_t blocks = outer * ((inner + TI - 1) / TI);
-    auto kern = k_fft_pass<LOGN, TI, false>;
+    auto kern = k_fft_pass<LOGN, TI, false, false, C>;
     HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), (int)smem),
                     "fft smem attr");
     kern<<<(unsigned)blocks, NT, smem, p->stream>>>(in, out, outer, inner, N, inv_c, tw, o_start, o_total, a_lo,
@@ -629,6 +641,56 @@ static int launch_pass(Plan* p, int logn, const double* in, double* out, int64_t
       set_error("FFT length not supported");
       return HPNFFT_E_UNSUPPORTED;
   }
+}
+
+// FP32 plans (NEXT #4): the same pruned Stockham passes on complex64 lines (no four-step n = 1024
+// special case), float twiddles and deconvolution tables
+static int launch_pass_f32(Plan* p, int logn, const float* in, float* out, int64_t outer, int64_t inner, int N,
+                           const float* inv_c, const float* tw, bool contig, int64_t o_start, int64_t o_total,
+                           int a_lo, int a_len) {
+  const cplxf* ci = reinterpret_cast<const cplxf*>(in);
+  cplxf* co = reinterpret_cast<cplxf*>(out);
+  const cplxf* ct = reinterpret_cast<const cplxf*>(tw);
+  switch (logn) {
+    case 2: return launch_pass_n<2, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 3: return launch_pass_n<3, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 4: return launch_pass_n<4, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 5: return launch_pass_n<5, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 6: return launch_pass_n<6, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 7: return launch_pass_n<7, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 8: return launch_pass_n<8, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 9: return launch_pass_n<9, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    case 10: return launch_pass_n<10, cplxf>(p, ci, co, outer, inner, N, inv_c, ct, contig, o_start, o_total, a_lo, a_len, nullptr, 1, 0);
+    default:
+      set_error("FFT length not supported");
+      return HPNFFT_E_UNSUPPORTED;
+  }
+}
+
+// FP32 adjoint: passes z, y, x (+ deconvolve, crop) of the complex64 grid (d < 3: fewer passes)
+int fft_and_deconvolve_f32(Plan* p, float* fhat) {
+  const int64_t n0 = p->n[0], n1 = p->n[1];
+  const int64_t N1 = p->N[1], N2 = p->N[2];
+  const int lead = 3 - p->d;
+  const int64_t plo = p->plane_lo, plen = p->plane_len;
+  float* grid = reinterpret_cast<float*>(p->grid);
+  float* bufA = reinterpret_cast<float*>(p->bufA);
+  int rc;
+  stage_begin(p, 4);
+  rc = launch_pass_f32(p, p->logn[2], grid, lead == 2 ? fhat : bufA, plen * n1, 1, (int)N2, p->inv_cf[2], p->twiddle_f[2],
+                       true, plo * n1, n0 * n1, 0, (int)p->n[2]);
+  stage_end(p, 4);
+  if (rc || lead == 2) return rc;
+  stage_begin(p, 5);
+  rc = launch_pass_f32(p, p->logn[1], bufA, lead == 1 ? fhat : grid, plen, N2, (int)N1, p->inv_cf[1], p->twiddle_f[1],
+                       false, plo, n0, 0, (int)n1);
+  stage_end(p, 5);
+  if (rc || lead == 1) return rc;
+  stage_begin(p, 6);
+  rc = launch_pass_f32(p, p->logn[0], grid, fhat, 1, N1 * N2, (int)p->N[0], p->inv_cf[0], p->twiddle_f[0], false, 0, 1,
+                       (int)plo, (int)plen);
+  stage_end(p, 6);
+  return rc;
 }
 
 int fft_pass(Plan* p, int dim, const double* in, double* out, int64_t outer, int64_t inner, bool contig,
@@ -697,7 +759,8 @@ k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, 
             int64_t o_start, int64_t o_total) {
   constexpr int h = 1 << LOGH;
   constexpr int T = (h >= 8 ? h / 8 : 1);
-  extern __shared__ cplx smem[];
+  extern __shared__ __align__(16) unsigned char smem_bytes[];
+  cplx* smem = reinterpret_cast<cplx*>(smem_bytes);
   const int tid = threadIdx.x;
   const int col = tid / T, tj = tid % T;
   LineIO io;

@@ -16,9 +16,11 @@ namespace hpnfft {
 
 // coordinate t of point j: x is [M][d] with the d given dimensions last; the 3 - d leading
 // (trivial) dimensions of a d < 3 plan read 0
-__device__ __forceinline__ double coord(const double* __restrict__ x, int64_t j, int d, int t) {
+// (x is float for the FP32 plans: the conversion to double is exact)
+template <typename T>
+__device__ __forceinline__ double coord(const T* __restrict__ x, int64_t j, int d, int t) {
   const int lead = 3 - d;
-  return t < lead ? 0.0 : x[(int64_t)d * j + (t - lead)];
+  return t < lead ? 0.0 : (double)x[(int64_t)d * j + (t - lead)];
 }
 
 __global__ void k_range_init(int* err) {
@@ -27,7 +29,8 @@ __global__ void k_range_init(int* err) {
   else err[t] = (t & 1) ? 0x7fffffff : -1;                // slot minima / maxima
 }
 
-__global__ void k_keys(const double* __restrict__ x, int d, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
+template <typename T>
+__global__ void k_keys(const T* __restrict__ x, int d, int64_t M, int64_t n0, int64_t n1, int64_t n2, int s2, int lc,
                        uint32_t k_lo, uint32_t k_hi, uint32_t* __restrict__ count, uint32_t* __restrict__ key,
                        uint32_t* __restrict__ rank, int* __restrict__ err) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -178,7 +181,8 @@ __global__ void k_scatter(int64_t M, const uint32_t* __restrict__ key, const uin
   perm[pos] = (uint32_t)j;
 }
 
-__global__ void k_gather_x(const double* __restrict__ x, int d, int64_t M, const uint32_t* __restrict__ perm,
+template <typename T>
+__global__ void k_gather_x(const T* __restrict__ x, int d, int64_t M, const uint32_t* __restrict__ perm,
                            double* __restrict__ xs) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= M) return;
@@ -208,7 +212,8 @@ void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi) {
   }
 }
 
-int sort_points(Plan* p, const double* x) {
+template <typename T>
+static int sort_points_t(Plan* p, const T* x) {
   const int64_t M = p->M;
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
@@ -243,5 +248,8 @@ int sort_points(Plan* p, const double* x) {
   stage_end(p, 2);
   return HPNFFT_OK;
 }
+
+int sort_points(Plan* p, const double* x) { return sort_points_t(p, x); }
+int sort_points_f32(Plan* p, const float* x) { return sort_points_t(p, x); }
 
 }  // namespace hpnfft

@@ -1542,6 +1542,7 @@ size_t record_bytes(int m) {
 
 bool sweep_supported(const Plan* p) {
   if (p->m > kMaxSweepM) return false;   // m = 9..15: the generic atomic spread / warp gather
+  if (p->precision != HPNFFT_PRECISION_F64) return false;   // FP32 plans: spread_f32.cu
   const int W = 2 * p->m;
   const int P1 = 16, P2 = 32;   // largest extent of any patch variant
   if (p->n[2] < P2 || p->n[1] < P1) return false;

@@ -345,6 +345,56 @@ def test_multi_gpu_modes_match_single_gpu():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+# -------------------------------------------------------- FP32 plans (NEXT #4 remainder) --
+# Bar: E2 vs the float64 CPU NFFT (O2, same m) <= 1e-5 -- float rounding of the
+# taps (~6e-8 each), of the per-node sums, and of the 3 pruned FFT passes (~eps log2 n^3 < 2e-6)
+# with a 5x margin; vs the direct NDFT (O1) the method's own error at m adds (KB m = 3: ~1e-5).
+def gpu_adjoint_f32(x, f, N, m=3, window="kb"):
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    plan = hp.Plan(N, x.shape[0], m=m, window=window, device=dev, precision="f32")
+    plan.set_points(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev))
+    out = plan.adjoint(torch.from_numpy(np.ascontiguousarray(f, dtype=np.complex64)).to(dev)).cpu().numpy()
+    plan.close()
+    return out
+
+
+@pytest.mark.parametrize("N,M,m,dist", [((16, 16, 16), 1000, 3, "uniform"), ((16, 16, 16), 1000, 6, "uniform"),
+                                        ((32, 16, 64), 4099, 2, "uniform"), ((32, 16, 64), 4099, 8, "uniform"),
+                                        ((64, 64, 64), 200000, 3, "clustered"), ((128, 64, 32), 100003, 4, "uniform"),
+                                        ((64, 32), 5000, 3, "uniform"), ((512,), 3000, 3, "uniform"),
+                                        ((8, 4, 16), 300, 3, "uniform")])
+def test_f32_adjoint_vs_oracle(N, M, m, dist):
+    d = len(N)
+    if dist == "clustered":
+        x = inputs.clustered_points(M, s=0.05, seed=80)
+    else:
+        x = inputs.uniform_points(M, seed=80, d=d)
+    x = x.astype(np.float32).astype(np.float64)   # the float coordinates are the problem's points
+    f = inputs.uniform_values(M, seed=80).astype(np.complex64).astype(np.complex128)
+    g = gpu_adjoint_f32(x, f, N, m=m)
+    assert g.dtype == np.complex64 and g.shape == N
+    assert oracle.rel_l2_error(g, oracle.nfft_adjoint(x, f, N, m=m)) <= 1e-5
+    if M <= 5000 and m >= 3:
+        e_method = oracle.rel_l2_error(oracle.nfft_adjoint(x, f, N, m=m), oracle.ndft_direct(x, f, N))
+        assert oracle.rel_l2_error(g, oracle.ndft_direct(x, f, N)) <= e_method + 1e-5
+
+
+def test_f32_empty_and_precision_errors():
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    p = hp.Plan((16, 16, 16), 0, m=3, device=dev, precision="f32")
+    p.set_points(torch.zeros((0, 3), dtype=torch.float32, device=dev))
+    assert torch.all(p.adjoint(torch.zeros(0, dtype=torch.complex64, device=dev)) == 0)
+    lib = hp.load_library()
+    import ctypes
+    z = torch.zeros((4, 3), dtype=torch.float64, device=dev)
+    assert lib.hpnfft_set_points(p._h, ctypes.c_void_p(z.data_ptr())) == -1   # float64 call on an FP32 plan
+    p.close()
+    with pytest.raises(NotImplementedError):
+        hp.Plan((16, 16, 16), 10, m=9, device=dev, precision="f32")
+
+
 # ---------------------------------------------- race / protocol checks without a sanitizer --
 def _run_py(code, env_extra=None, timeout=900):
     import subprocess
