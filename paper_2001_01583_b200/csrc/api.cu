@@ -139,6 +139,7 @@ static void free_plan(Plan* p) {
   cudaFree(p->perm);
   cudaFree(p->xs);
   cudaFree(p->scan_tmp);
+  cudaFree(p->sort2_buf);
   cudaFree(p->rec);
   cudaFree(p->group_rows);
   cudaFree(p->tile_counter);

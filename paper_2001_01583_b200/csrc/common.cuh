@@ -95,6 +95,8 @@ struct Plan {
   uint32_t* perm = nullptr;       // [M] sorted position -> original index
   double* xs = nullptr;           // [M][3] sorted coordinates
   void* scan_tmp = nullptr;       // block sums for the scan
+  void* sort2_buf = nullptr;      // two-level sort workspace (lazy, large M): keys, indices, coordinates
+  int64_t sort2_hist_n = 0;       //   in chunk order + [chunks][blocks] counts + scan block sums
   int64_t scan_tmp_elems = 0;
   double* rec = nullptr;          // point records for the sweep spread [rec_group][22 + 4m]
   int64_t rec_group = 0;          // points per record group (== M unless memory-limited)

@@ -10,6 +10,8 @@
 // a sweep CTA fetches the records of its (chunk, row) with one bulk copy.
 // Counting sort: histogram with arrival ranks (atomicAdd) -> exclusive scan -> scatter.
 // The order inside a bin is the atomic arrival order (not deterministic; Q21).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace hpnfft {
@@ -27,6 +29,35 @@ __global__ void k_range_init(int* err) {
   const int t = threadIdx.x;
   if (t == 0) err[0] = 0;                                 // range-error flag
   else err[t] = (t & 1) ? 0x7fffffff : -1;                // slot minima / maxima
+}
+
+// bin key of point j (A1): cells c_t = floor(n_t x_t) mod n_t, chunk-major key; out-of-range
+// coordinates (or NaN) set *err = 1 and count as the origin; keys outside [k_lo, k_hi) (a
+// grid-slab rank's foreign planes) set *err = 2 and take k_lo
+template <typename T>
+__device__ __forceinline__ uint32_t point_key(const T* __restrict__ x, int64_t j, int d, int64_t n0, int64_t n1,
+                                              int64_t n2, int s2, int lc, uint32_t k_lo, uint32_t k_hi,
+                                              int* __restrict__ err, double* xo) {
+  double x0 = coord(x, j, d, 0), x1 = coord(x, j, d, 1), x2 = coord(x, j, d, 2);
+  if (!(fabs(x0) <= 0.5 && fabs(x1) <= 0.5 && fabs(x2) <= 0.5)) {
+    *err = 1;   // benign race: any writer sets 1
+    x0 = x1 = x2 = 0.0;
+  }
+  if (xo) {
+    xo[0] = x0;
+    xo[1] = x1;
+    xo[2] = x2;
+  }
+  int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x0)) & (n0 - 1);
+  int64_t c1 = (int64_t)floor(__dmul_rn((double)n1, x1)) & (n1 - 1);
+  int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
+  int64_t nb2 = n2 >> s2;
+  uint32_t k = (uint32_t)(((((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc) | (c0 & ((1 << lc) - 1)));
+  if (k < k_lo || k >= k_hi) {   // grid-slab plan: the point is outside this rank's planes
+    *err = 2;
+    k = k_lo;
+  }
+  return k;
 }
 
 template <typename T>
@@ -62,22 +93,169 @@ __global__ void k_keys(const T* __restrict__ x, int d, int64_t M, int64_t n0, in
     }
   }
   if (j >= M) return;
-  double x0 = coord(x, j, d, 0), x1 = coord(x, j, d, 1), x2 = coord(x, j, d, 2);
-  if (!(fabs(x0) <= 0.5 && fabs(x1) <= 0.5 && fabs(x2) <= 0.5)) {
-    *err = 1;   // benign race: any writer sets 1
-    x0 = x1 = x2 = 0.0;
-  }
-  int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, x0)) & (n0 - 1);
-  int64_t c1 = (int64_t)floor(__dmul_rn((double)n1, x1)) & (n1 - 1);
-  int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
-  int64_t nb2 = n2 >> s2;
-  uint32_t k = (uint32_t)(((((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc) | (c0 & ((1 << lc) - 1)));
-  if (k < k_lo || k >= k_hi) {   // grid-slab plan: the point is outside this rank's planes
-    *err = 2;
-    k = k_lo;
-  }
+  const uint32_t k = point_key(x, j, d, n0, n1, n2, s2, lc, k_lo, k_hi, err, nullptr);
   key[j] = k;
   rank[j] = atomicAdd(&count[k], 1u);
+}
+
+// ---- two-level sort for large M (HPNFFT_SORT2; default from 2^25 points) -------------------
+// Level 1 partitions the points by plane chunk (the key's top bits, C <= 1024 buckets): every
+// block owns one contiguous slice of the input, counts its chunks in shared memory (K1), a scan
+// of the chunk-major [C][blocks] counts gives every (chunk, block) a contiguous output run, and
+// the block re-reads its slice and moves (key, index, coordinates) into its runs (K2).  Level 2
+// is the counting sort of above on the chunk-ordered points: its count atomics, rank and output
+// writes then stay inside one chunk's slice of the bin table / output at a time (L2-resident)
+// instead of spreading random atomics over the whole table and random 24-byte reads over the
+// whole input (what made the single-level sort ~8 % of HBM at 1e9 points).
+constexpr int kSortBlocks = 1024;
+constexpr int kSortThreads = 256;
+constexpr int kMaxChunks = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kSortThreads) k_keys_coarse(const T* __restrict__ x, int d, int64_t M, int64_t n0,
+                                                              int64_t n1, int64_t n2, int s2, int lc, int fine_bits,
+                                                              int C, uint32_t k_lo, uint32_t k_hi,
+                                                              uint32_t* __restrict__ key, uint32_t* __restrict__ histT,
+                                                              int* __restrict__ err) {
+  __shared__ uint32_t hist[kMaxChunks];
+  __shared__ unsigned s_min, s_max;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) hist[c] = 0u;
+  if (threadIdx.x == 0) {
+    s_min = 0xffffffffu;
+    s_max = 0u;
+  }
+  __syncthreads();
+  const int64_t per = (M + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per, hi = min(M, lo + per);
+  unsigned bmin = 0xffffffffu, bmax = 0u;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const int64_t c0 = (int64_t)floor(__dmul_rn((double)n0, coord(x, j, d, 0))) & (n0 - 1);
+    const unsigned cx = (unsigned)((c0 + n0 / 2) & (n0 - 1));
+    bmin = min(bmin, cx);
+    bmax = max(bmax, cx);
+    const uint32_t k = point_key(x, j, d, n0, n1, n2, s2, lc, k_lo, k_hi, err, nullptr);
+    key[j] = k;
+    atomicAdd(&hist[k >> fine_bits], 1u);
+  }
+  atomicMin(&s_min, bmin);
+  atomicMax(&s_max, bmax);
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) histT[(size_t)c * gridDim.x + blockIdx.x] = hist[c];
+  if (threadIdx.x == 0 && s_min != 0xffffffffu) {   // occupied planes (see k_keys)
+    const int slot = (int)(blockIdx.x % kRangeSlots);
+    atomicMin(err + 1 + 2 * slot, (int)s_min);
+    atomicMax(err + 2 + 2 * slot, (int)s_max);
+  }
+}
+
+// K2: the block's slice in tiles of kTile points, each tile counting-sorted by chunk in shared
+// memory first, so that the runs of one chunk leave the block as contiguous (coalesced) writes
+constexpr int kTile = 1024;   // static shared memory < 48 KB
+
+template <typename T>
+__global__ void __launch_bounds__(kSortThreads) k_coarse_scatter(const T* __restrict__ x, int d, int64_t M,
+                                                                 const uint32_t* __restrict__ key, int fine_bits, int C,
+                                                                 const uint32_t* __restrict__ offT,
+                                                                 uint32_t* __restrict__ tkey, uint32_t* __restrict__ tidx,
+                                                                 double* __restrict__ tx) {
+  __shared__ uint32_t cursor[kMaxChunks];   // next global position of every chunk (this block)
+  __shared__ uint32_t lstart[kMaxChunks];   // tile: first local slot of every chunk
+  __shared__ uint32_t lfill[kMaxChunks];    // tile: slots used so far
+  __shared__ uint32_t skey[kTile], sidx[kTile];
+  __shared__ double sx[kTile * 3];
+  __shared__ uint32_t wsum[kSortThreads / 32];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) cursor[c] = offT[(size_t)c * gridDim.x + blockIdx.x];
+  const int64_t per = (M + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * per, hi = min(M, lo + per);
+  constexpr int PT = kTile / kSortThreads;   // points per thread per tile
+  for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
+    const int cnt = (int)min((int64_t)kTile, hi - t0);
+    for (int c = threadIdx.x; c < C; c += blockDim.x) lfill[c] = 0u;
+    __syncthreads();
+    uint32_t kk[PT], rk[PT];
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      const int i = threadIdx.x + q * kSortThreads;
+      kk[q] = i < cnt ? key[t0 + i] : 0xffffffffu;
+      rk[q] = i < cnt ? atomicAdd(&lfill[kk[q] >> fine_bits], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of the tile's chunk counts (C <= 1024, kSortThreads threads, <= 4 per thread)
+    {
+      constexpr int CPT = kMaxChunks / kSortThreads;
+      uint32_t v[CPT], sum = 0;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int c = threadIdx.x * CPT + q;
+        v[q] = c < C ? lfill[c] : 0u;
+        sum += v[q];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= o) incl += y;
+      }
+      if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      uint32_t wbase = 0;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) wbase += wsum[w];
+      uint32_t run = wbase + incl - sum;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int c = threadIdx.x * CPT + q;
+        if (c < C) lstart[c] = run;
+        run += v[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      const int i = threadIdx.x + q * kSortThreads;
+      if (i < cnt) {
+        const uint32_t slot = lstart[kk[q] >> fine_bits] + rk[q];
+        const int64_t j = t0 + i;
+        skey[slot] = kk[q];
+        sidx[slot] = (uint32_t)j;
+        sx[3 * slot] = coord(x, j, d, 0);
+        sx[3 * slot + 1] = coord(x, j, d, 1);
+        sx[3 * slot + 2] = coord(x, j, d, 2);
+      }
+    }
+    __syncthreads();
+    // slot s (chunk c) -> global cursor[c] + (s - lstart[c]): consecutive threads, consecutive addresses
+    for (int sl = threadIdx.x; sl < cnt; sl += blockDim.x) {
+      const uint32_t c = skey[sl] >> fine_bits;
+      const uint32_t pos = cursor[c] + (uint32_t)sl - lstart[c];
+      tkey[pos] = skey[sl];
+      tidx[pos] = sidx[sl];
+      tx[3 * (size_t)pos] = sx[3 * sl];
+      tx[3 * (size_t)pos + 1] = sx[3 * sl + 1];
+      tx[3 * (size_t)pos + 2] = sx[3 * sl + 2];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) cursor[c] += lfill[c];
+    __syncthreads();
+  }
+}
+
+__global__ void k_fine_count(const uint32_t* __restrict__ tkey, int64_t M, uint32_t* __restrict__ count,
+                             uint32_t* __restrict__ rank) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < M) rank[i] = atomicAdd(&count[tkey[i]], 1u);
+}
+
+__global__ void k_fine_scatter(const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ tidx,
+                               const double* __restrict__ tx, const uint32_t* __restrict__ rank,
+                               const uint32_t* __restrict__ start, int64_t M, uint32_t* __restrict__ perm,
+                               double* __restrict__ xs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const uint32_t pos = start[tkey[i]] + rank[i];
+  perm[pos] = tidx[i];
+  xs[3 * (size_t)pos] = tx[3 * (size_t)i];
+  xs[3 * (size_t)pos + 1] = tx[3 * (size_t)i + 1];
+  xs[3 * (size_t)pos + 2] = tx[3 * (size_t)i + 2];
 }
 
 // ---- device-wide exclusive scan of uint32 (three-phase, recursive over block sums) ----
@@ -212,6 +390,24 @@ void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi) {
   }
 }
 
+// two-level sort workspace (lazy): chunk-ordered keys, indices, coordinates, the [C][blocks]
+// counts and their scan's block sums
+static int sort2_workspace(Plan* p, int64_t hist_n) {
+  if (p->sort2_buf && p->sort2_hist_n >= hist_n) return HPNFFT_OK;
+  cudaFree(p->sort2_buf);
+  p->sort2_buf = nullptr;
+  const size_t M = (size_t)(p->M > 0 ? p->M : 1);
+  const size_t scan_n = (size_t)scan_tmp_need(hist_n);
+  const size_t bytes = M * (4 + 4 + 24) + sizeof(uint32_t) * ((size_t)hist_n + scan_n) + 256;
+  if (cudaMalloc(&p->sort2_buf, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    p->sort2_buf = nullptr;
+    return HPNFFT_E_NOMEM;
+  }
+  p->sort2_hist_n = hist_n;
+  return HPNFFT_OK;
+}
+
 template <typename T>
 static int sort_points_t(Plan* p, const T* x) {
   const int64_t M = p->M;
@@ -219,10 +415,56 @@ static int sort_points_t(Plan* p, const T* x) {
   while ((1 << (s2 + 1)) <= 8 && (1ll << (s2 + 1)) <= p->n[2]) ++s2;
   uint32_t k_lo, k_hi;
   key_range(p, k_lo, k_hi);
+  const int lc = p->chunk_log;
+  const int64_t C = p->n[0] >> lc;   // plane chunks = level-1 buckets
+  int fine_bits = lc;
+  while ((int64_t(1) << (fine_bits - lc)) < p->n[1] * (p->n[2] >> s2)) ++fine_bits;
+  const char* e2 = getenv("HPNFFT_SORT2");
+  bool two = M >= (int64_t(1) << 25);
+  if (e2) two = e2[0] == '1';
+  two = two && M > 0 && C <= kMaxChunks && (int64_t(1) << fine_bits) == p->n[1] * (p->n[2] >> s2) << lc;
+  const int64_t hist_n = C * kSortBlocks + 1;
+  if (two && sort2_workspace(p, hist_n) != HPNFFT_OK) two = false;   // out of memory: one level
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count + k_lo, 0, sizeof(uint32_t) * ((size_t)(k_hi - k_lo) + 1), p->stream),
                   "memset bins");
   k_range_init<<<1, 2 * kRangeSlots + 1, 0, p->stream>>>(p->err_flag);
   p->launches++;
+  if (two) {
+    uint32_t* tkey = reinterpret_cast<uint32_t*>(p->sort2_buf);
+    uint32_t* tidx = tkey + M;
+    double* tx = reinterpret_cast<double*>(tidx + M);   // 8 M bytes in: 8-byte aligned
+    uint32_t* histT = reinterpret_cast<uint32_t*>(tx + 3 * M);
+    uint32_t* scan_tmp = histT + hist_n;
+    stage_begin(p, 0);
+    HPNFFT_CUDA_TRY(p, cudaMemsetAsync(histT + hist_n - 1, 0, sizeof(uint32_t), p->stream), "memset hist tail");
+    k_keys_coarse<<<kSortBlocks, kSortThreads, 0, p->stream>>>(x, p->d, M, p->n[0], p->n[1], p->n[2], s2, lc,
+                                                                fine_bits, (int)C, k_lo, k_hi, p->key, histT,
+                                                                p->err_flag);
+    p->launches++;
+    int rc = check_launch(p, "keys (level 1)");
+    if (rc) return rc;
+    rc = scan_exclusive(p, histT, hist_n, scan_tmp);
+    if (rc) return rc;
+    k_coarse_scatter<<<kSortBlocks, kSortThreads, 0, p->stream>>>(x, p->d, M, p->key, fine_bits, (int)C, histT, tkey,
+                                                                   tidx, tx);
+    k_fine_count<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(tkey, M, p->bin_count, p->rank);
+    p->launches += 2;
+    rc = check_launch(p, "level-1 scatter / level-2 count");
+    if (rc) return rc;
+    stage_end(p, 0);
+    stage_begin(p, 1);
+    rc = scan_exclusive(p, p->bin_count + k_lo, (int64_t)(k_hi - k_lo) + 1, reinterpret_cast<uint32_t*>(p->scan_tmp));
+    if (rc) return rc;
+    stage_end(p, 1);
+    stage_begin(p, 2);
+    k_fine_scatter<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(tkey, tidx, tx, p->rank, p->bin_count, M, p->perm,
+                                                                      p->xs);
+    p->launches++;
+    rc = check_launch(p, "level-2 scatter");
+    if (rc) return rc;
+    stage_end(p, 2);
+    return HPNFFT_OK;
+  }
   stage_begin(p, 0);
   if (M > 0) {
     k_keys<<<(unsigned)((M + 255) / 256), 256, 0, p->stream>>>(x, p->d, M, p->n[0], p->n[1], p->n[2], s2, p->chunk_log,

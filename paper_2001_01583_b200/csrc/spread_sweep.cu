@@ -1020,10 +1020,14 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((S
       for (int nt = 0; nt < NT; ++nt)
         w1v[nt] = lds_f64(w12_addr<W>(ra, R::kW1, (unsigned)(d1 - (kWR - 1) + (REAL ? 2 * nt + br0 : nt)), zaddr));
 #if HPNFFT_SWEEP_NTSKIP
-      static_assert(!REAL, "n-tile skipping: complex sweep only");
-      const int lo = act ? max(0, (kWR - 1) - d1) : NT, hi = act ? min(NT - 1, W + kWR - 2 - d1) : -1;
-      ntlo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
-      nthi = __reduce_max_sync(0xffffffffu, hi + 1) - 1;
+      if constexpr (!REAL) {
+        const int lo = act ? max(0, (kWR - 1) - d1) : NT, hi = act ? min(NT - 1, W + kWR - 2 - d1) : -1;
+        ntlo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
+        nthi = __reduce_max_sync(0xffffffffu, hi + 1) - 1;
+      } else {
+        ntlo = 0;
+        nthi = NT - 1;
+      }
 #else
       ntlo = 0;
       nthi = NT - 1;

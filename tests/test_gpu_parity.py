@@ -444,6 +444,27 @@ def test_sweep_bitwise_reproducible_and_schedule_invariant(monkeypatch):
     assert oracle.rel_l2_error(ref.cpu().numpy(), oracle.nfft_adjoint(x, f, N)) <= 1e-12
 
 
+@pytest.mark.parametrize("dist", ["uniform", "clustered"])
+def test_two_level_sort(dist, monkeypatch):
+    """The two-level bin sort (plane-chunk partition, then the counting sort inside each chunk;
+    default from 2^25 points, forced here): the same bin table and sorted points as the one-level
+    sort, so the transform equals O2 -- single plan (adjoint + inverse), FP32 plan and a grid-slab
+    rank group (each rank sorts only its key range)."""
+    monkeypatch.setenv("HPNFFT_SORT2", "1")
+    N, M = (64, 32, 64), 150001
+    x = inputs.uniform_points(M, seed=90) if dist == "uniform" else inputs.clustered_points(M, s=0.05, seed=90)
+    f = inputs.uniform_values(M, seed=90)
+    ref = oracle.nfft_adjoint(x, f, N)
+    assert oracle.rel_l2_error(gpu_adjoint(x, f, N), ref) <= 1e-12
+    fh = _spectrum(N, 90)
+    assert oracle.rel_l2_error(gpu_inverse(x, fh, N), oracle.nfft_inverse(x, fh, N)) <= 1e-12
+    x32 = x.astype(np.float32).astype(np.float64)
+    g32 = gpu_adjoint_f32(x32, f, N, m=3)
+    assert oracle.rel_l2_error(g32, oracle.nfft_adjoint(x32, f, N, m=3)) <= 1e-5
+    full = _assemble(_group_adjoint(x, f, N, 4, "grid_slab"), "grid_slab")
+    assert oracle.rel_l2_error(full, ref) <= 1e-12
+
+
 # ------------------------------------------------------------ d = 1, 2 plans (NEXT #4) --
 @pytest.mark.parametrize("N,M,m,window", [((256,), 1000, 6, "kb"), ((512,), 3001, 6, "kb"), ((64,), 700, 11, "kb"),
                                           ((64, 32), 5003, 6, "kb"), ((512, 16), 4001, 4, "gaussian"),
