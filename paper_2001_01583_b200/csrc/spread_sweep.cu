@@ -34,9 +34,29 @@ namespace hpnfft {
 
 namespace {
 
-constexpr int kWR = 4;          // warp sub-patch of the DMMA consumer: 4 rows (l1) x 4 cols (l2)
+#ifndef HPNFFT_SWEEP_WR
+#define HPNFFT_SWEEP_WR 4
+#endif
+constexpr int kWR = HPNFFT_SWEEP_WR;   // warp sub-patch of the DMMA consumer: kWR rows (l1) x 4 cols (l2)
 constexpr int kWC = 4;
-constexpr int kBinW = 8;        // c2 bin width of the sort keys (sort.cu)
+constexpr int kBinW = 8;
+// CTA patch shapes instantiated by the dispatch (run_sweep): the default (D) and the measurement
+// variants; kWR = 2 (measurement builds) has 2x the sub-patches per patch, so its patches shrink
+#if HPNFFT_SWEEP_WR == 4
+#define HPNFFT_P_D1 8
+#define HPNFFT_P_D2 32
+#define HPNFFT_P_A1 12
+#define HPNFFT_P_A2 32
+#define HPNFFT_P_B1 16
+#define HPNFFT_P_B2 16
+#else
+#define HPNFFT_P_D1 8
+#define HPNFFT_P_D2 16
+#define HPNFFT_P_A1 4
+#define HPNFFT_P_A2 32
+#define HPNFFT_P_B1 8
+#define HPNFFT_P_B2 8
+#endif        // c2 bin width of the sort keys (sort.cu)
 #ifndef HPNFFT_SWEEP_NS
 #define HPNFFT_SWEEP_NS 3
 #endif
@@ -1448,9 +1468,9 @@ int run_sweep(Plan* p, const double* f) {
       const int v = real ? 0 : sweep_variant();
       const int rco = v == 4 ? prepare_tile_order<12, 16, M_>(p, g0, g1)
                     : v == 3 ? prepare_tile_order<8, 16, M_>(p, g0, g1)
-                    : v == 1 ? prepare_tile_order<12, 32, M_>(p, g0, g1)
-                    : v == 2 ? prepare_tile_order<16, 16, M_>(p, g0, g1)
-                             : prepare_tile_order<8, 32, M_>(p, g0, g1);
+                    : v == 1 ? prepare_tile_order<HPNFFT_P_A1, HPNFFT_P_A2, M_>(p, g0, g1)
+                    : v == 2 ? prepare_tile_order<HPNFFT_P_B1, HPNFFT_P_B2, M_>(p, g0, g1)
+                             : prepare_tile_order<HPNFFT_P_D1, HPNFFT_P_D2, M_>(p, g0, g1);
       if (rco) return rco;
     }
     if (cnt > 0) {
@@ -1474,14 +1494,14 @@ int run_sweep(Plan* p, const double* f) {
     }
     int rc;
     if (real) {
-      rc = launch_sweep_group<8, 32, M_, false, true>(p, g0, g1, p->group_rows, multi);
+      rc = launch_sweep_group<HPNFFT_P_D1, HPNFFT_P_D2, M_, false, true>(p, g0, g1, p->group_rows, multi);
     } else {
       const int var = sweep_variant();
       rc = var == 4 ? launch_sweep_group<12, 16, M_>(p, g0, g1, p->group_rows, multi)
          : var == 3 ? launch_sweep_group<8, 16, M_>(p, g0, g1, p->group_rows, multi)
-         : var == 1 ? launch_sweep_group<12, 32, M_>(p, g0, g1, p->group_rows, multi)
-         : var == 2 ? launch_sweep_group<16, 16, M_>(p, g0, g1, p->group_rows, multi)
-                    : launch_sweep_group<8, 32, M_>(p, g0, g1, p->group_rows, multi);
+         : var == 1 ? launch_sweep_group<HPNFFT_P_A1, HPNFFT_P_A2, M_>(p, g0, g1, p->group_rows, multi)
+         : var == 2 ? launch_sweep_group<HPNFFT_P_B1, HPNFFT_P_B2, M_>(p, g0, g1, p->group_rows, multi)
+                    : launch_sweep_group<HPNFFT_P_D1, HPNFFT_P_D2, M_>(p, g0, g1, p->group_rows, multi);
     }
     if (rc) return rc;
     g0 = g1;
@@ -1501,7 +1521,7 @@ int run_interp_sweep(Plan* p, double* fout) {
     const uint32_t g1 = (M - g0) < G ? M : g0 + G;
     const uint32_t cnt = g1 - g0;
     {
-      const int rco = prepare_tile_order<8, 32, M_>(p, g0, g1);
+      const int rco = prepare_tile_order<HPNFFT_P_D1, HPNFFT_P_D2, M_>(p, g0, g1);
       if (rco) return rco;
     }
     if (cnt > 0) {
@@ -1522,7 +1542,7 @@ int run_interp_sweep(Plan* p, double* fout) {
       k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
       p->launches++;
     }
-    const int rc = launch_sweep_group<8, 32, M_, true>(p, g0, g1, p->group_rows, multi, fout);
+    const int rc = launch_sweep_group<HPNFFT_P_D1, HPNFFT_P_D2, M_, true>(p, g0, g1, p->group_rows, multi, fout);
     if (rc) return rc;
     g0 = g1;
   } while (g0 < M);
