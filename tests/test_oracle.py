@@ -195,6 +195,27 @@ def test_O3_sinc_power_fourier_pair_quadrature(m):
         assert abs(val - ref) <= 2e-7 * ref + 1e-12
 
 
+@pytest.mark.parametrize("m", [2, 4, 6])
+def test_O3_sinc_power_taps_poisson_sum(m):
+    """Value pin of the sinc-power window's TAPS (the C oracle's oracle_taps): the transform of
+    sinc^{2m}(pi beta u) is supported in |xi| <= m beta = (2 sigma - 1)/(2 sigma) < 1, so by Poisson
+    summation sum_{l in Z} Phi(u - l) = Phi_hat(0) = M_2m(0)/beta exactly, for every u.  The 2m taps
+    are the terms with |u - l| < m; the rest (the truncated tail) is summed here with numpy's sinc
+    over 2e5 periods.  A wrong exponent, beta, tap offset or truncation breaks the identity."""
+    sigma = 2.0
+    beta = windows.sinc_beta(sigma, m)
+    ref = windows.bspline(np.array([0.0]), 2 * m)[0] / beta
+    n = 64
+    ls = np.arange(-200000, 200001, dtype=np.float64)
+    for x in np.random.default_rng(m).uniform(-0.5, 0.5, 5):
+        w, _ = oracle.taps_1d(n, m, sigma, windows.SINC_POWER, float(x))
+        d = n * float(x) - ls
+        far = np.abs(d) >= m
+        tail = np.sum(np.sinc(beta * d[far]) ** (2 * m))
+        assert abs(w.sum() + tail - ref) <= 1e-13 * ref, (m, x, w.sum() + tail, ref)
+    assert windows.phi_hat(0.0, m, sigma, windows.SINC_POWER) == pytest.approx(ref, rel=1e-14)
+
+
 def test_O2_windows_accuracy_fig12_shape():
     """Fig. 12's shape (values unpinned): on the §4 setup (M = 4096, N = 16^3,
     sigma = 2) E2 of the CPU NFFT against the direct NDFT falls with m for all four windows, and
