@@ -520,9 +520,11 @@ def run_f32(args):
     dom = "spread" if stages.get("spread", 0.0) >= fft_ms else "fft"
     if dom == "spread":
         ach = sp_bytes / (stages["spread"] * 1e-3) / 1e9
-        roof = {"kernel": "k_spread_box_f32 (+ grid zero fill)", "bound": "hbm", "achieved": ach, "peak": hbm,
+        roof = {"kernel": "k_spread_red_f32 (+ grid zero fill)", "bound": "hbm", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                "algorithmic": "36 B/point (float64 sorted x, perm, complex64 f) + 16 B/cell (zero + write)"}
+                "algorithmic": "36 B/point (float64 sorted x, perm, complex64 f) + 16 B/cell (zero + write)",
+                "limiter": f"L2 vector float2 reductions, (2m)^3 = {(2 * m) ** 3} per point: "
+                           f"{M * (2 * m) ** 3 / (stages['spread'] * 1e-3):.3g} reductions/s (DESIGN.md §9e)"}
     else:
         ach = fft_b / (fft_ms * 1e-3) / 1e9
         roof = {"kernel": "k_fft_pass<complex64> z, y, x", "bound": "hbm", "achieved": ach, "peak": hbm,
