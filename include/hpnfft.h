@@ -247,11 +247,16 @@ int hpnfft_ewald_reciprocal(hpnfft_plan_t p, const double* q, double L, double a
  *       c0x in [r n0/P, (r+1) n0/P), c0x = (floor(n0 x0) + n0/2) mod n0 (the equal-size x-slab
  *       [-1/2 + r/P, -1/2 + (r+1)/P)); all its points must lie there (else
  *       set_points returns HPNFFT_E_RANGE).  The rank spreads into its planes plus the m - 1
- *       planes below and m above, sends those halos to its neighbours (ncclSend/Recv) and adds
- *       theirs, runs the z and y FFT passes on its own planes only, exchanges blocks all-to-all
- *       (grouped ncclSend/Recv) and runs the x pass on its k1 slab: fhat[N0][r N1/P .. (r+1)
+ *       planes below and m above, adds the neighbours' halo planes to its own (pulled from their
+ *       grids over NVLink peer memory; ncclSend/Recv when peer memory is unavailable), runs the z
+ *       and y FFT passes on its own planes only, exchanges blocks all-to-all (the y pass stores
+ *       straight into the destination ranks' grids; grouped ncclSend/Recv otherwise) and runs the
+ *       x pass on its k1 slab: fhat[N0][r N1/P .. (r+1)
  *       N1/P)[N2] (row-major [N0][N1/P][N2]).  Requires P a power of two, N1 % P == 0 and
- *       n0 / P >= 2m.
+ *       n0 / P >= 2m.  Over NVLink peer memory (CUDA IPC, chosen collectively: all ranks agree)
+ *       the phases are ordered by cross-GPU flag barriers with a 5 s timeout; after a timeout the
+ *       rank touches no peer memory any more, its fhat block is undefined, and its next
+ *       hpnfft_set_points returns HPNFFT_E_NCCL (the plan is then failed).
  */
 enum {
   HPNFFT_DIST_ALLREDUCE = 0,
