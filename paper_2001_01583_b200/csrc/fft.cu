@@ -104,6 +104,7 @@ struct EnergyArgs {
 __device__ __forceinline__ double half_mult(int k0, int k1, int k2, const EnergyArgs& ea) {
   const bool in0 = k0 >= -ea.N0o / 2 && k0 < ea.N0o / 2, in1 = k1 >= -ea.N1o / 2 && k1 < ea.N1o / 2;
   const bool mi0 = -k0 >= -ea.N0o / 2 && -k0 < ea.N0o / 2, mi1 = -k1 >= -ea.N1o / 2 && -k1 < ea.N1o / 2;
+  if (k2 > ea.N2o / 2) return 0.0;   // pad columns of the half lines
   return (double)((k2 < ea.N2o / 2 && in0 && in1) ? 1 : 0) + (double)((k2 >= 1 && mi0 && mi1) ? 1 : 0);
 }
 
@@ -754,7 +755,7 @@ int fft_and_deconvolve(Plan* p, double* fhat) {
 // complex): half the bytes of the complex pass, the other half follows from X(-k) = conj X(k).
 template <int LOGH, int TC>
 __global__ void __launch_bounds__(TC*((1 << LOGH) >= 8 ? (1 << LOGH) / 8 : 1))
-k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int N2,
+k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, int N2, int N2s,
             const double* __restrict__ inv_c, const cplx* __restrict__ tw_h, const cplx* __restrict__ tw_n,
             int64_t o_start, int64_t o_total) {
   constexpr int h = 1 << LOGH;
@@ -775,8 +776,11 @@ k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, 
   io.peers = nullptr;
   run_stages_to_smem<LOGH, TC, true, 0>(smem, col, tj, tw_h, io);
   if (!io.valid) return;
+  // output lines of N2s >= N2/2 + 1 entries (padded to 128-byte rows: the strided passes then read
+  // aligned row segments); the pad entries are zero
   const int N2h = N2 / 2 + 1;
-  cplx* gout = out + oc * (int64_t)N2h;
+  cplx* gout = out + oc * (int64_t)N2s;
+  for (int k = N2h + tj; k < N2s; k += T) gout[k] = {0.0, 0.0};
   for (int k = tj; k < N2h; k += T) {
     const cplx zk = smem[slot<LOGH, TC, true>(k & (h - 1), col)];
     const cplx zr = smem[slot<LOGH, TC, true>((h - k) & (h - 1), col)];
@@ -789,7 +793,7 @@ k_fft_r2c_z(const cplx* __restrict__ in, cplx* __restrict__ out, int64_t outer, 
 }
 
 template <int LOGH>
-static int launch_r2c_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int N2, const double* inv_c,
+static int launch_r2c_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int N2, int N2s, const double* inv_c,
                         const cplx* tw_h, const cplx* tw_n, int64_t o_start, int64_t o_total) {
   constexpr int TC = tile_cols_contig<LOGH>();
   constexpr int h = 1 << LOGH;
@@ -797,13 +801,13 @@ static int launch_r2c_n(Plan* p, const cplx* in, cplx* out, int64_t outer, int N
   const size_t smem = tile_elems<LOGH, TC, true>() * sizeof(cplx);
   auto kern = k_fft_r2c_z<LOGH, TC>;
   HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(kern), smem), "r2c smem attr");
-  kern<<<(unsigned)((outer + TC - 1) / TC), TC * (h >= 8 ? h / 8 : 1), smem, p->stream>>>(in, out, outer, N2, inv_c,
-                                                                                       tw_h, tw_n, o_start, o_total);
+  kern<<<(unsigned)((outer + TC - 1) / TC), TC * (h >= 8 ? h / 8 : 1), smem, p->stream>>>(in, out, outer, N2, N2s,
+                                                                                       inv_c, tw_h, tw_n, o_start, o_total);
   p->launches++;
   return check_launch(p, "fft r2c z pass");
 }
 
-static int launch_r2c(Plan* p, int logh, const double* in, double* out, int64_t outer, int64_t o_start,
+static int launch_r2c(Plan* p, int logh, const double* in, double* out, int64_t outer, int N2s, int64_t o_start,
                       int64_t o_total) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
   cplx* co = reinterpret_cast<cplx*>(out);
@@ -812,15 +816,15 @@ static int launch_r2c(Plan* p, int logh, const double* in, double* out, int64_t 
   const int N2 = (int)p->N[2];
   const double* ic = p->inv_c[2];
   switch (logh) {
-    case 1: return launch_r2c_n<1>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 2: return launch_r2c_n<2>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 3: return launch_r2c_n<3>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 4: return launch_r2c_n<4>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 5: return launch_r2c_n<5>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 6: return launch_r2c_n<6>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 7: return launch_r2c_n<7>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 8: return launch_r2c_n<8>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
-    case 9: return launch_r2c_n<9>(p, ci, co, outer, N2, ic, th, tn, o_start, o_total);
+    case 1: return launch_r2c_n<1>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 2: return launch_r2c_n<2>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 3: return launch_r2c_n<3>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 4: return launch_r2c_n<4>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 5: return launch_r2c_n<5>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 6: return launch_r2c_n<6>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 7: return launch_r2c_n<7>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 8: return launch_r2c_n<8>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
+    case 9: return launch_r2c_n<9>(p, ci, co, outer, N2, N2s, ic, th, tn, o_start, o_total);
     default:
       set_error("R2C length not supported");
       return HPNFFT_E_UNSUPPORTED;
@@ -887,10 +891,14 @@ static int64_t energy_x_pass(Plan* p, const double* in, int64_t inner, int N0, c
 // frequency with its multiplicity in I_N (half_mult).  Exact: the same sum as the complex path.
 int energy_r2c(Plan* p) {
   const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
-  const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2], N2h = N2 / 2 + 1;
+  const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
+  // half lines k2 in [0, N2/2] stored with a stride padded to 8 (128-byte rows); the pad columns
+  // are zero (R2C pass) and count 0 times in the energy (half_mult)
+  int64_t N2h = ((N2 / 2 + 1) + 7) / 8 * 8;
+  if (N2h > N2) N2h = N2 / 2 + 1;   // small N2: bufA holds n0 n1 N2 entries
   const int64_t plo = p->plane_lo, plen = p->plane_len;
   stage_begin(p, 4);
-  int rc = launch_r2c(p, p->logn[2] - 1, p->grid, p->bufA, plen * n1, plo * n1, n0 * n1);
+  int rc = launch_r2c(p, p->logn[2] - 1, p->grid, p->bufA, plen * n1, (int)N2h, plo * n1, n0 * n1);
   stage_end(p, 4);
   if (rc) return rc;
   stage_begin(p, 5);

@@ -465,6 +465,60 @@ def test_two_level_sort(dist, monkeypatch):
     assert oracle.rel_l2_error(full, ref) <= 1e-12
 
 
+def test_randomized_configurations_vs_cpu_nfft():
+    """Seeded random plans across the supported space: d = 1..3, N_t in {2 .. 256} (n_t <= 512),
+    m = 1..15, all four windows, uniform / clustered / boundary points, M from 0 to 3e4, sweep /
+    atomic / auto spread, adjoint and inverse: every one equals O2 / O2i (bar of reading Q25)."""
+    from oracle import windows
+
+    hp = _hp()
+    dev = torch.device("cuda", 0)
+    wins = {"kb": windows.KAISER_BESSEL, "gaussian": windows.GAUSSIAN, "b_spline": windows.B_SPLINE,
+            "sinc_power": windows.SINC_POWER}
+    rng = np.random.default_rng(2024)
+    kernels = set()
+    for case in range(24):
+        if case % 2 == 0:   # 3-D grids the DMMA sweep serves (n_t >= 32, m <= 8)
+            d = 3
+            N = tuple(int(2 ** rng.integers(4, 8)) for _ in range(d))
+            m = int(rng.integers(1, 9))
+        else:
+            d = int(rng.integers(1, 4))
+            N = tuple(int(2 ** rng.integers(1, 9)) for _ in range(d))
+            m = int(rng.integers(1, 16))
+        while np.prod([2 * v for v in N]) > 2 ** 22:   # keep the CPU oracle at seconds
+            i = int(np.argmax(N))
+            N = N[:i] + (N[i] // 2,) + N[i + 1:]
+        win = list(wins)[case % 4]
+        M = int(rng.choice([513, 4099, 30011, 100003])) if case % 2 == 0 else int(rng.choice([0, 1, 7, 513, 4099, 30011]))
+        method = ["auto", "atomic", "sweep"][case % 3]
+        x = inputs.clustered_points(M, s=0.03, seed=case, d=d) if case % 2 else inputs.uniform_points(M, seed=case, d=d)
+        if M > 2:
+            x[0, 0], x[1, -1] = 0.5, -0.5
+        f = inputs.uniform_values(M, seed=case)
+        plan = hp.Plan(N, M, m=m, window=win, device=dev)
+        if method == "sweep":
+            info = plan.info()
+            if info["spread_kernel"] != "sweep":
+                method = "auto"   # the sweep does not serve this grid / m / d
+        plan.set_spread_method(method)
+        kernels.add(plan.info()["spread_kernel"])
+        plan.set_points(torch.from_numpy(np.ascontiguousarray(x)).to(dev))
+        g = plan.adjoint(torch.from_numpy(f).to(dev)).cpu().numpy()
+        fh = _spectrum(N, case)
+        fl = plan.inverse(torch.from_numpy(fh).to(dev)).cpu().numpy()
+        plan.close()
+        if M == 0:
+            assert np.all(g == 0) and fl.size == 0
+            continue
+        o2 = oracle.nfft_adjoint(x, f, N, m=m, window=wins[win])
+        floor = oracle.rel_l2_error(oracle.nfft_adjoint(x[::-1], f[::-1], N, m=m, window=wins[win]), o2)
+        assert oracle.rel_l2_error(g, o2) <= max(1e-12, 4 * floor), (case, d, N, m, win, M, method)
+        o2i = oracle.nfft_inverse(x, fh, N, m=m, window=wins[win])
+        assert oracle.rel_l2_error(fl, o2i) <= max(1e-12, 4 * floor), (case, d, N, m, win, M)
+    assert kernels == {"sweep", "atomic"}
+
+
 # ------------------------------------------------------------ d = 1, 2 plans (NEXT #4) --
 @pytest.mark.parametrize("N,M,m,window", [((256,), 1000, 6, "kb"), ((512,), 3001, 6, "kb"), ((64,), 700, 11, "kb"),
                                           ((64, 32), 5003, 6, "kb"), ((512, 16), 4001, 4, "gaussian"),
