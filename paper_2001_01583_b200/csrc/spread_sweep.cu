@@ -172,6 +172,13 @@ struct SweepParams {
 // of a tap share the tap's coefficients (a broadcast shared-memory load per step); the records
 // are staged in shared memory and written to HBM with coalesced 16-byte stores.
 constexpr int kRecPts = 128;
+#ifndef HPNFFT_REC_CHUNKS
+#define HPNFFT_REC_CHUNKS 4   // runs of kRecPts points per CTA (measured: 1 / 4 -> 1.12 / 1.02 ms at config 4)
+#endif
+#ifndef HPNFFT_REC_UNROLL
+#define HPNFFT_REC_UNROLL 2   // taps evaluated together (independent Horner chains: 3 per tap)
+#endif
+constexpr int kRecUnroll = HPNFFT_REC_UNROLL;
 
 template <int M_>
 __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restrict__ xs, const uint32_t* __restrict__ perm,
@@ -185,7 +192,9 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
   __shared__ double poly[W * PD];
   extern __shared__ __align__(16) double stage[];   // [kRecPts][RD]
   for (int e = threadIdx.x; e < W * PD; e += blockDim.x) poly[e] = poly_g[e];
-  const uint32_t kb = blockIdx.x * kRecPts;          // first point of this CTA (group-relative)
+  // a CTA builds HPNFFT_REC_CHUNKS consecutive runs of kRecPts points (the table load amortised)
+  for (uint32_t kb = blockIdx.x * kRecPts * HPNFFT_REC_CHUNKS; kb < count && kb < (blockIdx.x + 1) * kRecPts * HPNFFT_REC_CHUNKS;
+       kb += kRecPts) {
   const uint32_t k = kb + threadIdx.x;
   double2 fv = make_double2(0.0, 0.0);
   double x0 = 0.0, x1 = 0.0, x2 = 0.0;
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
   double* out = stage + threadIdx.x * RD;
   const CellT a0 = cell_of(x0, n0), a1 = cell_of(x1, n1), a2 = cell_of(x2, n2);
   const double s0 = fma(2.0, a0.t, -1.0), s1 = fma(2.0, a1.t, -1.0), s2 = fma(2.0, a2.t, -1.0);
-#pragma unroll 2
+#pragma unroll kRecUnroll
   for (int i = 0; i < W; ++i) {
     const double* cf = poly + i * PD;
     double v0 = cf[PD - 1], v1 = v0, v2 = v0;
@@ -236,6 +245,7 @@ __global__ void __launch_bounds__(kRecPts) k_point_records(const double* __restr
   const double2* sp = reinterpret_cast<const double2*>(stage);
   double2* gp = reinterpret_cast<double2*>(rec + (size_t)kb * RD);
   for (int c = threadIdx.x; c < nchunk; c += blockDim.x) gp[c] = sp[c];
+  }
 }
 
 // plane chunks spanned by sorted points [g0, g1): binary search of the bin table (multi-group).
@@ -1478,7 +1488,8 @@ int run_sweep(Plan* p, const double* f) {
       const size_t rsmem = sizeof(double) * kRecPts * Rec<2 * M_>::kDoubles;
       HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>), (int)rsmem),
                       "records smem attr");
-      k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
+      k_point_records<M_><<<(cnt + kRecPts * HPNFFT_REC_CHUNKS - 1) / (kRecPts * HPNFFT_REC_CHUNKS), kRecPts, rsmem,
+                            p->stream>>>(
           p->xs, p->perm, f, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
       p->launches++;
       int rc = check_launch(p, "point records");
@@ -1529,7 +1540,8 @@ int run_interp_sweep(Plan* p, double* fout) {
       HPNFFT_CUDA_TRY(p, set_max_smem(reinterpret_cast<const void*>(k_point_records<M_>),
                                               (int)rsmem),
                       "records smem attr");
-      k_point_records<M_><<<(cnt + kRecPts - 1) / kRecPts, kRecPts, rsmem, p->stream>>>(
+      k_point_records<M_><<<(cnt + kRecPts * HPNFFT_REC_CHUNKS - 1) / (kRecPts * HPNFFT_REC_CHUNKS), kRecPts, rsmem,
+                            p->stream>>>(
           p->xs, p->perm, nullptr, p->poly, p->rec, g0, cnt, p->n[0], p->n[1], p->n[2]);
       p->launches++;
       int rc = check_launch(p, "point records");
