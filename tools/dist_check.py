@@ -3,8 +3,10 @@
 Every rank builds the same seeded point set, keeps its x-slab (equal-size, equal-count, or the
 cell-aligned grid slab), runs the library's multi-GPU plan (hpnfft_plan_dist: NCCL inside
 libhpnfft.so) and the distributed result is gathered on rank 0, which
-compares with a single-GPU transform of all points (<= 1e-13) and with sampled direct NDFT
-values from the oracle (<= 1e-9).  Exit code 0 on success.
+compares with a single-GPU transform of all points (<= 1e-13), with the CPU NFFT oracle (O2) on
+the full fhat (<= 1e-12, Eq. 8) and with sampled direct NDFT values from the oracle (<= 1e-9).  The
+grid-slab mode runs over NVLink peer memory and (HPNFFT_DIST_P2P=0) over NCCL send/recv.  Exit
+code 0 on success.
 """
 import os
 import sys
@@ -34,14 +36,18 @@ def main():
     for dist_kind, part, mode in [("uniform", "equal_size", "allreduce"), ("clustered", "equal_count", "allreduce"),
                                   ("uniform", "equal_size", "reduce"), ("uniform", "equal_size", "reduce_scatter"),
                                   ("uniform", "grid", "grid_slab"), ("clustered", "grid", "grid_slab"),
-                                  ("clustered", "grid_count", "grid_slab")]:
+                                  ("clustered", "grid_count", "grid_slab"), ("clustered", "grid_nccl", "grid_slab")]:
+        if part == "grid_nccl":   # the NCCL send/recv version of option G
+            os.environ["HPNFFT_DIST_P2P"] = "0"
+        else:
+            os.environ.pop("HPNFFT_DIST_P2P", None)
         x = idev.uniform_points(M, device=dev) if dist_kind == "uniform" else idev.clustered_points(M, device=dev)
         f = idev.uniform_values(M, device=dev)
         edges = equal_count_edges(x, world) if part == "equal_count" else None
         gedges = None
         if part == "grid_count":   # equal-count cell-plane slabs (hpnfft_set_slabs), histogram summed over ranks
             gedges = grid_slab_edges(x[rank::world], world, 2 * N[0])
-        if part in ("grid", "grid_count"):
+        if part in ("grid", "grid_count", "grid_nccl"):
             mask = grid_slab_mask(x, rank, world, 2 * N[0], gedges)
         else:
             mask = slab_mask(x, rank, world, edges)
@@ -66,9 +72,10 @@ def main():
             sref = oracle.ndft_direct(xh, fhh, N, ks=ks)
             got = np.array([out[tuple(k + np.array(N) // 2)].item() for k in ks])
             e2 = oracle.rel_l2_error(got, sref)
-            print(f"[{dist_kind}/{part}/{mode}] world={world} local M={xl.shape[0]} "
-                  f"E2(dist vs 1-GPU)={e:.2e} E2(vs NDFT, sampled)={e2:.2e}", flush=True)
-            ok &= e <= 1e-13 and e2 <= 1e-9
+            eo2 = oracle.rel_l2_error(out.cpu().numpy(), oracle.nfft_adjoint(xh, fhh, N))
+            print(f"[{dist_kind}/{part}/{mode}] world={world} local M={xl.shape[0]} p2p={dp.plan.info()['exchange_path']} "
+                  f"E2(dist vs 1-GPU)={e:.2e} E2(vs CPU NFFT, full)={eo2:.2e} E2(vs NDFT, sampled)={e2:.2e}", flush=True)
+            ok &= e <= 1e-13 and eo2 <= 1e-12 and e2 <= 1e-9
             ref_plan.close()
         # inverse direction (Eq. 6, Alg. 4): every rank takes the full fhat and
         # interpolates its own points; compare with the single-GPU inverse on the same points
