@@ -205,3 +205,23 @@ def test_grid_slab_rank_follows_the_cell_planes():
     x0 = torch.tensor([-0.5, -0.25 - 1e-12, -0.25, 0.0, 0.2499999, 0.25, 0.49, 0.5], dtype=torch.float64)
     x = torch.stack([x0, torch.zeros_like(x0), torch.zeros_like(x0)], 1)
     assert grid_slab_rank(x, world, n0).tolist() == [0, 0, 1, 2, 2, 3, 3, 0]
+
+
+def test_grid_slab_edges_from_histogram_match():
+    """bench.py's chunked shard generation cuts the slabs on a histogram accumulated chunk by chunk
+    (dist.grid_slab_edges_hist); it must give the same edges as dist.grid_slab_edges on the points."""
+    import inputs
+    from paper_2001_01583_b200.dist import grid_slab_edges, grid_slab_edges_hist
+
+    x = torch.from_numpy(inputs.clustered_points(50000, s=0.05))
+    n0 = 128
+    c0 = torch.floor(x[:, 0] * float(n0)).to(torch.int64) % n0
+    hist = torch.zeros(n0, dtype=torch.int64)
+    for part in torch.split(c0, 7777):   # chunk by chunk, as bench.shard_inputs does
+        hist += torch.bincount(part, minlength=n0)
+    for world in (2, 4):
+        for w in (0.0, 8000.0):
+            a = grid_slab_edges(x, world, n0, m=6, reduce=False, plane_weight=w)
+            b = grid_slab_edges_hist(hist, world, n0, m=6, plane_weight=w)
+            assert a == b
+            assert len(a) == world + 1 and a[-1] - a[0] == n0
