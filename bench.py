@@ -284,6 +284,9 @@ def run_ours(args):
     ms_local = e0.elapsed_time(e1)
     stages = plan.stage_times()
     plan.enable_timing(False)
+    if os.environ.get("HPNFFT_BENCH_RANK_STAGES"):   # diagnostics: every rank's own stage times
+        print(json.dumps({"rank": rank, "M_local": M_local, "ms": ms_local / args.steps, "info": plan.info()["planes"],
+                          "stages": {k: round(v, 4) for k, v in stages.items()}}), file=sys.stderr, flush=True)
     ms = ms_local
     if ws > 1:
         t = torch.tensor([ms_local], dtype=torch.float64, device=dev)

@@ -1308,6 +1308,17 @@ __global__ void __launch_bounds__(1024) k_tile_order(const unsigned long long* _
   for (int i = threadIdx.x; i < ntiles; i += blockDim.x) order[i] = (int)(sk[i] & 0xffffffffull) - 1;
 }
 
+// Node planes per tile segment (HPNFFT_SWEEP_SEG, default 256; a multiple of the chunk).  Shorter
+// segments split a patch's planes over more tiles (each with its 2m - 1 halo planes again): more
+// total work, but a heavy patch (clustered points) no longer bounds the persistent grid's makespan.
+template <int CH>
+int sweep_max_seg() {
+  const char* e = getenv("HPNFFT_SWEEP_SEG");
+  int s = e ? atoi(e) : 256;
+  if (s < 4 * CH) s = 4 * CH;
+  return s / CH * CH;
+}
+
 // Tile order for the next sweep of group [g0, g1), computed on the plan's side stream so that
 // it overlaps the records kernel (it only needs the bin table of set_points).  HPNFFT_SWEEP_LPT=0
 // keeps index order.  Same plane range / segment geometry as launch_sweep_group.
@@ -1333,7 +1344,7 @@ int prepare_tile_order(Plan* p, uint32_t g0, uint32_t g1) {
   if (len_al > n0) len_al = n0;
   prm.plane_lo = (int)lo_al;
   prm.plane_len = (int)len_al;
-  prm.seg = (int)(len_al < 256 ? len_al : 256);
+  prm.seg = (int)(len_al < sweep_max_seg<CH>() ? len_al : sweep_max_seg<CH>());
   prm.nseg = (int)((len_al + prm.seg - 1) / prm.seg);
   const int64_t tiles = ((p->n[1] + P1 - 1) / P1) * (p->n[2] / P2) * prm.nseg;
   if (tiles <= 1 || tiles > kMaxOrderTiles) return HPNFFT_OK;
@@ -1413,7 +1424,7 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   if (len_al > n0) len_al = n0;
   prm.plane_lo = (int)lo_al;
   prm.plane_len = (int)len_al;
-  prm.seg = (int)(len_al < 256 ? len_al : 256);
+  prm.seg = (int)(len_al < sweep_max_seg<CH>() ? len_al : sweep_max_seg<CH>());
   prm.nseg = (int)((len_al + prm.seg - 1) / prm.seg);
   prm.cap = cap;
   prm.tile_counter = p->tile_counter;
