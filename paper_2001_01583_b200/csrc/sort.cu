@@ -259,8 +259,18 @@ __global__ void k_fine_scatter(const uint32_t* __restrict__ tkey, const uint32_t
 }
 
 // ---- device-wide exclusive scan of uint32 (three-phase, recursive over block sums) ----
+// HPNFFT_SCAN_VEC=1: 256-thread tiles, 32 contiguous elements per thread moved as 8 uint4 (one
+// 8-warp block scan per 8192 elements); 0: 1024 threads x 8 scalar elements (round 1).
+#ifndef HPNFFT_SCAN_VEC
+#define HPNFFT_SCAN_VEC 1
+#endif
+#if HPNFFT_SCAN_VEC
+constexpr int kScanThreads = 256;
+constexpr int kScanPerThread = 32;
+#else
 constexpr int kScanThreads = 1024;
 constexpr int kScanPerThread = 8;
+#endif
 constexpr int kScanTile = kScanThreads * kScanPerThread;
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
@@ -298,6 +308,43 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(uint32_t* __restric
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPerThread;
   uint32_t v[kScanPerThread];
   uint32_t s = 0;
+#if HPNFFT_SCAN_VEC
+  // a is 16-byte aligned at every tile boundary when the caller's base is (bin_count + k_lo is
+  // not in general): vector path only for full, aligned thread slices
+  const bool vec = base + kScanPerThread <= n && ((reinterpret_cast<uintptr_t>(a + base) & 15) == 0);
+  if (vec) {
+    const uint4* a4 = reinterpret_cast<const uint4*>(a + base);
+#pragma unroll
+    for (int q = 0; q < kScanPerThread / 4; ++q) {
+      const uint4 t = a4[q];
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanPerThread; ++q) v[q] = (base + q < n) ? a[base + q] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) s += v[q];
+  uint32_t off = block_exclusive_scan(s, &total);
+  if (vec) {
+    uint4* a4 = reinterpret_cast<uint4*>(a + base);
+#pragma unroll
+    for (int q = 0; q < kScanPerThread / 4; ++q) {
+      uint4 t;
+      t.x = off; off += v[4 * q];
+      t.y = off; off += v[4 * q + 1];
+      t.z = off; off += v[4 * q + 2];
+      t.w = off; off += v[4 * q + 3];
+      a4[q] = t;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanPerThread; ++q) {
+      if (base + q < n) a[base + q] = off;
+      off += v[q];
+    }
+  }
+#else
 #pragma unroll
   for (int q = 0; q < kScanPerThread; ++q) {
     v[q] = (base + q < n) ? a[base + q] : 0u;
@@ -309,19 +356,30 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(uint32_t* __restric
     if (base + q < n) a[base + q] = off;
     off += v[q];
   }
+#endif
   if (threadIdx.x == 0 && sums) sums[blockIdx.x] = total;
 }
 
-__global__ void k_scan_add(uint32_t* __restrict__ a, int64_t n, const uint32_t* __restrict__ sums) {
-  int64_t i = (int64_t)blockIdx.x * kScanTile + threadIdx.x;
-  uint32_t add = sums[blockIdx.x];
+__global__ void __launch_bounds__(kScanThreads) k_scan_add(uint32_t* __restrict__ a, int64_t n,
+                                                           const uint32_t* __restrict__ sums) {
+  const uint32_t add = sums[blockIdx.x];
+  const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
+#if HPNFFT_SCAN_VEC
+  const int64_t head = (int64_t)((16 - (reinterpret_cast<uintptr_t>(a + t0) & 15)) & 15) / 4;   // to alignment
+  const int64_t tile_n = n - t0 < kScanTile ? n - t0 : kScanTile;
+  if (head == 0 && tile_n == kScanTile) {
+    uint4* a4 = reinterpret_cast<uint4*>(a + t0);
 #pragma unroll
-  for (int q = 0; q < kScanPerThread; ++q) {
-    int64_t e = i + (int64_t)q * kScanThreads;
-    if (e < n) a[e] += add;
+    for (int q = 0; q < kScanPerThread / 4; ++q) {
+      uint4 t = a4[q * kScanThreads + threadIdx.x];
+      t.x += add; t.y += add; t.z += add; t.w += add;
+      a4[q * kScanThreads + threadIdx.x] = t;
+    }
+    return;
   }
+#endif
+  for (int64_t e = t0 + threadIdx.x; e < t0 + kScanTile && e < n; e += kScanThreads) a[e] += add;
 }
-
 static int64_t scan_tmp_need(int64_t n) {
   int64_t need = 0;
   while (n > kScanTile) {
