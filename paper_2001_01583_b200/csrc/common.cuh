@@ -63,6 +63,7 @@ struct Plan {
   bool energy = false;
   double e_a = 0.0;
   double* e_partial = nullptr;
+  double* e_w0 = nullptr;   // Eq. 12 x-dimension weights (inside the e_partial allocation)
   int64_t e_nparts = 0, e_cap = 0;
   double* fq = nullptr;   // [M] complex (q, 0) of hpnfft_ewald_reciprocal
   // real values (the ENUF charges, NEXT #2): spread onto a REAL grid [n0][n1][n2] (doubles) and

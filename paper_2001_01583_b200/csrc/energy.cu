@@ -94,7 +94,8 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
     return HPNFFT_E_UNSUPPORTED;
   }
   // partials: one per x-pass CTA (at most N1 N2 lines) + the charge CTAs
-  const int64_t need = p->N[1] * p->N[2] + kChargeBlocks;
+  // + the x pass's weight table (N0 + 2 entries)
+  const int64_t need = p->N[1] * p->N[2] + kChargeBlocks + p->N[0] + 2;
   if (p->e_cap < need) {
     cudaFree(p->e_partial);
     p->e_partial = nullptr;
@@ -115,6 +116,7 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
   }
   p->launches = 0;
   double* q2_partial = p->e_partial + p->N[1] * p->N[2];
+  p->e_w0 = q2_partial + kChargeBlocks;
   k_charges<<<kChargeBlocks, kThreads, 0, p->stream>>>(q, reinterpret_cast<double2*>(p->fq), p->M, q2_partial);
   p->launches++;
   int rc = check_launch(p, "charges");

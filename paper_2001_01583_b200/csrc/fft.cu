@@ -97,7 +97,18 @@ struct EnergyArgs {
   // represents: itself and its mirror -k (|S(-k)| = |S(k)| for real charges, Eq. 12)
   int real_half;
   int N0o, N1o, N2o;
+  // w0[k] = inv_c[k]^2 exp(-e_a (k - N/2)^2) over the x pass's kept outputs (k_energy_w0): the
+  // Gaussian of Eq. 12 factorises over the three dimensions, so each output needs one table
+  // value and the thread's exp(-e_a (n1^2 + n2^2)) instead of an exp of its own
+  const double* w0;
 };
+
+__global__ void k_energy_w0(double* __restrict__ w0, const double* __restrict__ inv_c, int N, double e_a) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const double b0 = (double)(k - N / 2);
+  w0[k] = inv_c[k] * inv_c[k] * exp(-e_a * b0 * b0);
+}
 
 // multiplicity of the half-spectrum frequency k (k2 >= 0) in Eq. 12's sum over I_N: k itself
 // (k2 < N2/2, k0, k1 in I) plus its mirror -k (k2 >= 1, -k0, -k1 in I)
@@ -133,6 +144,7 @@ struct LineIOT {
   double e_a;
   int64_t k1_base;
   int N1e, N2e;
+  double n12, g12;   // |(n1, n2)|^2 of the line and exp(-e_a n12)
   double esum;
   EnergyArgs ea;
 };
@@ -222,15 +234,14 @@ __device__ __forceinline__ void stockham_stage(C* buf, int col, int tj, const C*
         const bool lo = q < N / 2, hi = q >= n - N / 2;
         if (io.valid && (lo || hi)) {
           const int k = lo ? q + N / 2 : q - (n - N / 2);
-          const double sc = (double)io.inv_c[k];
-          const double re = (double)v[b][r].x * sc, im = (double)v[b][r].y * sc;
+          const double re = (double)v[b][r].x, im = (double)v[b][r].y;
           const int64_t k1 = io.k1_base + io.line_i / io.N2e;
           const int i0 = k - N / 2, i1 = (int)(k1 - io.N1e / 2);
           const int i2 = io.ea.real_half ? (int)(io.line_i % io.N2e) : (int)(io.line_i % io.N2e - io.N2e / 2);
-          const double a0 = (double)i0, a1 = (double)i1, a2 = (double)i2;
-          const double nn = a0 * a0 + a1 * a1 + a2 * a2;
+          const double a0 = (double)i0;
+          const double nn = a0 * a0 + io.n12;
           const double mult = io.ea.real_half ? half_mult(i0, i1, i2, io.ea) : 1.0;
-          if (nn > 0.0 && mult > 0.0) io.esum += mult * exp(-io.e_a * nn) / nn * (re * re + im * im);
+          if (nn > 0.0 && mult > 0.0) io.esum += mult * io.ea.w0[k] * io.g12 / nn * (re * re + im * im);
         }
       } else if (OUT_G && io.inv) {
         if (io.valid) io.gout[(int64_t)q * io.ostride] = {v[b][r].x, -v[b][r].y};
@@ -326,6 +337,13 @@ k_fft_pass(const C* __restrict__ in, C* __restrict__ out, int64_t outer, int64_t
   io.N2e = ea.N2 > 0 ? ea.N2 : 1;
   io.esum = 0.0;
   io.ea = ea;
+  if constexpr (EN) {
+    const int64_t k1 = io.k1_base + io.line_i / io.N2e;
+    const double a1 = (double)(k1 - io.N1e / 2);
+    const double a2 = ea.real_half ? (double)(io.line_i % io.N2e) : (double)(io.line_i % io.N2e - io.N2e / 2);
+    io.n12 = a1 * a1 + a2 * a2;
+    io.g12 = exp(-ea.e_a * io.n12);
+  }
   run_stages<LOGN, TI, CONTIG, EN, 0>(smem, col, tj, tw, io);
   if constexpr (EN) {   // CTA partial of Eq. 12's sum, fixed order (deterministic)
     __shared__ double red[32];
@@ -519,17 +537,17 @@ __global__ void __launch_bounds__(32 * CW) k_fft1024_strided(const cplx* __restr
       const int i1 = (int)(ea.k1_base + ic / N2e - ea.N1 / 2);
       const int i2 = ea.real_half ? (int)(ic % N2e) : (int)(ic % N2e - N2e / 2);
       const double b1 = (double)i1, b2 = (double)i2;
+      const double n12 = b1 * b1 + b2 * b2, g12 = exp(-ea.e_a * n12);
 #pragma unroll
       for (int k2 = 0; k2 < 32; ++k2) {
         const int q = k1 + 32 * k2;
         const bool lo = q < N / 2, hi = q >= n - N / 2;
         if (lo || hi) {
           const int k = lo ? q + N / 2 : q - (n - N / 2);
-          const double sc = inv_c[k];
-          const double re = v[k2].x * sc, im = v[k2].y * sc, b0 = (double)(k - N / 2);
-          const double nn = b0 * b0 + b1 * b1 + b2 * b2;
+          const double re = v[k2].x, im = v[k2].y, b0 = (double)(k - N / 2);
+          const double nn = b0 * b0 + n12;
           const double mult = ea.real_half ? half_mult(k - N / 2, i1, i2, ea) : 1.0;
-          if (nn > 0.0 && mult > 0.0) esum += mult * exp(-ea.e_a * nn) / nn * (re * re + im * im);
+          if (nn > 0.0 && mult > 0.0) esum += mult * ea.w0[k] * g12 / nn * (re * re + im * im);
         }
       }
     }
@@ -868,8 +886,13 @@ static int64_t launch_energy_n(Plan* p, const cplx* in, int64_t inner, int N0, c
 }
 
 static int64_t energy_x_pass(Plan* p, const double* in, int64_t inner, int N0, const double* inv_c0,
-                             const EnergyArgs& ea, int a_lo, int a_len) {
+                             const EnergyArgs& ea_in, int a_lo, int a_len) {
   const cplx* ci = reinterpret_cast<const cplx*>(in);
+  EnergyArgs ea = ea_in;
+  ea.w0 = p->e_w0;
+  k_energy_w0<<<(unsigned)((N0 + 255) / 256), 256, 0, p->stream>>>(p->e_w0, inv_c0, N0, ea.e_a);
+  p->launches++;
+  if (check_launch(p, "energy weight table")) return -1;
   switch (p->logn[0]) {
     case 2: return launch_energy_n<2>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
     case 3: return launch_energy_n<3>(p, ci, inner, N0, inv_c0, ea, a_lo, a_len);
