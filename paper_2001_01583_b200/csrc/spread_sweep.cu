@@ -57,9 +57,6 @@ constexpr int kBinW = 8;
 #define HPNFFT_P_B1 8
 #define HPNFFT_P_B2 8
 #endif        // c2 bin width of the sort keys (sort.cu)
-#ifndef HPNFFT_SWEEP_NS
-#define HPNFFT_SWEEP_NS 3
-#endif
 #ifndef HPNFFT_SWEEP_NTSKIP
 #define HPNFFT_SWEEP_NTSKIP 0   // skip n-tiles no record of a k-step reaches (measured: DESIGN.md)
 #endif
@@ -118,7 +115,32 @@ struct Chunk {
   static_assert(CH + 2 * M_ - 1 <= 16, "chunk must fit the 16-row cyclic accumulator");
 };
 
-template <int P1, int P2, int M_>
+// Ring stages and list warps per sweep mode (measured): the list warp is the
+// bottleneck of the one-chunk adjoint sweep with one list warp (consumers idle waiting for lists),
+// so the dense adjoint and the inverse gather run three (one per ring stage), the merged-chunk
+// (sparse) adjoint four stages with two.
+#ifndef HPNFFT_SWEEP_NS
+#define HPNFFT_SWEEP_NS 3
+#endif
+#ifndef HPNFFT_SWEEP_LISTW
+#define HPNFFT_SWEEP_LISTW 3
+#endif
+#ifndef HPNFFT_SWEEP_NS_SPARSE
+#define HPNFFT_SWEEP_NS_SPARSE 4
+#endif
+#ifndef HPNFFT_SWEEP_LISTW_SPARSE
+#define HPNFFT_SWEEP_LISTW_SPARSE 2
+#endif
+#ifndef HPNFFT_SWEEP_NS_INV
+#define HPNFFT_SWEEP_NS_INV 3
+#endif
+#ifndef HPNFFT_SWEEP_LISTW_INV
+#define HPNFFT_SWEEP_LISTW_INV 3
+#endif
+enum SweepMode { kDense = 0, kSparse = 1, kInverse = 2 };
+__host__ __device__ constexpr int sweep_mode(bool inv, bool merge) { return inv ? kInverse : (merge ? kSparse : kDense); }
+
+template <int P1, int P2, int M_, int MODE = kDense>
 struct SweepCfg {
   static constexpr int W = 2 * M_;                         // taps per dimension
   static constexpr int NL = (P1 / kWR) * (P2 / kWC);       // 4 x 4 sub-patches (= record lists)
@@ -128,13 +150,12 @@ struct SweepCfg {
   static constexpr int SUB = HPNFFT_SWEEP_SUB;             // sub-patches per consumer warp
   static_assert(NL % SUB == 0, "whole sub-patches per warp");
   static constexpr int NW = NL / SUB;                      // consumer warps
-  static constexpr int NS = HPNFFT_SWEEP_NS;               // ring stages
+  static constexpr int NS = MODE == kSparse ? HPNFFT_SWEEP_NS_SPARSE
+                           : MODE == kInverse ? HPNFFT_SWEEP_NS_INV : HPNFFT_SWEEP_NS;   // ring stages
   // list warps: warp i owns ring stages i, i + kListWarps, ... (so that it waits on every phase of
   // its stages' barriers in order; a parity wait must never skip a phase)
-#ifndef HPNFFT_SWEEP_LISTW
-#define HPNFFT_SWEEP_LISTW 1
-#endif
-  static constexpr int kListWarps = HPNFFT_SWEEP_LISTW;
+  static constexpr int kListWarps = MODE == kSparse ? HPNFFT_SWEEP_LISTW_SPARSE
+                                    : MODE == kInverse ? HPNFFT_SWEEP_LISTW_INV : HPNFFT_SWEEP_LISTW;
   static_assert(NS % kListWarps == 0, "a list warp owns whole ring stages");
   static constexpr int kThreads = (NW + 1 + kListWarps) * 32;   // + copy warp + list warps
   static constexpr int kRows = P1 + W - 1;                 // candidate c1 rows
@@ -358,9 +379,9 @@ __host__ __device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 
 // chunks are empty and the producer would otherwise wait one global-load latency per chunk
 constexpr int kBinPrefetch = 8;
 
-template <int P1, int P2, int M_>
+template <int P1, int P2, int M_, int MODE>
 __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap, bool merge) {
-  using C = SweepCfg<P1, P2, M_>;
+  using C = SweepCfg<P1, P2, M_, MODE>;
   return sizeof(double) * ((size_t)C::NS * cap * Rec<2 * M_>::kDoubles + Rec<2 * M_>::kDoubles) +
          (sizeof(uint64_t) * 3 + sizeof(BatchHdr)) * C::NS + sizeof(uint32_t) * (size_t)C::NS * C::NL * (list_cap(cap, merge) + 1) +
          sizeof(uint32_t) * kBinPrefetch * 32 * 4 + 32;
@@ -372,9 +393,9 @@ __host__ __device__ constexpr size_t sweep_smem_bytes_of(int cap, bool merge) {
 // [n0][n1][n2] (doubles; the R2C z pass reads it as n2/2 complex per line): an n-tile is then 8
 // real columns = 2 rows x 4 columns of the 4 x 4 sub-patch, half the DMMAs of the complex sweep.
 template <int P1, int P2, int M_, bool INV, bool MERGE, bool REAL = false>
-__global__ void __launch_bounds__(SweepCfg<P1, P2, M_>::kThreads) __maxnreg__((SweepCfg<P1, P2, M_>::kMaxRegs))
-    k_spread_sweep(SweepParams prm) {
-  using C = SweepCfg<P1, P2, M_>;
+__global__ void __launch_bounds__(SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>::kThreads)
+    __maxnreg__((SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>::kMaxRegs)) k_spread_sweep(SweepParams prm) {
+  using C = SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>;
   using R = Rec<2 * M_>;
   constexpr int W = C::W, NW = C::NW, NS = C::NS, NL = C::NL, SUB = C::SUB;
   constexpr int RD = R::kDoubles;
@@ -1401,9 +1422,12 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
     const char* e = getenv("HPNFFT_SWEEP_CAP");
     return e ? atoi(e) : 480;
   }();
-  while (cap + 32 <= 511 && cap + 32 <= cap_max && sweep_smem_bytes_of<P1, P2, M_>(cap + 32, merge) <= smem_max)
-    cap += 32;
-  const size_t smem = sweep_smem_bytes_of<P1, P2, M_>(cap, merge);
+  constexpr int kModeA = INV ? kInverse : kDense;   // the non-merged instantiation's mode
+  auto smem_of = [&](int c) {
+    return merge ? sweep_smem_bytes_of<P1, P2, M_, kSparse>(c, true) : sweep_smem_bytes_of<P1, P2, M_, kModeA>(c, false);
+  };
+  while (cap + 32 <= 511 && cap + 32 <= cap_max && smem_of(cap + 32) <= smem_max) cap += 32;
+  const size_t smem = smem_of(cap);
   SweepParams prm;
   prm.rec = p->rec;
   prm.start = p->bin_count;
@@ -1453,7 +1477,8 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   const int sms = device_sm_count();
   const int64_t slots = (int64_t)sms * C::kCtasPerSm;
   const int64_t blocks = tiles < slots ? tiles : slots;
-  kern<<<(unsigned)blocks, C::kThreads, smem, p->stream>>>(prm);
+  const int threads = merge ? SweepCfg<P1, P2, M_, kSparse>::kThreads : SweepCfg<P1, P2, M_, kModeA>::kThreads;
+  kern<<<(unsigned)blocks, threads, smem, p->stream>>>(prm);
   p->launches++;
   if (prof) {
     unsigned long long h[16];
