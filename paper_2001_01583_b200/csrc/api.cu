@@ -309,11 +309,12 @@ static int create_plan(hpnfft_plan_t* out, int d, const int64_t* N, int64_t M, i
   p->stream = reinterpret_cast<cudaStream_t>(stream);
   int s2 = 0;
   while ((1 << (s2 + 1)) <= 8 && (int64_t(1) << (s2 + 1)) <= n[2]) ++s2;
-  p->nbins = n[1] * (n[2] >> s2) * n[0];
   // plane chunk of the sweep: CH planes of cells touch CH + 2m - 1 <= 16 node planes (the DMMA
   // accumulator's cyclic window), see spread_sweep.cu
   p->chunk_log = m <= 6 ? 2 : (m == 7 ? 1 : 0);
-  if (p->chunk_log > p->logn[0]) p->chunk_log = p->logn[0];   // n0 < CH (d < 3: n0 = 1): keys stay < nbins
+  if (p->chunk_log > p->logn[0]) p->chunk_log = p->logn[0];   // n0 < CH (d < 3: n0 = 1)
+  // one bin per (plane chunk, c1 row, c2 bin) (sort.cu)
+  p->nbins = n[1] * (n[2] >> s2) * (n[0] >> p->chunk_log);
   int rc = HPNFFT_OK;
   // complex grid and z-pass buffer: complex128, or complex64 for an FP32 plan
   const size_t cdoubles = precision == HPNFFT_PRECISION_F32 ? 1 : 2;

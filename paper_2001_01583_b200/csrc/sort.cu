@@ -4,10 +4,12 @@
 // PAPER.md:162-164); the B200 design sorts the points once so the spread kernel can sweep
 // the grid with register/tensor-core resident windows.
 //   u_t = n_t x_t (exact for power-of-two n_t), c_t = floor(u_t) mod n_t  (integer cell)
-//   key = (((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc | (c0 & (CH - 1)),
+//   key = ((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2),
 //   CH = 2^lc planes per chunk, nb2 = n2 >> s2, s2 = log2(min(8, n2))
 // so the points of one plane chunk and one c1 row are contiguous across consecutive c2 bins:
-// a sweep CTA fetches the records of its (chunk, row) with one bulk copy.
+// a sweep CTA fetches the records of its (chunk, row) with one bulk copy.  The cell plane inside
+// the chunk (c0 mod CH) is not part of the key: the sweep applies a chunk's records in any order
+// (round 1 kept it in the key, four times the bins to zero and scan: 0.46 ms at n = 1024^3).
 // Counting sort: histogram with arrival ranks (atomicAdd) -> exclusive scan -> scatter.
 // The order inside a bin is the atomic arrival order (not deterministic; Q21).
 #include <stdlib.h>
@@ -52,7 +54,7 @@ __device__ __forceinline__ uint32_t point_key(const T* __restrict__ x, int64_t j
   int64_t c1 = (int64_t)floor(__dmul_rn((double)n1, x1)) & (n1 - 1);
   int64_t c2 = (int64_t)floor(__dmul_rn((double)n2, x2)) & (n2 - 1);
   int64_t nb2 = n2 >> s2;
-  uint32_t k = (uint32_t)(((((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2)) << lc) | (c0 & ((1 << lc) - 1)));
+  uint32_t k = (uint32_t)(((c0 >> lc) * n1 + c1) * nb2 + (c2 >> s2));
   if (k < k_lo || k >= k_hi) {   // grid-slab plan: the point is outside this rank's planes
     *err = 2;
     k = k_lo;
@@ -441,7 +443,7 @@ void key_range(const Plan* p, uint32_t& k_lo, uint32_t& k_hi) {
   k_lo = 0;
   k_hi = (uint32_t)p->nbins;
   if (p->dist_mode == HPNFFT_DIST_GRID_SLAB && p->nranks > 1) {
-    const int64_t n0 = p->n[0], lc = p->chunk_log, per_chunk = (p->n[1] * (p->n[2] >> s2)) << lc;
+    const int64_t n0 = p->n[0], lc = p->chunk_log, per_chunk = p->n[1] * (p->n[2] >> s2);
     const int64_t c0a = ((p->slab_lo + n0 / 2) % n0);   // first memory plane of the slab
     k_lo = (uint32_t)((c0a >> lc) * per_chunk);
     k_hi = (uint32_t)(((c0a + p->slab_len) >> lc) * per_chunk);
@@ -475,12 +477,12 @@ static int sort_points_t(Plan* p, const T* x) {
   key_range(p, k_lo, k_hi);
   const int lc = p->chunk_log;
   const int64_t C = p->n[0] >> lc;   // plane chunks = level-1 buckets
-  int fine_bits = lc;
-  while ((int64_t(1) << (fine_bits - lc)) < p->n[1] * (p->n[2] >> s2)) ++fine_bits;
+  int fine_bits = 0;   // key bits below the chunk
+  while ((int64_t(1) << fine_bits) < p->n[1] * (p->n[2] >> s2)) ++fine_bits;
   const char* e2 = getenv("HPNFFT_SORT2");
   bool two = M >= (int64_t(1) << 25);
   if (e2) two = e2[0] == '1';
-  two = two && M > 0 && C <= kMaxChunks && (int64_t(1) << fine_bits) == p->n[1] * (p->n[2] >> s2) << lc;
+  two = two && M > 0 && C <= kMaxChunks && (int64_t(1) << fine_bits) == p->n[1] * (p->n[2] >> s2);
   const int64_t hist_n = C * kSortBlocks + 1;
   if (two && sort2_workspace(p, hist_n) != HPNFFT_OK) two = false;   // out of memory: one level
   HPNFFT_CUDA_TRY(p, cudaMemsetAsync(p->bin_count + k_lo, 0, sizeof(uint32_t) * ((size_t)(k_hi - k_lo) + 1), p->stream),

@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(kBoxThreads) k_spread_box_f32(
     for (int r = warp; r < nranges; r += kBoxWarps) {
       const int ch = Z0 / CH + r / BY, row = Y0 + r % BY;
       const size_t rowbase = ((size_t)ch * n1 + row) * nb2;
-      const uint32_t beg = __ldg(start + ((rowbase + (X0 >> s2)) << lc));
-      const uint32_t end = __ldg(start + ((rowbase + ((X0 + BX - 1) >> s2) + 1) << lc));
+      const uint32_t beg = __ldg(start + (rowbase + (X0 >> s2)));
+      const uint32_t end = __ldg(start + (rowbase + ((X0 + BX - 1) >> s2) + 1));
       for (uint32_t j = beg; j < end; ++j) {   // one warp per point
         const CellT a0 = cell_of(xs[3 * (size_t)j], n0), a1 = cell_of(xs[3 * (size_t)j + 1], n1),
                     a2 = cell_of(xs[3 * (size_t)j + 2], n2);

@@ -400,7 +400,6 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>::
   constexpr int W = C::W, NW = C::NW, NS = C::NS, NL = C::NL, SUB = C::SUB;
   constexpr int RD = R::kDoubles;
   constexpr int CH = Chunk<M_>::CH;
-  constexpr int LC = Chunk<M_>::LOG;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int cap = prm.cap;
@@ -500,11 +499,11 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>::
           if (ci < nch && r < C::kRows) {
             const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
             const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
-            cp_async4(d + 0, prm.start + ((rowbase + ra0) << LC));
-            cp_async4(d + 1, prm.start + ((rowbase + rb0 + 1) << LC));
+            cp_async4(d + 0, prm.start + (rowbase + ra0));
+            cp_async4(d + 1, prm.start + (rowbase + rb0 + 1));
             if (rb1 >= ra1) {
-              cp_async4(d + 2, prm.start + ((rowbase + ra1) << LC));
-              cp_async4(d + 3, prm.start + ((rowbase + rb1 + 1) << LC));
+              cp_async4(d + 2, prm.start + (rowbase + ra1));
+              cp_async4(d + 3, prm.start + (rowbase + rb1 + 1));
             } else {
               d[2] = d[3] = 0u;
             }
@@ -1234,7 +1233,6 @@ template <int P1, int P2, int M_>
 __global__ void __launch_bounds__(256) k_tile_counts(SweepParams prm, int ntiles, unsigned long long* keys) {
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
-  constexpr int LC = Chunk<M_>::LOG;
   const int lane = threadIdx.x & 31;
   const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (t >= ntiles) return;
@@ -1271,8 +1269,8 @@ __global__ void __launch_bounds__(256) k_tile_counts(SweepParams prm, int ntiles
       const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
       auto run = [&](int ra, int rb) {
         if (rb < ra) return;
-        const uint32_t lo = max(__ldg(prm.start + ((rowbase + ra) << LC)), prm.g0);
-        const uint32_t hi = min(__ldg(prm.start + ((rowbase + rb + 1) << LC)), prm.g1);
+        const uint32_t lo = max(__ldg(prm.start + (rowbase + ra)), prm.g0);
+        const uint32_t hi = min(__ldg(prm.start + (rowbase + rb + 1)), prm.g1);
         cnt += hi > lo ? hi - lo : 0u;
       };
       run(ra0, rb0);
@@ -1533,7 +1531,7 @@ int run_sweep(Plan* p, const double* f) {
       if (rc) return rc;
     }
     if (multi) {
-      const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1] * Chunk<M_>::CH;
+      const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1];
       uint32_t k_lo, k_hi;
       key_range(p, k_lo, k_hi);
       k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
@@ -1584,7 +1582,7 @@ int run_interp_sweep(Plan* p, double* fout) {
       if (rc) return rc;
     }
     if (multi) {
-      const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1] * Chunk<M_>::CH;
+      const int64_t bins_per_chunk = (p->n[2] / kBinW) * p->n[1];
       uint32_t k_lo, k_hi;
       key_range(p, k_lo, k_hi);
       k_group_chunks<<<1, 32, 0, p->stream>>>(p->bin_count, k_lo, k_hi, g0, g1, bins_per_chunk, p->group_rows);
