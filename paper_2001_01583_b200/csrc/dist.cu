@@ -257,10 +257,14 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 // every rank writes `epoch` into its slot of every rank's flags, then waits for all slots of its
 // own flags; gives up after 5 s (sets *err) instead of hanging the GPU
-__global__ void k_xbarrier(uint32_t* const* peer_flags, int P, int r, uint32_t epoch, int* err) {
+__global__ void k_xbarrier(uint32_t* const* peer_flags, int P, int r, uint32_t epoch, int* err, int fault) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
   for (int s = 0; s < P; ++s) st_release_sys(peer_flags[s] + r, epoch);
+  if (fault) {   // fault injection (tests): behave as if the wait had timed out
+    *err = 1;
+    return;
+  }
   const uint32_t* mine = peer_flags[r];
   const uint64_t t0 = globaltimer();
   for (int s = 0; s < P; ++s) {
@@ -296,7 +300,12 @@ __global__ void k_halo_pull(double2* __restrict__ grid, const double2* __restric
 int xbarrier(Plan* p) {
   if (p->virt) return HPNFFT_OK;   // one-GPU rank group: stream order is the barrier
   ++p->epoch;
-  k_xbarrier<<<1, 32, 0, p->stream>>>(p->peer_flags, p->nranks, p->dist_rank, p->epoch, p->dist_err);
+  // HPNFFT_XBARRIER_FAULT=1 (read per call; tools/dist_check.py): this rank's barriers report a
+  // timeout after releasing their own flags, to exercise the error path (skipped peer traffic,
+  // NaN output, HPNFFT_E_NCCL from the next call)
+  const char* fe = getenv("HPNFFT_XBARRIER_FAULT");
+  const int fault = fe && fe[0] == '1';
+  k_xbarrier<<<1, 32, 0, p->stream>>>(p->peer_flags, p->nranks, p->dist_rank, p->epoch, p->dist_err, fault);
   p->launches++;
   return check_launch(p, "cross-GPU barrier");
 }
@@ -368,11 +377,27 @@ int slab_phase_x(Plan* p, double* fhat) {
 
 namespace {
 
+// a cross-GPU barrier of this transform timed out (*err set by k_xbarrier): the phases after it
+// skipped their peer traffic, so the rank's output is filled with NaN instead of being left
+// plausible-looking (the plan's next call returns HPNFFT_E_NCCL)
+__global__ void k_poison_on_err(double* __restrict__ a, int64_t n, const int* __restrict__ err) {
+  if (*err == 0) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = nan;
+}
+
 int slab_adjoint_p2p(Plan* p, double* fhat) {
   int rc = slab_phase_halo(p);
   if (!rc) rc = slab_phase_z(p);
   if (!rc) rc = slab_phase_y(p);
   if (!rc) rc = slab_phase_x(p, fhat);
+  if (!rc && fhat && p->dist_err && !p->virt) {
+    const int64_t n = 2 * p->N[0] * (p->N[1] / p->nranks) * p->N[2];   // this rank's k1 slab of fhat
+    k_poison_on_err<<<(unsigned)(device_sm_count() * 4), 256, 0, p->stream>>>(fhat, n, p->dist_err);
+    p->launches++;
+    rc = check_launch(p, "barrier error poison");
+  }
   return rc;
 }
 

@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kThreads) k_charges(const double* __restrict__
 // U = sum(e partials) / (2 pi L) - alpha / sqrt(pi) sum(q^2 partials), one CTA, fixed order
 __global__ void __launch_bounds__(kThreads) k_energy_final(const double* __restrict__ e_partial, int64_t ne,
                                                             const double* __restrict__ q2_partial, int nq,
-                                                            double inv_2pi_l, double self_c, double* __restrict__ U) {
+                                                            double inv_2pi_l, double self_c, double* __restrict__ U,
+                                                            const int* __restrict__ dist_err) {
   __shared__ double se[kThreads], sq[kThreads];
   double a = 0.0, b = 0.0;
   for (int64_t i = threadIdx.x; i < ne; i += kThreads) a += e_partial[i];
@@ -58,7 +59,9 @@ __global__ void __launch_bounds__(kThreads) k_energy_final(const double* __restr
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *U = se[0] * inv_2pi_l - self_c * sq[0];
+  // a timed-out cross-GPU barrier (grid slab): NaN instead of a plausible wrong energy
+  const bool bad = dist_err && *dist_err != 0;
+  if (threadIdx.x == 0) *U = bad ? __longlong_as_double(0x7ff8000000000000ll) : se[0] * inv_2pi_l - self_c * sq[0];
 }
 
 }  // namespace
@@ -138,7 +141,8 @@ extern "C" int hpnfft_ewald_reciprocal(hpnfft_plan_t h, const double* q, double 
   p->energy = false;
   if (rc) return rc;
   k_energy_final<<<1, kThreads, 0, p->stream>>>(p->e_partial, p->e_nparts, q2_partial, kChargeBlocks,
-                                                 1.0 / (2.0 * pi * L), alpha / std::sqrt(pi), U);
+                                                 1.0 / (2.0 * pi * L), alpha / std::sqrt(pi), U,
+                                                 p->virt ? nullptr : p->dist_err);
   p->launches++;
   rc = check_launch(p, "energy final sum");
   if (rc) return rc;

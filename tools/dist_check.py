@@ -110,6 +110,41 @@ def main():
                 ok &= ee <= 1e-12
         dp.close()
         dist.barrier()
+    # barrier fault injection (grid slab over peer memory): the last rank's cross-GPU barriers
+    # report a timeout; that rank's fhat must come back NaN and its next call must fail
+    # (HPNFFT_E_NCCL), the other ranks must still match the single-GPU result
+    os.environ.pop("HPNFFT_DIST_P2P", None)
+    x = idev.uniform_points(M, device=dev)
+    f = idev.uniform_values(M, device=dev)
+    mask = grid_slab_mask(x, rank, world, 2 * N[0], None)
+    xl, fl = x[mask].contiguous(), f[mask].contiguous()
+    dp = DistPlan(N, xl.shape[0], mode="grid_slab", device=dev)
+    if dp.plan.info()["exchange_path"] == "grid_slab_nvlink_p2p":
+        dp.set_points(xl)
+        faulty = rank == world - 1
+        if faulty:
+            os.environ["HPNFFT_XBARRIER_FAULT"] = "1"
+        out = dp.adjoint(fl)
+        torch.cuda.synchronize()
+        os.environ.pop("HPNFFT_XBARRIER_FAULT", None)
+        if faulty:
+            all_nan = bool(torch.isnan(out).all().item())
+            try:
+                dp.set_points(xl)
+                failed_next = False
+            except Exception as exc:   # noqa: BLE001 - the binding raises on HPNFFT_E_NCCL
+                failed_next = "NCCL" in str(exc) or "barrier" in str(exc)
+            good = all_nan and failed_next
+        else:
+            good = not bool(torch.isnan(out).any().item())
+        fl_ok = torch.tensor([1 if good else 0], device=dev)
+        dist.all_reduce(fl_ok, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"[barrier fault on rank {world - 1}] faulty rank: NaN output + failing next call; others finite: "
+                  f"{bool(fl_ok.item())}", flush=True)
+            ok &= bool(fl_ok.item())
+    dp.close()
+    dist.barrier()
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
