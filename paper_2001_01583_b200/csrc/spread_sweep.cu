@@ -497,7 +497,9 @@ __global__ void __launch_bounds__(SweepCfg<P1, P2, M_, sweep_mode(INV, MERGE)>::
         auto prefetch = [&](int ci) {
           uint32_t* d = s_pf + ((ci % kBinPrefetch) * 32 + lane) * 4;
           if (ci < nch && r < C::kRows) {
-            const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
+            int a = a_lo + ci;   // chunk index mod nchunks0 (no integer division on the producer's path)
+            while (a < 0) a += nchunks0;
+            while (a >= nchunks0) a -= nchunks0;
             const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
             cp_async4(d + 0, prm.start + (rowbase + ra0));
             cp_async4(d + 1, prm.start + (rowbase + rb0 + 1));
@@ -1265,7 +1267,9 @@ __global__ void __launch_bounds__(256) k_tile_counts(SweepParams prm, int ntiles
   if (row < P1) {
 #pragma unroll 4
     for (int ci = 2 * phase; ci < nch; ci += 8) {
-      const int a = ((a_lo + ci) % nchunks0 + nchunks0) % nchunks0;
+      int a = a_lo + ci;
+      while (a < 0) a += nchunks0;
+      while (a >= nchunks0) a -= nchunks0;
       const size_t rowbase = ((size_t)a * n1 + c1) * prm.nb2;
       auto run = [&](int ra, int rb) {
         if (rb < ra) return;
