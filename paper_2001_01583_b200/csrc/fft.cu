@@ -103,6 +103,19 @@ struct EnergyArgs {
   const double* w0;
 };
 
+// a / nn of one Eq. 12 term; HPNFFT_ENERGY_RCP=1: times the correctly rounded reciprocal (no
+// division subroutine; within an ulp of the quotient)
+#ifndef HPNFFT_ENERGY_RCP
+#define HPNFFT_ENERGY_RCP 1
+#endif
+__device__ __forceinline__ double energy_term(double a, double nn) {
+#if HPNFFT_ENERGY_RCP
+  return a * __drcp_rn(nn);
+#else
+  return a / nn;
+#endif
+}
+
 __global__ void k_energy_w0(double* __restrict__ w0, const double* __restrict__ inv_c, int N, double e_a) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= N) return;
@@ -241,7 +254,7 @@ __device__ __forceinline__ void stockham_stage(C* buf, int col, int tj, const C*
           const double a0 = (double)i0;
           const double nn = a0 * a0 + io.n12;
           const double mult = io.ea.real_half ? half_mult(i0, i1, i2, io.ea) : 1.0;
-          if (nn > 0.0 && mult > 0.0) io.esum += mult * io.ea.w0[k] * io.g12 / nn * (re * re + im * im);
+          if (nn > 0.0 && mult > 0.0) io.esum += energy_term(mult * io.ea.w0[k] * (re * re + im * im), nn);
         }
       } else if (OUT_G && io.inv) {
         if (io.valid) io.gout[(int64_t)q * io.ostride] = {v[b][r].x, -v[b][r].y};
@@ -347,7 +360,7 @@ k_fft_pass(const C* __restrict__ in, C* __restrict__ out, int64_t outer, int64_t
   run_stages<LOGN, TI, CONTIG, EN, 0>(smem, col, tj, tw, io);
   if constexpr (EN) {   // CTA partial of Eq. 12's sum, fixed order (deterministic)
     __shared__ double red[32];
-    double v = io.esum;
+    double v = io.esum * io.g12;   // the line's Gaussian factor, once
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((tid & 31) == 0) red[tid >> 5] = v;
@@ -547,9 +560,10 @@ __global__ void __launch_bounds__(32 * CW) k_fft1024_strided(const cplx* __restr
           const double re = v[k2].x, im = v[k2].y, b0 = (double)(k - N / 2);
           const double nn = b0 * b0 + n12;
           const double mult = ea.real_half ? half_mult(k - N / 2, i1, i2, ea) : 1.0;
-          if (nn > 0.0 && mult > 0.0) esum += mult * ea.w0[k] * g12 / nn * (re * re + im * im);
+          if (nn > 0.0 && mult > 0.0) esum += energy_term(mult * ea.w0[k] * (re * re + im * im), nn);
         }
       }
+      esum *= g12;   // the line's Gaussian factor, once
     }
     __shared__ double red[32];
 #pragma unroll
