@@ -1410,14 +1410,18 @@ int launch_sweep_group(Plan* p, uint32_t g0, uint32_t g1, const int* chunks, boo
   using C = SweepCfg<P1, P2, M_>;
   constexpr int CH = Chunk<M_>::CH;
   const size_t smem_max = C::kCtasPerSm == 1 ? (size_t)(227 * 1024) : (size_t)(113 * 1024);
-  // multi-chunk batches when a (tile, chunk) holds few records on average (sparse points: one
-  // pipeline round trip per chunk would dominate); HPNFFT_SWEEP_MERGE=0/1 forces the choice
+  // multi-chunk batches when a (tile, chunk) holds few records on average (sparse REAL points:
+  // one pipeline round trip per chunk would dominate); HPNFFT_SWEEP_MERGE=0/1 forces the choice
   constexpr int W = 2 * M_;
   // (points per cell of the planes this plan spreads: a grid-slab rank's slab, occupied planes)
   const double planes = (double)(p->plane_len > 0 ? p->plane_len : p->n[0]);
   const double dens = (double)p->M / (planes * (double)p->n[1] * (double)p->n[2]);
   const double per_chunk = dens * (P1 + W - 1) * (P2 + W - 1) * CH;
-  bool merge = !INV && C::SUB == 1 && per_chunk < 64.0;
+  // measured (tools/merge_threshold.py, tools/enuf_bench.py): with one list warp per stage the
+  // one-chunk kernel wins for complex values at every density down to ~1 record per (tile,
+  // chunk); the merged kernel still wins for the REAL sweep of the ENUF charges (half the DMMA
+  // work per record, so the per-chunk round trip dominates)
+  bool merge = !INV && C::SUB == 1 && REAL && per_chunk < 64.0;
   if (const char* e = getenv("HPNFFT_SWEEP_MERGE")) merge = !INV && C::SUB == 1 && e[0] == '1';
   int cap = 32;
   static const int cap_max = [] {   // HPNFFT_SWEEP_CAP: smaller ring stages (measurement)
