@@ -360,7 +360,10 @@ __device__ __forceinline__ void dmma16(double (&c)[4], double a0, double a1, dou
 // A batch holds the records of one chunk or, at low point density, of up to kMaxSeg chunks
 // (segments; records in chunk order), so that sparse inputs do not pay one pipeline round trip
 // per chunk of a handful of records.
-constexpr int kMaxSeg = 8;
+#ifndef HPNFFT_MAX_SEG
+#define HPNFFT_MAX_SEG 16
+#endif
+constexpr int kMaxSeg = HPNFFT_MAX_SEG;
 struct BatchHdr {
   int B;      // records in the batch; -1 terminates
   int tile;   // tile id
